@@ -1,0 +1,197 @@
+/*
+ * hccx.h -- C ABI of the B200-native compressed-collective engine.
+ *
+ * This is the drop-in boundary for the reference's hot path
+ * (arxiv/paper_2409_02423, "hybridcomm", /root/reference/proj).  The
+ * reference has no C ABI: its interface is the C++ header API quoted beside
+ * each entry point below.  The C++ host mirror of that API (namespace hcc,
+ * include/hcc/*.hpp, paper_2409_02423_b200/host/) is a thin shim over these
+ * functions, and INTEGRATION.md shows the ctypes/extern "C" bindings.
+ *
+ * Conventions
+ *   - Plain pointers and sizes only.  Pointers named d_* are device memory on
+ *     the current (or stated) CUDA device; h_* are host memory.  Caller owns
+ *     all memory.  Streams are cudaStream_t passed as void* (NULL = legacy
+ *     default stream).
+ *   - Every function returns an hccx_status_t.  Codes map 1:1 onto the
+ *     reference's exception hierarchy (proj/include/hcc/errors.hpp:15-60);
+ *     HCCX_ERR_CUDA / _INVALID_ARGUMENT / _TIMEOUT / _UNSUPPORTED are
+ *     device-side additions.
+ *   - Device entry points are asynchronous on the given stream.  Errors found
+ *     by the kernels (NaN/Inf reaching a lossy codec, a peer timing out) are
+ *     OR-ed into a device flag word; *_status() / hccx_flag_status() read it
+ *     back (synchronising the stream) and map it to a status.
+ *   - Results are bit-identical to the reference CPU path on the same inputs
+ *     (fixed-rate and identity codecs; ring schedule of
+ *     proj/src/collectives.cpp).  The zfp-rate codec (kind 3) is a new codec
+ *     not present in the reference.
+ */
+#ifndef HCCX_H
+#define HCCX_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HCCX_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define HCCX_API __attribute__((visibility("default")))
+#else
+#define HCCX_API
+#endif
+
+typedef enum hccx_status {
+  HCCX_OK = 0,
+  HCCX_ERR_NONFINITE = 1,            /* hcc::NonFiniteInputError    errors.hpp:15-19 */
+  HCCX_ERR_CORRUPT_PAYLOAD = 2,      /* hcc::CorruptPayloadError    errors.hpp:21-25 */
+  HCCX_ERR_DATA_DEPENDENT_SIZE = 3,  /* hcc::DataDependentSizeError errors.hpp:27-31 */
+  HCCX_ERR_BAD_CHUNKING = 4,         /* hcc::BadChunkingError       errors.hpp:33-37 */
+  HCCX_ERR_BAD_LAYOUT = 5,           /* hcc::BadLayoutError         errors.hpp:39-43 */
+  HCCX_ERR_INVALID_SCHEME = 6,       /* hcc::InvalidSchemeError     errors.hpp:45-49 */
+  HCCX_ERR_CONFIG = 7,               /* hcc::ConfigError            errors.hpp:51-60 */
+  HCCX_ERR_CUDA = 8,
+  HCCX_ERR_INVALID_ARGUMENT = 9,
+  HCCX_ERR_TIMEOUT = 10,
+  HCCX_ERR_UNSUPPORTED = 11
+} hccx_status_t;
+
+/* hcc::CodecKind (codec.hpp:16-20) plus the zfp-mode codec. */
+typedef enum hccx_codec_kind {
+  HCCX_CODEC_IDENTITY = 0,
+  HCCX_CODEC_LOSSLESS = 1, /* LosslessPredictor: size law and host codec only */
+  HCCX_CODEC_FIXED_RATE = 2,
+  HCCX_CODEC_ZFP_RATE = 3 /* NOT in the reference: 1-D zfp fixed-rate, 4*rate bits/block */
+} hccx_codec_kind_t;
+
+/* hcc::CodecSpec (codec.hpp:22-32). */
+typedef struct hccx_codec {
+  int32_t kind;      /* hccx_codec_kind_t */
+  int32_t rate_bits; /* fixed-rate: [2,32]; zfp-rate: [3,32]; else 0 */
+} hccx_codec_t;
+
+/* hcc::ReduceMode (collectives.hpp:21). */
+typedef enum hccx_reduce_mode { HCCX_SUM = 0, HCCX_AVERAGE = 1 } hccx_reduce_mode_t;
+
+HCCX_API const char* hccx_status_string(hccx_status_t s);
+HCCX_API int hccx_abi_version(void);
+
+/* Replaces CodecSpec::fixed_rate's range check (src/codec.cpp:11-17):
+ * HCCX_ERR_INVALID_SCHEME when the rate is out of range. */
+HCCX_API hccx_status_t hccx_codec_validate(hccx_codec_t codec);
+
+/* Replaces hcc::wire_size_bytes (codec.hpp:63-67, src/codec.cpp:47-61):
+ * payload bytes for n values; HCCX_ERR_DATA_DEPENDENT_SIZE for lossless. */
+HCCX_API hccx_status_t hccx_wire_size_bytes(hccx_codec_t codec, uint64_t n, uint64_t* bytes);
+
+/* CompressedBuffer::chunk_count (codec.hpp:47): 64-value blocks for
+ * fixed-rate, 4-value blocks for zfp-rate, 0 for identity. */
+HCCX_API hccx_status_t hccx_chunk_count(hccx_codec_t codec, uint64_t n, uint64_t* count);
+
+/* ---------------------------------------------------------------- codec -- */
+
+/* Device compress (replaces hcc::compress, codec.hpp:53-55 /
+ * src/codec_omp.cpp:19-85, for identity / fixed-rate / zfp-rate).
+ * d_out must hold hccx_wire_size_bytes() bytes.  d_err (nullable): device
+ * word OR-ed with 1 when a live value is NaN/Inf (the reference throws
+ * NonFiniteInputError, src/codec_omp.cpp:45); check with hccx_flag_status. */
+HCCX_API hccx_status_t hccx_compress(hccx_codec_t codec, const float* d_in, uint64_t n, uint8_t* d_out,
+                            uint32_t* d_err, void* stream);
+
+/* Device decompress (replaces hcc::decompress, codec.hpp:57-61 /
+ * src/codec_omp.cpp:87-111).  payload_bytes must equal the size law, else
+ * HCCX_ERR_CORRUPT_PAYLOAD (src/codec_omp.cpp:94-96). */
+HCCX_API hccx_status_t hccx_decompress(hccx_codec_t codec, const uint8_t* d_in, uint64_t payload_bytes,
+                              uint64_t n, float* d_out, void* stream);
+
+/* Synchronise `stream`, read the device flag word, clear it, and map it to a
+ * status (HCCX_ERR_NONFINITE / HCCX_ERR_TIMEOUT / HCCX_OK). */
+HCCX_API hccx_status_t hccx_flag_status(uint32_t* d_err, void* stream);
+
+/* Host-buffer codec: the reference's value API (host vector in, host bytes
+ * out) run on `device`, with the host<->device copies pipelined against the
+ * kernels in slices.  Same results and errors as hcc::compress/decompress. */
+HCCX_API hccx_status_t hccx_compress_host(hccx_codec_t codec, const float* h_in, uint64_t n, uint8_t* h_out,
+                                 int device);
+HCCX_API hccx_status_t hccx_decompress_host(hccx_codec_t codec, const uint8_t* h_in, uint64_t payload_bytes,
+                                   uint64_t n, float* h_out, int device);
+
+/* ------------------------------------------- single-device ring (group) -- */
+/* All p members' buffers live on one device ("virtual ranks"): the value
+ * semantics of the reference's all-members-in-one-call collectives
+ * (collectives.hpp:23-25) executed by the same ring kernels.  p in [1,16]. */
+
+typedef struct hccx_group* hccx_group_t;
+
+HCCX_API hccx_status_t hccx_group_create(int p, int device, hccx_group_t* out);
+HCCX_API hccx_status_t hccx_group_destroy(hccx_group_t g);
+
+/* Replaces hcc::allreduce (collectives.hpp:61-64, src/collectives.cpp:202-248).
+ * d_in[j], d_out[j]: member j's n values (d_out[j] may equal d_in[j]).
+ * n % p != 0 -> HCCX_ERR_BAD_CHUNKING.  p == 1 copies the input untouched. */
+HCCX_API hccx_status_t hccx_group_allreduce(hccx_group_t g, const float* const* d_in, float* const* d_out,
+                                   uint64_t n, hccx_codec_t codec, int mode, void* stream);
+/* Replaces hcc::ring_reduce_scatter (collectives.hpp:51-55, src/collectives.cpp:154-181).
+ * d_shard[j] receives member j's n/p reduced values. */
+HCCX_API hccx_status_t hccx_group_reduce_scatter(hccx_group_t g, const float* const* d_in, float* const* d_shard,
+                                        uint64_t n, hccx_codec_t codec, void* stream);
+/* Replaces hcc::ring_allgather (collectives.hpp:57-59, src/collectives.cpp:183-200).
+ * d_out[j] receives p*shard_n values. */
+HCCX_API hccx_status_t hccx_group_allgather(hccx_group_t g, const float* const* d_shard, float* const* d_out,
+                                   uint64_t shard_n, hccx_codec_t codec, void* stream);
+/* Broadcast (NOT in the reference): every member, root
+ * included, receives dec(comp(d_in)). */
+HCCX_API hccx_status_t hccx_group_broadcast(hccx_group_t g, int root, const float* d_in, float* const* d_out,
+                                   uint64_t n, hccx_codec_t codec, void* stream);
+/* Replaces hcc::p2p's value path (collectives.hpp:45-48, src/collectives.cpp:130-152):
+ * d_out = dec(comp(d_in)). */
+HCCX_API hccx_status_t hccx_group_p2p(hccx_group_t g, const float* d_in, float* d_out, uint64_t n,
+                             hccx_codec_t codec, void* stream);
+/* Synchronise and report the group's device error flag (see hccx_flag_status). */
+HCCX_API hccx_status_t hccx_group_status(hccx_group_t g, void* stream);
+
+/* ------------------------------------ multi-process NVLink communicator -- */
+/* One process per GPU.  Each rank allocates a peer-visible window, exports
+ * an opaque handle (HCCX_HANDLE_BYTES), the caller all-gathers the handles
+ * (e.g. torch.distributed), and every rank connects.  Collectives are ONE
+ * persistent kernel per call per rank: compressed chunks are pushed into the
+ * next rank's window over NVLink with per-segment flags, and each hop is a
+ * fused decompress-add-recompress (same bits as the single-device ring). */
+
+#define HCCX_HANDLE_BYTES 256
+
+typedef struct hccx_comm* hccx_comm_t;
+
+/* max_n: largest per-rank buffer (values) any collective will use. */
+HCCX_API hccx_status_t hccx_comm_create(int rank, int nranks, int device, uint64_t max_n, hccx_comm_t* out);
+HCCX_API hccx_status_t hccx_comm_export(hccx_comm_t c, void* handle /* HCCX_HANDLE_BYTES */);
+HCCX_API hccx_status_t hccx_comm_connect(hccx_comm_t c, const void* handles /* nranks*HCCX_HANDLE_BYTES */);
+HCCX_API hccx_status_t hccx_comm_destroy(hccx_comm_t c);
+
+/* Same semantics as the group calls, for this rank's buffer only. */
+HCCX_API hccx_status_t hccx_allreduce(hccx_comm_t c, const float* d_in, float* d_out, uint64_t n,
+                             hccx_codec_t codec, int mode, void* stream);
+HCCX_API hccx_status_t hccx_reduce_scatter(hccx_comm_t c, const float* d_in, float* d_shard, uint64_t n,
+                                  hccx_codec_t codec, void* stream);
+HCCX_API hccx_status_t hccx_allgather(hccx_comm_t c, const float* d_shard, float* d_out, uint64_t shard_n,
+                             hccx_codec_t codec, void* stream);
+HCCX_API hccx_status_t hccx_broadcast(hccx_comm_t c, int root, const float* d_in, float* d_out, uint64_t n,
+                             hccx_codec_t codec, void* stream);
+/* Point-to-point: called by both src and dst (other ranks return at once).
+ * src passes d_in, dst passes d_out = dec(comp(src's d_in)). */
+HCCX_API hccx_status_t hccx_p2p(hccx_comm_t c, int src, int dst, const float* d_in, float* d_out, uint64_t n,
+                       hccx_codec_t codec, void* stream);
+/* Synchronise and report this rank's error flag (non-finite, peer timeout). */
+HCCX_API hccx_status_t hccx_comm_status(hccx_comm_t c, void* stream);
+
+/* Kernel launches issued by this library since it was loaded. */
+HCCX_API uint64_t hccx_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HCCX_H */

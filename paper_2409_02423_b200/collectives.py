@@ -1,0 +1,280 @@
+"""Compressed ring collectives with the reference's all-members-in-one-call API.
+
+Drop-in for proj/include/hcc/collectives.hpp:15-64 (implementation
+proj/src/collectives.cpp): ``inputs[j]`` is the buffer of communicator
+position j and one buffer per member is returned.  Here every member's buffer
+lives on one B200 ("virtual ranks") and the ring runs as the same fused
+kernels the NVLink engine uses (libhccx, hccx_group_*), so the results are
+bit-identical to the reference ring:
+
+  reduce_scatter  position i holds chunk i folded in ring order (i+1 ... i+p),
+                  decompress-add-recompress at every hop (collectives.cpp:27-66)
+  allgather       each shard compressed once, every member (origin included)
+                  keeps the decoded copy (collectives.cpp:69-111)
+  allreduce       RS then AG; Average = IEEE divide by float(p) after the gather
+                  (collectives.cpp:202-248)
+  p2p             dst receives dec(comp(buf)) (collectives.cpp:130-152)
+  broadcast       NOT in the reference: every member, root included, receives
+                  dec(comp(buf))
+
+Byte accounting (TraceEvent raw/wire bytes, round counts) is integer-identical
+to the reference; ``duration_s`` is the measured device time of the call.
+Inputs may be host numpy float32 arrays (copied to the device and back, like
+the reference's value semantics) or CUDA float32 tensors.
+"""
+from __future__ import annotations
+
+import enum
+from dataclasses import dataclass, field
+from typing import Dict, List, Sequence, Tuple
+
+import numpy as np
+
+from .codec import CodecKind, CodecSpec, wire_size_bytes
+from .comm_path import CommPath
+from .errors import BadChunkingError, UnsupportedError, check
+from .netsim import CollectiveKind, SimClock, TraceEvent
+
+
+@dataclass
+class Communicator:
+    """Ordered member list: ring orientation and reduction order (collectives.hpp:15-19)."""
+
+    ranks: List[int] = field(default_factory=list)
+
+    def size(self) -> int:
+        return len(self.ranks)
+
+
+class ReduceMode(enum.IntEnum):
+    Sum = 0
+    Average = 1
+
+
+_GROUPS: Dict[Tuple[int, int], int] = {}
+
+
+def _group(p: int, device: int) -> int:
+    import ctypes as C
+
+    from . import _lib
+
+    key = (p, device)
+    if key not in _GROUPS:
+        h = C.c_void_p()
+        check(_lib.hccx_group_create(p, device, C.byref(h)), "group_create")
+        _GROUPS[key] = h.value
+    return _GROUPS[key]
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+def _is_cuda(x) -> bool:
+    return hasattr(x, "is_cuda") and bool(x.is_cuda)
+
+
+def _as_device(bufs: Sequence) -> Tuple[list, bool, int]:
+    """-> (contiguous CUDA float32 tensors, inputs_were_host, device index)."""
+    torch = _torch()
+    if all(_is_cuda(b) for b in bufs):
+        ts = [b.contiguous().view(-1) for b in bufs]
+        return ts, False, ts[0].device.index if ts else torch.cuda.current_device()
+    dev = torch.cuda.current_device()
+    ts = [torch.from_numpy(np.ascontiguousarray(b, np.float32).reshape(-1)).to(f"cuda:{dev}") for b in bufs]
+    return ts, True, dev
+
+
+def _back(ts: list, host: bool) -> list:
+    if not host:
+        return ts
+    return [t.cpu().numpy() for t in ts]
+
+
+def _message_bytes(spec: CodecSpec, n: int) -> int:
+    if spec.kind == CodecKind.LosslessPredictor:
+        raise UnsupportedError("lossless accounting needs the device predictor size pass (not built yet)")
+    return wire_size_bytes(spec, n)
+
+
+class _Timer:
+    """Device time of one collective on the current stream (CUDA events)."""
+
+    def __init__(self, device: int):
+        torch = _torch()
+        self.stream = torch.cuda.current_stream(device)
+        self.a = torch.cuda.Event(enable_timing=True)
+        self.b = torch.cuda.Event(enable_timing=True)
+
+    def __enter__(self):
+        self.a.record(self.stream)
+        return self
+
+    def __exit__(self, *exc):
+        self.b.record(self.stream)
+
+    def seconds(self) -> float:
+        self.b.synchronize()
+        return self.a.elapsed_time(self.b) / 1e3
+
+
+def _commit(clock: SimClock, comm: Communicator, duration: float, raw_total: int, wire_total: int,
+            rounds: int, path: CommPath, kind: CollectiveKind) -> None:
+    """collectives.cpp:113-126."""
+    clock.sync_to_max(comm.ranks)
+    for r in comm.ranks:
+        clock.advance(r, duration)
+    p = comm.size()
+    clock.record(TraceEvent(0, path, kind, p, raw_total // p, wire_total // p, duration, rounds))
+
+
+def _ptrs(ts: list):
+    from . import _lib
+
+    return _lib.ptr_array([t.data_ptr() for t in ts])
+
+
+def _finish(g: int, stream, what: str) -> None:
+    from . import _lib
+
+    check(_lib.hccx_group_status(g, stream.cuda_stream), what)
+
+
+def ring_reduce_scatter(clock: SimClock, comm: Communicator, inputs: Sequence, spec: CodecSpec,
+                        path: CommPath) -> list:
+    """collectives.cpp:154-181."""
+    from . import _lib
+
+    p = comm.size()
+    assert len(inputs) == p
+    n = len(inputs[0])
+    if n % p != 0:
+        raise BadChunkingError(f"reduce_scatter: length {n} not divisible by {p}")
+    if any(len(b) != n for b in inputs):
+        raise BadChunkingError("reduce_scatter: ragged inputs")
+    if p == 1:
+        return [inputs[0].clone() if _is_cuda(inputs[0]) else np.array(inputs[0], np.float32)]
+    c = n // p
+    msg = _message_bytes(spec, c)
+    torch = _torch()
+    ts, host, dev = _as_device(inputs)
+    shards = [torch.empty(c, dtype=torch.float32, device=ts[0].device) for _ in range(p)]
+    g = _group(p, dev)
+    tin, _k1 = _ptrs(ts)
+    tout, _k2 = _ptrs(shards)
+    with _Timer(dev) as tm:
+        check(_lib.hccx_group_reduce_scatter(g, tin, tout, n, spec.c(), tm.stream.cuda_stream), "reduce_scatter")
+    _finish(g, tm.stream, "reduce_scatter")
+    rounds = p - 1
+    _commit(clock, comm, tm.seconds(), rounds * p * 4 * c, rounds * p * msg, rounds, path,
+            CollectiveKind.ReduceScatter)
+    return _back(shards, host)
+
+
+def ring_allgather(clock: SimClock, comm: Communicator, shards: Sequence, spec: CodecSpec,
+                   path: CommPath) -> list:
+    """collectives.cpp:183-200."""
+    from . import _lib
+
+    p = comm.size()
+    assert len(shards) == p
+    c = len(shards[0])
+    if any(len(s) != c for s in shards):
+        raise BadChunkingError("allgather: mismatched shard lengths")
+    if p == 1:
+        return [shards[0].clone() if _is_cuda(shards[0]) else np.array(shards[0], np.float32)]
+    msg = _message_bytes(spec, c)
+    torch = _torch()
+    ts, host, dev = _as_device(shards)
+    outs = [torch.empty(p * c, dtype=torch.float32, device=ts[0].device) for _ in range(p)]
+    g = _group(p, dev)
+    tin, _k1 = _ptrs(ts)
+    tout, _k2 = _ptrs(outs)
+    with _Timer(dev) as tm:
+        check(_lib.hccx_group_allgather(g, tin, tout, c, spec.c(), tm.stream.cuda_stream), "allgather")
+    _finish(g, tm.stream, "allgather")
+    rounds = p - 1
+    _commit(clock, comm, tm.seconds(), rounds * p * 4 * c, rounds * p * msg, rounds, path,
+            CollectiveKind.AllGather)
+    return _back(outs, host)
+
+
+def allreduce(clock: SimClock, comm: Communicator, inputs: Sequence, spec: CodecSpec, path: CommPath,
+              mode: ReduceMode = ReduceMode.Sum) -> list:
+    """collectives.cpp:202-248."""
+    from . import _lib
+
+    p = comm.size()
+    assert len(inputs) == p
+    n = len(inputs[0])
+    if n % p != 0:
+        raise BadChunkingError(f"allreduce: length {n} not divisible by {p}")
+    if any(len(b) != n for b in inputs):
+        raise BadChunkingError("allreduce: ragged inputs")
+    if p == 1:
+        return [inputs[0].clone() if _is_cuda(inputs[0]) else np.array(inputs[0], np.float32)]
+    c = n // p
+    msg = _message_bytes(spec, c)
+    torch = _torch()
+    ts, host, dev = _as_device(inputs)
+    outs = [torch.empty(n, dtype=torch.float32, device=ts[0].device) for _ in range(p)]
+    g = _group(p, dev)
+    tin, _k1 = _ptrs(ts)
+    tout, _k2 = _ptrs(outs)
+    with _Timer(dev) as tm:
+        check(_lib.hccx_group_allreduce(g, tin, tout, n, spec.c(), int(mode), tm.stream.cuda_stream),
+              "allreduce")
+    _finish(g, tm.stream, "allreduce")
+    rounds = p - 1
+    _commit(clock, comm, tm.seconds(), 2 * rounds * p * 4 * c, 2 * rounds * p * msg, 2 * rounds, path,
+            CollectiveKind.AllReduce)
+    return _back(outs, host)
+
+
+def p2p(clock: SimClock, src: int, dst: int, buf, spec: CodecSpec, path: CommPath):
+    """collectives.cpp:130-152: dst receives dec(comp(buf)); both clocks advance."""
+    from . import _lib
+
+    assert src != dst
+    n = len(buf)
+    msg = _message_bytes(spec, n)
+    torch = _torch()
+    (t,), host, dev = _as_device([buf])
+    out = torch.empty(n, dtype=torch.float32, device=t.device)
+    g = _group(2, dev)
+    with _Timer(dev) as tm:
+        check(_lib.hccx_group_p2p(g, t.data_ptr(), out.data_ptr(), n, spec.c(), tm.stream.cuda_stream), "p2p")
+    _finish(g, tm.stream, "p2p")
+    dur = tm.seconds()
+    clock.sync_to_max([src, dst])
+    clock.advance(src, dur)
+    clock.advance(dst, dur)
+    clock.record(TraceEvent(0, path, CollectiveKind.P2P, 2, 4 * n, msg, dur, 1))
+    return _back([out], host)[0]
+
+
+def broadcast(clock: SimClock, comm: Communicator, root: int, buf, spec: CodecSpec, path: CommPath) -> list:
+    """Broadcast from communicator position ``root`` (not in the reference;
+    defined by analogy with the allgather single-shard rule)."""
+    from . import _lib
+
+    p = comm.size()
+    n = len(buf)
+    if p == 1:
+        return [buf.clone() if _is_cuda(buf) else np.array(buf, np.float32)]
+    msg = _message_bytes(spec, n)
+    torch = _torch()
+    (t,), host, dev = _as_device([buf])
+    outs = [torch.empty(n, dtype=torch.float32, device=t.device) for _ in range(p)]
+    g = _group(p, dev)
+    tout, _k = _ptrs(outs)
+    with _Timer(dev) as tm:
+        check(_lib.hccx_group_broadcast(g, root, t.data_ptr(), tout, n, spec.c(), tm.stream.cuda_stream),
+              "broadcast")
+    _finish(g, tm.stream, "broadcast")
+    rounds = p - 1
+    _commit(clock, comm, tm.seconds(), rounds * 4 * n, rounds * msg, rounds, path, CollectiveKind.Broadcast)
+    return _back(outs, host)

@@ -1,0 +1,303 @@
+// codec_zfp.cuh -- ZFP-mode fixed-rate codec (CodecKind 3, "zfp-rate:N").
+//
+// NOT IN THE REFERENCE.  The north star asks for a ZFP-style transform codec
+// (SURVEY.md §8 row a12); the reference only has the block quantizer.  This
+// is the published 1-D zfp fixed-rate float path: 4-value blocks, a common
+// exponent (frexp of the block max, clamped at -126), block-floating-point
+// cast to 32-bit ints (x * 2^(30-emax), truncated), the forward lifting
+// transform, negabinary conversion and embedded bit-plane coding with group
+// tests, truncated at exactly 4*R bits per block (LSB-first stream).  Partial
+// blocks are padded as zfp's pad_block does.  Parity is UNPINNED: the oracle
+// is the CPU restatement in oracle/hcc_oracle.c (orc_zfp_*), and the device
+// code must match it bit-exactly.
+//
+// Warp mapping: lane L holds values 8L..8L+7 = zfp blocks 2L and 2L+1, whose
+// 2 x 4R bits form an R-byte lane chunk at group byte L*R (group = 256
+// values = 32R bytes).  Each lane codes its two blocks sequentially in
+// registers (two 64-bit words per block, no local memory).
+#pragma once
+#include "device_common.cuh"
+
+namespace hccx {
+
+namespace zfp_detail {
+
+constexpr uint32_t kNB = 0xaaaaaaaau;
+
+struct Bits128 {
+  uint64_t lo = 0, hi = 0;
+  int pos = 0;
+  __device__ __forceinline__ void put(uint64_t val, int nbits) {  // nbits <= 32, val < 2^nbits
+    if (nbits == 0) return;
+    if (pos < 64) {
+      lo |= val << pos;
+      if (pos + nbits > 64) hi |= val >> (64 - pos);
+    } else {
+      hi |= val << (pos - 64);
+    }
+    pos += nbits;
+  }
+  __device__ __forceinline__ uint64_t get(int nbits) {  // nbits <= 32
+    if (nbits == 0) return 0;
+    uint64_t v;
+    if (pos < 64) {
+      v = lo >> pos;
+      if (pos + nbits > 64) v |= hi << (64 - pos);
+    } else {
+      v = hi >> (pos - 64);
+    }
+    pos += nbits;
+    return v & ((1ull << nbits) - 1ull);
+  }
+};
+
+__device__ __forceinline__ int32_t wadd(int32_t a, int32_t b) {
+  return static_cast<int32_t>(static_cast<uint32_t>(a) + static_cast<uint32_t>(b));
+}
+__device__ __forceinline__ int32_t wsub(int32_t a, int32_t b) {
+  return static_cast<int32_t>(static_cast<uint32_t>(a) - static_cast<uint32_t>(b));
+}
+__device__ __forceinline__ int32_t wshl1(int32_t a) {
+  return static_cast<int32_t>(static_cast<uint32_t>(a) << 1);
+}
+
+__device__ __forceinline__ void fwd_lift(int32_t& x, int32_t& y, int32_t& z, int32_t& w) {
+  x = wadd(x, w); x >>= 1; w = wsub(w, x);
+  z = wadd(z, y); z >>= 1; y = wsub(y, z);
+  x = wadd(x, z); x >>= 1; z = wsub(z, x);
+  w = wadd(w, y); w >>= 1; y = wsub(y, w);
+  w = wadd(w, y >> 1); y = wsub(y, w >> 1);
+}
+
+__device__ __forceinline__ void inv_lift(int32_t& x, int32_t& y, int32_t& z, int32_t& w) {
+  y = wadd(y, w >> 1); w = wsub(w, y >> 1);
+  y = wadd(y, w); w = wshl1(w); w = wsub(w, y);
+  z = wadd(z, x); x = wshl1(x); x = wsub(x, z);
+  y = wadd(y, z); z = wshl1(z); z = wsub(z, y);
+  w = wadd(w, x); x = wshl1(x); x = wsub(x, w);
+}
+
+// One 4-value block -> exactly 4R bits (LSB-first) in b.
+template <int R>
+__device__ __forceinline__ void encode_block(const float (&v)[4], Bits128& b, uint32_t& bad) {
+  uint32_t fmax = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) fmax = max(fmax, __float_as_uint(v[i]) & 0x7fffffffu);
+  bad |= static_cast<uint32_t>(fmax >= 0x7f800000u);
+  if (fmax == 0) {
+    b.put(0, 1);
+    return;
+  }
+  const int f = static_cast<int>(fmax >> 23);
+  const int emax = max(f - 126, -126);  // frexp exponent of the block max, clamped
+  b.put(1, 1);
+  b.put(static_cast<uint64_t>(emax + 127), 8);
+  // q = trunc(v * 2^(30-emax)), exact via two power-of-two multiplies.
+  const int k = 30 - emax, k1 = k / 2, k2 = k - k1;
+  const float s1 = exp2i(k1), s2 = exp2i(k2);
+  int32_t q[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) q[i] = __float2int_rz(__fmul_rn(__fmul_rn(v[i], s1), s2));
+  fwd_lift(q[0], q[1], q[2], q[3]);
+  uint32_t u[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) u[i] = (static_cast<uint32_t>(q[i]) + kNB) ^ kNB;
+  uint32_t bits = 4 * R - 9;
+  uint32_t n = 0;
+  for (int k = 31; bits && k >= 0; --k) {
+    uint32_t x = ((u[0] >> k) & 1u) | (((u[1] >> k) & 1u) << 1) | (((u[2] >> k) & 1u) << 2) |
+                 (((u[3] >> k) & 1u) << 3);
+    const uint32_t m = min(n, bits);
+    bits -= m;
+    b.put(x & ((1u << m) - 1u), static_cast<int>(m));
+    x >>= m;
+    while (n < 4 && bits) {
+      bits--;
+      const uint32_t any = x != 0;
+      b.put(any, 1);
+      if (!any) break;
+      while (n < 3 && bits) {
+        bits--;
+        const uint32_t bit = x & 1u;
+        b.put(bit, 1);
+        if (bit) break;
+        x >>= 1;
+        n++;
+      }
+      x >>= 1;
+      n++;
+    }
+  }
+}
+
+template <int R>
+__device__ __forceinline__ void decode_block(Bits128& b, float (&v)[4]) {
+  if (!b.get(1)) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) v[i] = 0.0f;
+    return;
+  }
+  const int emax = static_cast<int>(b.get(8)) - 127;
+  uint32_t u[4] = {0, 0, 0, 0};
+  uint32_t bits = 4 * R - 9;
+  uint32_t n = 0;
+  for (int k = 31; bits && k >= 0; --k) {
+    const uint32_t m = min(n, bits);
+    bits -= m;
+    uint32_t x = static_cast<uint32_t>(b.get(static_cast<int>(m)));
+    while (n < 4 && bits) {
+      bits--;
+      if (!b.get(1)) break;
+      while (n < 3 && bits) {
+        bits--;
+        if (b.get(1)) break;
+        n++;
+      }
+      x += 1u << n;
+      n++;
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) u[i] += ((x >> i) & 1u) << k;
+  }
+  int32_t q[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) q[i] = static_cast<int32_t>((u[i] ^ kNB) - kNB);
+  inv_lift(q[0], q[1], q[2], q[3]);
+  const double s = __longlong_as_double(static_cast<long long>(emax - 30 + 1023) << 52);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) v[i] = __double2float_rn(__dmul_rn(static_cast<double>(q[i]), s));
+}
+
+}  // namespace zfp_detail
+
+template <int R>
+struct ZfpRateCodec {
+  static_assert(R >= 3 && R <= 32, "zfp rate out of range");
+  static constexpr int kKind = 3;
+  static constexpr int kRate = R;
+  static constexpr bool kCheckFinite = true;
+  static constexpr uint32_t kGroupBytes = 32 * R;
+  static constexpr int kWords = (R + 3) / 4;
+  static constexpr bool kFastPath = (R % 4) == 0;
+
+  __host__ __device__ static uint64_t wire_bytes(uint64_t n) {
+    return (((n + 3) / 4) * 4 * static_cast<uint64_t>(R) + 7) / 8;
+  }
+  __host__ __device__ static uint32_t group_bytes_live(uint32_t live) {
+    return (((live + 3) / 4) * 4 * R + 7) / 8;
+  }
+
+  struct Lane {
+    uint32_t d[kWords];
+    uint32_t hdr;
+  };
+
+  // Values beyond the buffer arrive as 0.0f; lane_live (0..8) says how many
+  // of this lane's values exist so partial blocks are padded like zfp.
+  __device__ __forceinline__ static void encode(const float (&v)[8], Lane& s, uint32_t& bad,
+                                                uint32_t lane_live) {
+    zfp_detail::Bits128 b0, b1;
+    float a[4], c[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      a[i] = v[i];
+      c[i] = v[4 + i];
+    }
+    pad(a, min(lane_live, 4u));
+    pad(c, lane_live > 4 ? lane_live - 4 : 0u);
+    zfp_detail::encode_block<R>(a, b0, bad);
+    zfp_detail::encode_block<R>(c, b1, bad);
+    // chunk = b0 (4R bits) | b1 << 4R
+    constexpr int S = 4 * R;
+    uint64_t c0 = b0.lo, c1 = b0.hi, c2 = 0, c3 = 0;
+    if constexpr (S < 64) {
+      c0 |= b1.lo << S;
+      c1 |= (b1.lo >> (64 - S)) | (b1.hi << S);
+      c2 |= b1.hi >> (64 - S);
+    } else if constexpr (S == 64) {
+      c1 |= b1.lo;
+      c2 |= b1.hi;
+    } else if constexpr (S < 128) {
+      c1 |= b1.lo << (S - 64);
+      c2 |= (b1.lo >> (128 - S)) | (b1.hi << (S - 64));
+      c3 |= b1.hi >> (128 - S);
+    } else {
+      c2 |= b1.lo;
+      c3 |= b1.hi;
+    }
+    const uint64_t cw[4] = {c0, c1, c2, c3};
+#pragma unroll
+    for (int w = 0; w < kWords; ++w) s.d[w] = static_cast<uint32_t>(cw[w >> 1] >> (32 * (w & 1)));
+    s.hdr = 0;
+  }
+
+  __device__ __forceinline__ static void decode(const Lane& s, float (&v)[8]) {
+    uint64_t cw[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int w = 0; w < kWords; ++w) cw[w >> 1] |= static_cast<uint64_t>(s.d[w]) << (32 * (w & 1));
+    constexpr int S = 4 * R;
+    zfp_detail::Bits128 b0, b1;
+    b0.lo = cw[0];
+    b0.hi = cw[1];
+    if constexpr (S < 64) {
+      b1.lo = (cw[0] >> S) | (cw[1] << (64 - S));
+      b1.hi = (cw[1] >> S) | (cw[2] << (64 - S));
+    } else if constexpr (S == 64) {
+      b1.lo = cw[1];
+      b1.hi = cw[2];
+    } else if constexpr (S < 128) {
+      b1.lo = (cw[1] >> (S - 64)) | (cw[2] << (128 - S));
+      b1.hi = (cw[2] >> (S - 64)) | (cw[3] << (128 - S));
+    } else {
+      b1.lo = cw[2];
+      b1.hi = cw[3];
+    }
+    // mask block 0 to its 4R bits (decoder never reads past them, but keep it clean)
+    float a[4], c[4];
+    zfp_detail::decode_block<R>(b0, a);
+    zfp_detail::decode_block<R>(b1, c);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      v[i] = a[i];
+      v[4 + i] = c[i];
+    }
+  }
+
+  __device__ __forceinline__ static void pad(float (&p)[4], uint32_t live) {
+    // zfp pad_block for 1-D: 0 -> zeros, 1 -> p0 p0 p0 p0, 2 -> p0 p1 p1 p0, 3 -> p0 p1 p2 p0
+    if (live >= 4) return;
+    if (live == 0) p[0] = 0.0f;
+    if (live <= 1) p[1] = p[0];
+    if (live <= 2) p[2] = p[1];
+    p[3] = p[0];
+  }
+
+  __device__ __forceinline__ static void store_fast(const Lane& s, uint32_t* gw, int lane) {
+    constexpr int R4 = R / 4;
+#pragma unroll
+    for (int q = 0; q < R4; ++q) stg_u32(gw + R4 * lane + q, s.d[q]);
+  }
+  template <bool kStream>
+  __device__ __forceinline__ static void load_fast(Lane& s, const uint32_t* gw, int lane) {
+    constexpr int R4 = R / 4;
+#pragma unroll
+    for (int q = 0; q < R4; ++q)
+      s.d[q] = kStream ? ldg_u32_stream(gw + R4 * lane + q) : ldg_u32_coherent(gw + R4 * lane + q);
+    s.hdr = 0;
+  }
+  __device__ __forceinline__ static void to_stage(const Lane& s, uint8_t* sm, int lane) {
+    uint8_t* c = sm + lane * R;
+#pragma unroll
+    for (int m = 0; m < R; ++m) c[m] = static_cast<uint8_t>(s.d[m >> 2] >> (8 * (m & 3)));
+  }
+  __device__ __forceinline__ static void from_stage(Lane& s, const uint8_t* sm, int lane) {
+    const uint8_t* c = sm + lane * R;
+#pragma unroll
+    for (int w = 0; w < kWords; ++w) s.d[w] = 0;
+#pragma unroll
+    for (int m = 0; m < R; ++m) s.d[m >> 2] |= static_cast<uint32_t>(c[m]) << (8 * (m & 3));
+    s.hdr = 0;
+  }
+};
+
+}  // namespace hccx

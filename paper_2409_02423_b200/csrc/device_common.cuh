@@ -1,0 +1,99 @@
+// device_common.cuh -- PTX-level helpers shared by every hccx kernel (sm_100a).
+//
+// Memory model notes for the NVLink engine (ring_fused.cu):
+//  * data written by a peer into our window is read with plain (non-.nc)
+//    loads after an acquire on the flag -- .nc would let the texture path
+//    serve stale lines;
+//  * flags are 32-bit epoch counters written with st.release.sys and polled
+//    with ld.acquire.sys.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace hccx {
+
+constexpr int kWarp = 32;
+constexpr uint32_t kFull = 0xffffffffu;
+
+// Values handled by one warp per step: 32 lanes x 8 consecutive floats.
+constexpr int kGroupVals = 256;
+constexpr int kLaneVals = 8;
+
+// ---- vector global loads/stores --------------------------------------------
+
+// 256-bit streaming load (LDG.E.256 on sm_100a); p must be 32-byte aligned
+// and the data must not be written during the kernel.
+__device__ __forceinline__ void ldg8_stream(const float* p, float (&v)[8]) {
+  asm volatile(
+      "ld.global.nc.L1::no_allocate.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+      : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]),
+        "=f"(v[7])
+      : "l"(p));
+}
+
+// 256-bit coherent load (peer-written or kernel-written data).
+__device__ __forceinline__ void ldg8_coherent(const float* p, float (&v)[8]) {
+  asm volatile(
+      "ld.global.L1::no_allocate.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+      : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]),
+        "=f"(v[7])
+      : "l"(p)
+      : "memory");
+}
+
+__device__ __forceinline__ void stg8(float* p, const float (&v)[8]) {
+  asm volatile("st.global.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "f"(v[0]),
+               "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7])
+               : "memory");
+}
+
+__device__ __forceinline__ uint32_t ldg_u32_coherent(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.global.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ uint32_t ldg_u32_stream(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+
+__device__ __forceinline__ void stg_u32(uint32_t* p, uint32_t v) {
+  asm volatile("st.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// ---- flags (system scope: visible across NVLink peers) ---------------------
+
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// ---- misc -------------------------------------------------------------------
+
+__device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
+
+// Bytes [8*off, 8*off + 32) of the 64-bit concatenation hi:lo (off in 0..3).
+__device__ __forceinline__ uint32_t funnel_bytes(uint32_t lo, uint32_t hi, int byte_off) {
+  return __funnelshift_r(lo, hi, 8 * byte_off);
+}
+
+// Power of two 2^e as a float, valid for e in [-149, 127].
+__device__ __forceinline__ float exp2i(int e) {
+  return e >= -126 ? __uint_as_float(static_cast<uint32_t>(e + 127) << 23)
+                   : __uint_as_float(1u << (e + 149));
+}
+
+}  // namespace hccx

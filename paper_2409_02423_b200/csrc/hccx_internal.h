@@ -1,0 +1,30 @@
+// hccx_internal.h -- host helpers shared by capi.cu and comm.cu.
+#pragma once
+#include <cuda_runtime.h>
+
+#include "hccx.h"
+#include "hccx_kernels.h"
+
+namespace hccx {
+
+hccx_status_t cuda_status(cudaError_t e);
+hccx_status_t check_codec(hccx_codec_t c);
+CodecSel sel_of(hccx_codec_t c);
+void finalize_params(StepParams& p, CodecSel c, int op);
+void set_divisor(StepParams& p, int mode, int nranks);
+hccx_status_t run_step(CodecSel c, int op, StepParams& p, cudaStream_t s);
+hccx_status_t read_flag(uint32_t* d_err, cudaStream_t s);
+
+// RAII: make `dev` current for the scope (no-op when dev < 0).
+class DeviceGuard {
+ public:
+  explicit DeviceGuard(int dev);
+  ~DeviceGuard();
+  DeviceGuard(const DeviceGuard&) = delete;
+  DeviceGuard& operator=(const DeviceGuard&) = delete;
+
+ private:
+  int prev_ = 0;
+};
+
+}  // namespace hccx

@@ -1,0 +1,79 @@
+"""Generate golden fixtures from the UNMODIFIED reference library.
+
+Run in the dev container (needs /root/reference to build oracle/_ref):
+
+    python tests/golden/make_golden.py
+
+Every array is produced by the reference's own code compiled from
+/root/reference/proj/src (oracle/_ref/libhcc_ref.so via oracle/ref_capi.cpp):
+inputs come from the reference's buffer generators (hcc::Rng,
+proj/tests/support/oracles.cpp:9-36), payloads from hcc::compress, decoded
+values from hcc::decompress, collective outputs and byte accounting from
+hcc::allreduce / ring_reduce_scatter / ring_allgather / p2p.  The fixtures
+travel with the repo, so the GPU box (where /root/reference does not exist)
+checks the kernels against the reference's own outputs.
+"""
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.dirname(HERE))
+
+import oracle_lib as O  # noqa: E402
+
+CODEC_RATES = [2, 3, 4, 5, 7, 8, 12, 13, 16, 22, 23, 24, 25, 26, 31, 32]
+CODEC_SIZES = [1, 63, 64, 65, 255, 256, 257, 1000, 2049]
+MODES = [("uniform", -1.0, 1.0), ("finite", 0, 0), ("sparse", 0.5, 0)]
+
+
+def main() -> None:
+    assert O.ref is not None, "oracle/_ref/libhcc_ref.so is required (build with oracle/build_ref.sh)"
+    codec = {}
+    seed = 1000
+    for rate in CODEC_RATES:
+        for n in CODEC_SIZES:
+            for mode, lo, hi in MODES:
+                seed += 1
+                x = O.ref_fill(seed, mode, n, lo, hi)
+                payload, cc = O.ref_compress("fixed-rate", rate, x)
+                dec = O.ref_decompress("fixed-rate", rate, payload, n, cc)
+                key = f"fr{rate}_n{n}_{mode}"
+                codec[f"{key}_in"] = x
+                codec[f"{key}_payload"] = payload
+                codec[f"{key}_dec"] = dec
+    np.savez_compressed(os.path.join(HERE, "fixed_rate.npz"), **codec)
+
+    coll = {}
+    seed = 5000
+    for p in [2, 3, 4, 8]:
+        for kind, rate in [("identity", 0), ("fixed-rate", 4), ("fixed-rate", 8), ("fixed-rate", 16)]:
+            for n_per in [64, 200, 320]:
+                n = n_per * p
+                seed += 1
+                x = np.stack([O.ref_fill(seed * 17 + j, "uniform", n) for j in range(p)])
+                key = f"p{p}_{kind}{rate}_n{n}"
+                coll[f"{key}_in"] = x
+                for avg in (0, 1):
+                    out, acct = O.ref_allreduce(x, kind, rate, bool(avg))
+                    coll[f"{key}_ar{avg}"] = out
+                    coll[f"{key}_ar{avg}_acct"] = np.array(acct, np.uint64)
+                rs, acct = O.ref_reduce_scatter(x, kind, rate)
+                coll[f"{key}_rs"] = rs
+                coll[f"{key}_rs_acct"] = np.array(acct, np.uint64)
+                shards = np.ascontiguousarray(x[:, :n_per])
+                ag, acct = O.ref_allgather(shards, kind, rate)
+                coll[f"{key}_ag"] = ag
+                coll[f"{key}_ag_acct"] = np.array(acct, np.uint64)
+                pp, acct = O.ref_p2p(x[0], kind, rate)
+                coll[f"{key}_p2p"] = pp
+                coll[f"{key}_p2p_acct"] = np.array(acct, np.uint64)
+    np.savez_compressed(os.path.join(HERE, "collectives.npz"), **coll)
+    print("wrote", len(codec), "codec arrays and", len(coll), "collective arrays")
+
+
+if __name__ == "__main__":
+    main()

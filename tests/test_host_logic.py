@@ -1,0 +1,112 @@
+"""Host-side logic mirrored from the reference (no GPU): codec specs and
+strings, the hybrid scheme table, the parallel layout, the HCC1 container
+and SimClock accounting.  Cases follow proj/tests/test_codec.cpp,
+test_parallel3d.cpp and test_netsim.cpp."""
+import io
+
+import numpy as np
+import pytest
+
+import paper_2409_02423_b200 as H
+from paper_2409_02423_b200.codec import CodecKind, CompressedBuffer
+from paper_2409_02423_b200.comm_path import CommPath, comm_path_from_string
+from paper_2409_02423_b200.netsim import CollectiveKind, SimClock, Topology, TraceEvent, write_trace_csv
+
+
+def test_fixed_rate_range():  # test_codec.cpp:25-30
+    H.CodecSpec.fixed_rate(2)
+    H.CodecSpec.fixed_rate(32)
+    for bad in (1, 33):
+        with pytest.raises(H.InvalidSchemeError):
+            H.CodecSpec.fixed_rate(bad)
+
+
+def test_string_round_trip():  # test_codec.cpp:32-39
+    for s in (H.CodecSpec.identity(), H.CodecSpec.lossless(), H.CodecSpec.fixed_rate(8),
+              H.CodecSpec.fixed_rate(24), H.CodecSpec.zfp_rate(8)):
+        assert H.codec_spec_from_string(H.to_string(s)) == s
+    with pytest.raises(H.ConfigError):
+        H.codec_spec_from_string("zfp")
+    with pytest.raises(H.InvalidSchemeError):
+        H.codec_spec_from_string("fixed-rate:99")
+    with pytest.raises(H.ConfigError):
+        H.codec_spec_from_string("fixed-rate:x")
+    assert H.codec_spec_from_string("fixed-rate: 8abc") == H.CodecSpec.fixed_rate(8)  # std::stoi
+
+
+def test_golden_identity_container():  # test_codec.cpp:47-58
+    cb = CompressedBuffer(H.CodecSpec.identity(), 1, 0, np.frombuffer(np.float32(1.0).tobytes(), np.uint8))
+    assert H.to_bytes(cb) == bytes([ord("H"), ord("C"), ord("C"), ord("1"), 0, 0, 1, 0, 0, 0, 0, 0, 0, 0,
+                                    0, 0, 0, 0, 0x00, 0x00, 0x80, 0x3F])
+
+
+def test_container_malformed():  # test_codec.cpp:212-240
+    cb = CompressedBuffer(H.CodecSpec.fixed_rate(8), 100, 2, np.arange(130, dtype=np.uint8))
+    b = H.to_bytes(cb)
+    back = H.from_bytes(b)
+    assert back.codec == cb.codec and back.original_len == 100 and back.chunk_count == 2
+    assert back.payload.tobytes() == cb.payload.tobytes()
+    with pytest.raises(H.CorruptPayloadError):
+        H.from_bytes(b[:10])
+    with pytest.raises(H.CorruptPayloadError):
+        H.from_bytes(b"X" + b[1:])
+    with pytest.raises(H.CorruptPayloadError):
+        H.from_bytes(b[:4] + bytes([7]) + b[5:])
+    with pytest.raises(H.CorruptPayloadError):
+        H.from_bytes(b[:5] + bytes([40]) + b[6:])
+
+
+def test_scheme_builders():  # test_parallel3d.cpp (scheme rows), parallel3d.cpp:43-122
+    z = H.scheme_from_name("z-hybrid:16,4")
+    assert z.at(CommPath.DpAllReduce) == H.CodecSpec.fixed_rate(4)
+    for p in (CommPath.PpP2p, CommPath.TpAllReduce, CommPath.TpAllGather, CommPath.Zero1AllGather,
+              CommPath.Zero1ReduceScatter):
+        assert z.at(p) == H.CodecSpec.fixed_rate(16)
+    assert z.name == "z-hybrid:16,4"
+    m = H.scheme_from_name("mz-hybrid:8")
+    assert m.at(CommPath.DpAllReduce) == H.CodecSpec.fixed_rate(8)
+    assert m.at(CommPath.TpAllReduce).kind == CodecKind.LosslessPredictor
+    assert H.scheme_from_name("baseline").name == "no-compression"
+    assert H.scheme_from_name("naive-zfp8").at(CommPath.PpP2p) == H.CodecSpec.fixed_rate(8)
+    assert H.scheme_from_name("naive-mpc").name == "naive-mpc"
+    with pytest.raises(H.InvalidSchemeError):
+        H.scheme_from_name("z-hybrid:4,16")
+    with pytest.raises(H.InvalidSchemeError):
+        H.scheme_from_name("naive-zfp40")
+    for bad in ("z-hybrid:16", "zhybrid", "naive-zfpx", "mz-hybrid:"):
+        with pytest.raises(H.ConfigError):
+            H.scheme_from_name(bad)
+    assert set(H.scheme_no_compression().paths) == set(CommPath)
+    assert comm_path_from_string("PpP2p") == CommPath.PpP2p
+    with pytest.raises(H.ConfigError):
+        comm_path_from_string("nope")
+
+
+def test_layout_groups():  # test_parallel3d.cpp, parallel3d.hpp:14-46
+    lay = H.build_layout(2, 3, 4, 24)
+    for r in range(24):
+        c = lay.coord_of(r)
+        assert lay.rank_of(c.d, c.p, c.t) == r
+        assert r in lay.dp_group(r) and r in lay.tp_group(r) and r in lay.pp_chain(r)
+    assert lay.tp_group(5) == [4, 5, 6, 7]
+    assert lay.dp_group(5) == [5, 17]
+    assert lay.pp_chain(5) == [1, 5, 9]
+    with pytest.raises(H.BadLayoutError):
+        H.build_layout(2, 2, 2, 10)
+    with pytest.raises(H.BadLayoutError):
+        H.build_layout(0, 2, 2, 0)
+
+
+def test_simclock_accounting():  # test_netsim.cpp
+    clk = SimClock(Topology.lassen_like(2))
+    assert clk.topology().world_size() == 8
+    clk.advance(1, 2.0)
+    clk.sync_to_max([0, 1, 2])
+    assert clk.time(0) == clk.time(2) == 2.0 and clk.time(3) == 0.0
+    clk.set_step(7)
+    clk.record(TraceEvent(0, CommPath.TpAllReduce, CollectiveKind.AllReduce, 4, 96, 24, 1e-3, 6))
+    assert clk.trace()[0].step == 7
+    s = io.StringIO()
+    write_trace_csv(s, clk.trace())
+    assert s.getvalue().splitlines() == ["step,path,collective,comm_size,raw_bytes,wire_bytes,duration_s",
+                                         "7,TpAllReduce,AllReduce,4,96,24,1.000000000e-03"]
