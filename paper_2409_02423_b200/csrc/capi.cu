@@ -43,7 +43,7 @@ CodecSel sel_of(hccx_codec_t c) {
 static bool aligned(const void* p, uintptr_t a) { return (reinterpret_cast<uintptr_t>(p) & (a - 1)) == 0; }
 
 void finalize_params(StepParams& p, CodecSel c, int op) {
-  bool vec = true, fast = true;
+  bool vec = true, fast = true, tma = true;
   const uintptr_t fa = fast_align(c);
   for (int j = 0; j < p.njobs; ++j) {
     const StepJob& J = p.jobs[j];
@@ -52,6 +52,7 @@ void finalize_params(StepParams& p, CodecSel c, int op) {
       fast = fast && aligned(J.dst, fa);
     } else {
       fast = fast && aligned(J.src, fa);
+      tma = tma && aligned(J.src, 16);
       if (op == kOpDAR) fast = fast && aligned(J.dst, fa);
       if (op == kOpDecodeAdd) vec = vec && aligned(J.dst, 32);
       if (op == kOpDAR || op == kOpDecodeAdd) vec = vec && aligned(J.local, 32);
@@ -60,6 +61,7 @@ void finalize_params(StepParams& p, CodecSel c, int op) {
   }
   p.vec_ok = vec ? 1 : 0;
   p.fast_ok = fast ? 1 : 0;
+  p.tma_ok = tma ? 1 : 0;
 }
 
 void set_divisor(StepParams& p, int mode, int nranks) {

@@ -147,29 +147,47 @@ struct FixedRateCodec {
     }
   }
 
-  template <bool kStream>
-  __device__ __forceinline__ static void load_fast(Lane& s, const uint32_t* gw, int lane) {
+  // Fast-path loads are split so a warp can put several groups' loads in
+  // flight before it assembles any of them (memory-level parallelism).
+  struct Raw {
+    uint32_t w[kFastPath ? R / 4 : 1];
+    uint32_t w0;
+  };
+
+  template <int kSrc>
+  __device__ __forceinline__ static void load_raw(Raw& r, const uint32_t* gw, int lane) {
     static_assert(kFastPath, "fast path needs R % 4 == 0");
     constexpr int R4 = R / 4;
     const int k = lane >> 3, l = lane & 7;
     const uint32_t* src = (k < 3) ? gw + 2 * R * k + R4 * l + 1 : gw + 6 * R + 1 + R4 * l;
-    uint32_t w[R4];
 #pragma unroll
-    for (int q = 0; q < R4; ++q) w[q] = kStream ? ldg_u32_stream(src + q) : ldg_u32_coherent(src + q);
-    const uint32_t w0 = (lane == 0) ? (kStream ? ldg_u32_stream(gw) : ldg_u32_coherent(gw)) : 0u;
-    uint32_t prev = __shfl_up_sync(kFull, w[R4 - 1], 1);
-    if (lane == 0) prev = w0;
-    const uint32_t hsrc = __shfl_sync(kFull, lane == 0 ? w0 : w[R4 - 1], k == 0 ? 0 : 8 * k - 1);
+    for (int q = 0; q < R4; ++q) r.w[q] = ld_word<kSrc>(src + q);
+    r.w0 = (lane == 0) ? ld_word<kSrc>(gw) : 0u;
+  }
+
+  __device__ __forceinline__ static void assemble(Lane& s, const Raw& r, int lane) {
+    constexpr int R4 = R / 4;
+    const int k = lane >> 3;
+    uint32_t prev = __shfl_up_sync(kFull, r.w[R4 - 1], 1);
+    if (lane == 0) prev = r.w0;
+    const uint32_t hsrc = __shfl_sync(kFull, lane == 0 ? r.w0 : r.w[R4 - 1], k == 0 ? 0 : 8 * k - 1);
     s.hdr = (hsrc >> (8 * k)) & 0xffu;
     if (k < 3) {
       const int a = k + 1;
-      s.d[0] = __funnelshift_r(prev, w[0], 8 * a);
+      s.d[0] = __funnelshift_r(prev, r.w[0], 8 * a);
 #pragma unroll
-      for (int q = 1; q < R4; ++q) s.d[q] = __funnelshift_r(w[q - 1], w[q], 8 * a);
+      for (int q = 1; q < R4; ++q) s.d[q] = __funnelshift_r(r.w[q - 1], r.w[q], 8 * a);
     } else {
 #pragma unroll
-      for (int q = 0; q < R4; ++q) s.d[q] = w[q];
+      for (int q = 0; q < R4; ++q) s.d[q] = r.w[q];
     }
+  }
+
+  template <bool kStream>
+  __device__ __forceinline__ static void load_fast(Lane& s, const uint32_t* gw, int lane) {
+    Raw r;
+    load_raw<kStream ? 0 : 1>(r, gw, lane);
+    assemble(s, r, lane);
   }
 
   // Any rate / partial group: bytes staged through this warp's shared

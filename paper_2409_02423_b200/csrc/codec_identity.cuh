@@ -38,15 +38,22 @@ struct IdentityCodec {
     decode(s, v);
     stg8(reinterpret_cast<float*>(gw) + 8 * lane, v);
   }
+  struct Raw {
+    float v[8];
+  };
+  template <int kSrc>
+  __device__ __forceinline__ static void load_raw(Raw& r, const uint32_t* gw, int lane) {
+    ld_vals<kSrc>(reinterpret_cast<const float*>(gw) + 8 * lane, r.v);
+  }
+  __device__ __forceinline__ static void assemble(Lane& s, const Raw& r, int) {
+    uint32_t dummy = 0;
+    encode(r.v, s, dummy, 8);
+  }
   template <bool kStream>
   __device__ __forceinline__ static void load_fast(Lane& s, const uint32_t* gw, int lane) {
-    float v[8];
-    if (kStream)
-      ldg8_stream(reinterpret_cast<const float*>(gw) + 8 * lane, v);
-    else
-      ldg8_coherent(reinterpret_cast<const float*>(gw) + 8 * lane, v);
-    uint32_t dummy = 0;
-    encode(v, s, dummy, 8);
+    Raw r;
+    load_raw<kStream ? 0 : 1>(r, gw, lane);
+    assemble(s, r, lane);
   }
   __device__ __forceinline__ static void to_stage(const Lane& s, uint8_t* sm, int lane) {
     uint32_t* w = reinterpret_cast<uint32_t*>(sm) + 8 * lane;

@@ -277,13 +277,26 @@ struct ZfpRateCodec {
 #pragma unroll
     for (int q = 0; q < R4; ++q) stg_u32(gw + R4 * lane + q, s.d[q]);
   }
-  template <bool kStream>
-  __device__ __forceinline__ static void load_fast(Lane& s, const uint32_t* gw, int lane) {
+  struct Raw {
+    uint32_t w[kFastPath ? R / 4 : 1];
+  };
+  template <int kSrc>
+  __device__ __forceinline__ static void load_raw(Raw& r, const uint32_t* gw, int lane) {
     constexpr int R4 = R / 4;
 #pragma unroll
     for (int q = 0; q < R4; ++q)
-      s.d[q] = kStream ? ldg_u32_stream(gw + R4 * lane + q) : ldg_u32_coherent(gw + R4 * lane + q);
+      r.w[q] = ld_word<kSrc>(gw + R4 * lane + q);
+  }
+  __device__ __forceinline__ static void assemble(Lane& s, const Raw& r, int) {
+#pragma unroll
+    for (int q = 0; q < R / 4; ++q) s.d[q] = r.w[q];
     s.hdr = 0;
+  }
+  template <bool kStream>
+  __device__ __forceinline__ static void load_fast(Lane& s, const uint32_t* gw, int lane) {
+    Raw r;
+    load_raw<kStream ? 0 : 1>(r, gw, lane);
+    assemble(s, r, lane);
   }
   __device__ __forceinline__ static void to_stage(const Lane& s, uint8_t* sm, int lane) {
     uint8_t* c = sm + lane * R;

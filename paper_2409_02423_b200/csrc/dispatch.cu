@@ -76,4 +76,29 @@ int stream_grid(const void* kernel, uint64_t work_items) {
   return static_cast<int>(want < cap ? want : cap);
 }
 
+int tma_grid(const void* kernel, int threads, uint32_t smem, uint64_t work_items) {
+  static std::mutex mu;
+  static std::unordered_map<const void*, int> per_sm;
+  static int sms = 0;
+  int blocks_per_sm = 1;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    if (sms == 0) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    auto it = per_sm.find(kernel);
+    if (it == per_sm.end()) {
+      int b = 0;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel, threads, smem) != cudaSuccess || b < 1) b = 1;
+      it = per_sm.emplace(kernel, b).first;
+    }
+    blocks_per_sm = it->second;
+  }
+  const uint64_t cap = static_cast<uint64_t>(blocks_per_sm) * static_cast<uint64_t>(sms > 0 ? sms : 148);
+  const uint64_t g = work_items < cap ? work_items : cap;
+  return static_cast<int>(g > 0 ? g : 1);
+}
+
 }  // namespace hccx

@@ -27,6 +27,7 @@ struct StepParams {
   uint64_t n;       // values per job
   int vec_ok;       // every float pointer 32-byte aligned
   int fast_ok;      // every payload pointer aligned for the codec's word path
+  int tma_ok;       // every source pointer 16-byte aligned (bulk-copy path)
   int div_mode;     // 0 none, 1 multiply by recip (p power of two), 2 IEEE divide
   float recip;
   float divisor;
@@ -56,5 +57,7 @@ void count_launch(uint64_t k = 1);
 
 // Grid size for a streaming kernel over `work_items` warp groups.
 int stream_grid(const void* kernel, uint64_t work_items);
+// Persistent grid for the TMA kernel: min(work_items, SMs x resident CTAs).
+int tma_grid(const void* kernel, int threads, uint32_t smem, uint64_t work_items);
 
 }  // namespace hccx

@@ -167,20 +167,243 @@ __device__ __forceinline__ void step_group(const StepJob& J, uint64_t g, uint64_
   }
 }
 
+// Full groups with aligned pointers: U groups per warp iteration, all of
+// their loads issued before any group is assembled, so each warp keeps
+// U x 1 KiB (Encode) or U x (payload + 1 KiB) (DAR) in flight.
+template <int kOp>
+struct StepUnroll {
+  static constexpr int value = (kOp == kOpEncode || kOp == kOpDecode) ? 4 : 2;
+};
+
+template <class Codec, int kOp, int U>
+__device__ __forceinline__ void step_fast(const StepJob& J, uint64_t g0, uint64_t S, uint64_t nfull,
+                                          int div_mode, float recip, float divisor, int lane,
+                                          uint32_t& bad) {
+  constexpr uint64_t GB = Codec::kGroupBytes;
+  float v[U][8];
+  float loc[U][8];
+  typename Codec::Raw raw[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const uint64_t g = g0 + u * S;
+    if (g < nfull) {
+      if constexpr (kOp == kOpEncode) {
+        ldg8_stream(static_cast<const float*>(J.src) + g * kGroupVals + 8 * lane, v[u]);
+      } else {
+        Codec::template load_raw<0>(
+            raw[u], reinterpret_cast<const uint32_t*>(static_cast<const uint8_t*>(J.src) + g * GB), lane);
+        if constexpr (kOp == kOpDAR || kOp == kOpDecodeAdd)
+          ldg8_stream(J.local + g * kGroupVals + 8 * lane, loc[u]);
+      }
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const uint64_t g = g0 + u * S;
+    if (g >= nfull) continue;
+    typename Codec::Lane s;
+    const uint64_t vo = g * kGroupVals + 8 * lane;
+    if constexpr (kOp == kOpEncode) {
+      Codec::encode(v[u], s, bad, 8u);
+      Codec::store_fast(s, reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(J.dst) + g * GB), lane);
+    } else {
+      Codec::assemble(s, raw[u], lane);
+      float w[8];
+      Codec::decode(s, w);
+      if constexpr (kOp == kOpDecode) {
+        apply_div(w, div_mode, recip, divisor);
+        for (int o = 0; o < J.nouts; ++o) stg8(J.outs[o] + vo, w);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) w[i] = __fadd_rn(w[i], loc[u][i]);
+        if constexpr (kOp == kOpDecodeAdd) {
+          stg8(static_cast<float*>(J.dst) + vo, w);
+        } else {
+          Codec::encode(w, s, bad, 8u);
+          Codec::store_fast(s, reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(J.dst) + g * GB), lane);
+          if (J.nouts > 0) {
+            Codec::decode(s, w);
+            apply_div(w, div_mode, recip, divisor);
+            stg8(J.outs[0] + vo, w);
+          }
+        }
+      }
+    }
+  }
+}
+
 template <class Codec, int kOp>
 __global__ void __launch_bounds__(kStepThreads) step_kernel(const __grid_constant__ StepParams P) {
   __shared__ __align__(16) uint8_t stage[kStepWarps][kStageBytes];
   const int lane = static_cast<int>(lane_id()), warp = static_cast<int>(threadIdx.x >> 5);
   const uint64_t ngroups = (P.n + kGroupVals - 1) / kGroupVals;
+  const uint64_t S = static_cast<uint64_t>(gridDim.x) * kStepWarps;
+  const uint64_t wid = static_cast<uint64_t>(blockIdx.x) * kStepWarps + warp;
   uint32_t bad = 0;
-  for (uint64_t g = static_cast<uint64_t>(blockIdx.x) * kStepWarps + warp; g < ngroups;
-       g += static_cast<uint64_t>(gridDim.x) * kStepWarps) {
+  uint64_t g_generic = wid;
+  if constexpr (Codec::kFastPath) {
+    if (P.vec_ok && P.fast_ok) {
+      constexpr int U = StepUnroll<kOp>::value;
+      const uint64_t nfull = P.n / kGroupVals;
+      for (uint64_t g0 = wid; g0 < nfull; g0 += S * U)
+        for (int j = 0; j < P.njobs; ++j)
+          step_fast<Codec, kOp, U>(P.jobs[j], g0, S, nfull, P.div_mode, P.recip, P.divisor, lane, bad);
+      g_generic = nfull + wid;  // only the trailing partial group is left
+    }
+  }
+  for (uint64_t g = g_generic; g < ngroups; g += S) {
     for (int j = 0; j < P.njobs; ++j)
       step_group<Codec, kOp, true>(P.jobs[j], g, P.n, P.vec_ok, P.fast_ok, P.div_mode, P.recip,
                                    P.divisor, stage[warp], lane, bad);
   }
   if constexpr (Codec::kCheckFinite) {
     if (__any_sync(kFull, bad) && lane == 0 && P.err) atomicOr(P.err, kErrNonFinite);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// TMA-staged streaming kernel (the production path for aligned buffers).
+//
+// 8 consumer warps + 1 producer warp per CTA, persistent over "tiles" of 8
+// full groups of one job.  The producer's elected lane streams each tile's
+// source bytes (payload and/or fp32) into a kTmaStages-deep shared-memory
+// ring with cp.async.bulk, completing on a per-stage "full" mbarrier; every
+// consumer warp decodes/encodes one group of the tile from shared memory,
+// writes its result with coalesced global stores and arrives on the stage's
+// "empty" mbarrier.  Loads are therefore always in flight (kTmaStages tiles per
+// CTA) no matter what the consumers are computing.  Leftover groups (fewer
+// than 8 at the end of a job, and the partial last group) use the per-warp
+// path above.
+// ---------------------------------------------------------------------------
+
+constexpr int kTmaStages = 4;
+constexpr int kTmaConsumers = 8;
+constexpr int kTmaThreads = (kTmaConsumers + 1) * 32;
+constexpr int kTileGroups = kTmaConsumers;
+
+template <class Codec, int kOp>
+struct TmaLayout {
+  static constexpr uint32_t kA = (kOp == kOpEncode ? 4u * kGroupVals : Codec::kGroupBytes) * kTileGroups;
+  static constexpr uint32_t kAPad = (kA + 127u) / 128u * 128u;
+  static constexpr uint32_t kB = (kOp == kOpDAR || kOp == kOpDecodeAdd) ? 4u * kGroupVals * kTileGroups : 0u;
+  static constexpr uint32_t kStage = kAPad + kB;
+  static constexpr uint32_t kBarOff = kStage * kTmaStages;
+  static constexpr uint32_t kStageOff = kBarOff + 2 * 8 * kTmaStages;  // per-warp staging for leftovers
+  static constexpr uint32_t kSmem = kStageOff + kTmaConsumers * kStageBytes;
+};
+
+template <class Codec, int kOp>
+__device__ __forceinline__ void tma_group(const StepJob& J, uint64_t g, const uint8_t* a, const float* b,
+                                          int div_mode, float recip, float divisor, int lane, uint32_t& bad) {
+  constexpr uint64_t GB = Codec::kGroupBytes;
+  typename Codec::Lane s;
+  const uint64_t vo = g * kGroupVals + 8 * lane;
+  if constexpr (kOp == kOpEncode) {
+    float v[8];
+    ld_vals<2>(reinterpret_cast<const float*>(a) + 8 * lane, v);
+    Codec::encode(v, s, bad, 8u);
+    Codec::store_fast(s, reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(J.dst) + g * GB), lane);
+  } else {
+    typename Codec::Raw raw;
+    Codec::template load_raw<2>(raw, reinterpret_cast<const uint32_t*>(a), lane);
+    Codec::assemble(s, raw, lane);
+    float w[8];
+    Codec::decode(s, w);
+    if constexpr (kOp == kOpDecode) {
+      apply_div(w, div_mode, recip, divisor);
+      for (int o = 0; o < J.nouts; ++o) stg8(J.outs[o] + vo, w);
+    } else {
+      float loc[8];
+      ld_vals<2>(b + 8 * lane, loc);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) w[i] = __fadd_rn(w[i], loc[i]);
+      if constexpr (kOp == kOpDecodeAdd) {
+        stg8(static_cast<float*>(J.dst) + vo, w);
+      } else {
+        Codec::encode(w, s, bad, 8u);
+        Codec::store_fast(s, reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(J.dst) + g * GB), lane);
+        if (J.nouts > 0) {
+          Codec::decode(s, w);
+          apply_div(w, div_mode, recip, divisor);
+          stg8(J.outs[0] + vo, w);
+        }
+      }
+    }
+  }
+}
+
+template <class Codec, int kOp>
+__global__ void __launch_bounds__(kTmaThreads) step_tma_kernel(const __grid_constant__ StepParams P) {
+  using L = TmaLayout<Codec, kOp>;
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::kBarOff);
+  uint64_t* empty = full + kTmaStages;
+  const int lane = static_cast<int>(lane_id()), warp = static_cast<int>(threadIdx.x >> 5);
+  const uint64_t nfull = P.n / kGroupVals;
+  const uint64_t tiles_per_job = nfull / kTileGroups;
+  const uint64_t total = tiles_per_job * static_cast<uint64_t>(P.njobs);
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < kTmaStages; ++st) {
+      mbar_init(&full[st], 1);
+      mbar_init(&empty[st], kTmaConsumers);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  uint32_t bad = 0;
+  if (warp == kTmaConsumers) {
+    if (lane == 0) {
+      int st = 0;
+      uint32_t phase = 0;
+      for (uint64_t t = blockIdx.x; t < total; t += gridDim.x) {
+        mbar_wait(&empty[st], phase ^ 1u);
+        const int j = static_cast<int>(t / tiles_per_job);
+        const uint64_t tile = t - static_cast<uint64_t>(j) * tiles_per_job;
+        const StepJob& J = P.jobs[j];
+        uint8_t* base = smem + st * L::kStage;
+        mbar_arrive_expect_tx(&full[st], L::kA + L::kB);
+        bulk_g2s(base, static_cast<const uint8_t*>(J.src) + tile * L::kA, L::kA, &full[st]);
+        if constexpr (L::kB != 0)
+          bulk_g2s(base + L::kAPad, reinterpret_cast<const uint8_t*>(J.local) + tile * L::kB, L::kB, &full[st]);
+        if (++st == kTmaStages) {
+          st = 0;
+          phase ^= 1u;
+        }
+      }
+    }
+  } else {
+    int st = 0;
+    uint32_t phase = 0;
+    constexpr uint32_t kAGroup = L::kA / kTileGroups;
+    for (uint64_t t = blockIdx.x; t < total; t += gridDim.x) {
+      const int j = static_cast<int>(t / tiles_per_job);
+      const uint64_t tile = t - static_cast<uint64_t>(j) * tiles_per_job;
+      mbar_wait(&full[st], phase);
+      const uint8_t* base = smem + st * L::kStage;
+      tma_group<Codec, kOp>(P.jobs[j], tile * kTileGroups + warp, base + warp * kAGroup,
+                            reinterpret_cast<const float*>(base + L::kAPad) + warp * kGroupVals, P.div_mode,
+                            P.recip, P.divisor, lane, bad);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
+      if (++st == kTmaStages) {
+        st = 0;
+        phase ^= 1u;
+      }
+    }
+    // leftovers: groups [tiles_per_job*8, ngroups) of every job
+    const uint64_t ngroups = (P.n + kGroupVals - 1) / kGroupVals;
+    const uint64_t first = tiles_per_job * kTileGroups;
+    const uint64_t per_job = ngroups - first;
+    const uint64_t wid = static_cast<uint64_t>(blockIdx.x) * kTmaConsumers + warp;
+    uint8_t* sm = smem + L::kStageOff + warp * kStageBytes;
+    for (uint64_t r = wid; r < per_job * P.njobs; r += static_cast<uint64_t>(gridDim.x) * kTmaConsumers) {
+      const int j = static_cast<int>(r / per_job);
+      step_group<Codec, kOp, true>(P.jobs[j], first + (r - j * per_job), P.n, P.vec_ok, P.fast_ok, P.div_mode,
+                                   P.recip, P.divisor, sm, lane, bad);
+    }
+  }
+  if constexpr (Codec::kCheckFinite) {
+    if (warp < kTmaConsumers && __any_sync(kFull, bad) && lane == 0 && P.err) atomicOr(P.err, kErrNonFinite);
   }
 }
 

@@ -2,26 +2,55 @@
 // the per-rate-range translation units so the 31 fixed-rate instantiations
 // compile in parallel.
 #pragma once
+#include <atomic>
+
 #include "step_kernel.cuh"
 
 namespace hccx {
 
-template <class Codec>
-cudaError_t launch_codec_step(int op, const StepParams& p, cudaStream_t stream) {
-  const void* k = nullptr;
-  switch (op) {
-    case kOpEncode: k = reinterpret_cast<const void*>(&step_kernel<Codec, kOpEncode>); break;
-    case kOpDecode: k = reinterpret_cast<const void*>(&step_kernel<Codec, kOpDecode>); break;
-    case kOpDAR: k = reinterpret_cast<const void*>(&step_kernel<Codec, kOpDAR>); break;
-    case kOpDecodeAdd: k = reinterpret_cast<const void*>(&step_kernel<Codec, kOpDecodeAdd>); break;
-    default: return cudaErrorInvalidValue;
+template <class Codec, int kOp>
+cudaError_t launch_tma(const StepParams& p, cudaStream_t stream) {
+  using L = TmaLayout<Codec, kOp>;
+  const void* k = reinterpret_cast<const void*>(&step_tma_kernel<Codec, kOp>);
+  static std::atomic<uint64_t> configured{0};  // one bit per device
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint64_t bit = 1ull << (dev & 63);
+  if (!(configured.load() & bit)) {
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(L::kSmem));
+    configured.fetch_or(bit);
   }
   const uint64_t groups = (p.n + kGroupVals - 1) / kGroupVals;
+  const uint64_t tiles = (p.n / kGroupVals / kTileGroups) * static_cast<uint64_t>(p.njobs);
+  const int grid = tma_grid(k, kTmaThreads, L::kSmem, tiles > 0 ? tiles : groups * p.njobs);
+  void* args[] = {const_cast<StepParams*>(&p)};
+  count_launch();
+  return cudaLaunchKernel(k, dim3(grid), dim3(kTmaThreads), args, L::kSmem, stream);
+}
+
+template <class Codec, int kOp>
+cudaError_t launch_op(const StepParams& p, cudaStream_t stream) {
+  const uint64_t groups = (p.n + kGroupVals - 1) / kGroupVals;
   if (groups == 0 || p.njobs == 0) return cudaSuccess;
+  if constexpr (Codec::kFastPath) {
+    if (p.vec_ok && p.fast_ok && p.tma_ok) return launch_tma<Codec, kOp>(p, stream);
+  }
+  const void* k = reinterpret_cast<const void*>(&step_kernel<Codec, kOp>);
   const int grid = stream_grid(k, groups);
   void* args[] = {const_cast<StepParams*>(&p)};
   count_launch();
   return cudaLaunchKernel(k, dim3(grid), dim3(kStepThreads), args, 0, stream);
+}
+
+template <class Codec>
+cudaError_t launch_codec_step(int op, const StepParams& p, cudaStream_t stream) {
+  switch (op) {
+    case kOpEncode: return launch_op<Codec, kOpEncode>(p, stream);
+    case kOpDecode: return launch_op<Codec, kOpDecode>(p, stream);
+    case kOpDAR: return launch_op<Codec, kOpDAR>(p, stream);
+    case kOpDecodeAdd: return launch_op<Codec, kOpDecodeAdd>(p, stream);
+    default: return cudaErrorInvalidValue;
+  }
 }
 
 }  // namespace hccx
