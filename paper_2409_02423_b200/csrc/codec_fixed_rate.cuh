@@ -121,6 +121,15 @@ struct FixedRateCodec {
   // whole words with funnel shifts (plus the boundary word carrying the next
   // block's header); lane 0 also emits word 0.
   __device__ __forceinline__ static void store_fast(const Lane& s, uint32_t* gw, int lane) {
+    store_words<0>(s, gw, lane);
+  }
+  // Same layout into shared memory (or any generic address).
+  __device__ __forceinline__ static void store_fast_generic(const Lane& s, uint32_t* gw, int lane) {
+    store_words<2>(s, gw, lane);
+  }
+
+  template <int kDst>
+  __device__ __forceinline__ static void store_words(const Lane& s, uint32_t* gw, int lane) {
     static_assert(kFastPath, "fast path needs R % 4 == 0");
     constexpr int R4 = R / 4;
     const int k = lane >> 3, l = lane & 7;
@@ -130,7 +139,7 @@ struct FixedRateCodec {
       const int a = k + 1;
       uint32_t* dst = gw + 2 * R * k + R4 * l + 1;
 #pragma unroll
-      for (int q = 1; q < R4; ++q) stg_u32(dst + q - 1, __funnelshift_r(s.d[q - 1], s.d[q], 8 * (4 - a)));
+      for (int q = 1; q < R4; ++q) st_word<kDst>(dst + q - 1, __funnelshift_r(s.d[q - 1], s.d[q], 8 * (4 - a)));
       uint32_t last;
       if (l < 7) {
         last = __funnelshift_r(s.d[R4 - 1], nxt0, 8 * (4 - a));
@@ -138,12 +147,12 @@ struct FixedRateCodec {
         last = (s.d[R4 - 1] >> (8 * (4 - a))) | (nxth << (8 * a));
         if (a < 3) last |= nxt0 << (8 * (a + 1));
       }
-      stg_u32(dst + R4 - 1, last);
-      if (lane == 0) stg_u32(gw, s.hdr | (s.d[0] << 8));
+      st_word<kDst>(dst + R4 - 1, last);
+      if (lane == 0) st_word<kDst>(gw, s.hdr | (s.d[0] << 8));
     } else {
       uint32_t* dst = gw + 6 * R + 1 + R4 * l;
 #pragma unroll
-      for (int q = 0; q < R4; ++q) stg_u32(dst + q, s.d[q]);
+      for (int q = 0; q < R4; ++q) st_word<kDst>(dst + q, s.d[q]);
     }
   }
 

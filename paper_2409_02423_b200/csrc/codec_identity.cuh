@@ -41,6 +41,11 @@ struct IdentityCodec {
   struct Raw {
     float v[8];
   };
+  __device__ __forceinline__ static void store_fast_generic(const Lane& s, uint32_t* gw, int lane) {
+    uint4* w = reinterpret_cast<uint4*>(gw + 8 * lane);
+    w[0] = make_uint4(s.d[0], s.d[1], s.d[2], s.d[3]);
+    w[1] = make_uint4(s.d[4], s.d[5], s.d[6], s.d[7]);
+  }
   template <int kSrc>
   __device__ __forceinline__ static void load_raw(Raw& r, const uint32_t* gw, int lane) {
     ld_vals<kSrc>(reinterpret_cast<const float*>(gw) + 8 * lane, r.v);

@@ -277,6 +277,11 @@ struct ZfpRateCodec {
 #pragma unroll
     for (int q = 0; q < R4; ++q) stg_u32(gw + R4 * lane + q, s.d[q]);
   }
+  __device__ __forceinline__ static void store_fast_generic(const Lane& s, uint32_t* gw, int lane) {
+    constexpr int R4 = R / 4;
+#pragma unroll
+    for (int q = 0; q < R4; ++q) gw[R4 * lane + q] = s.d[q];
+  }
   struct Raw {
     uint32_t w[kFastPath ? R / 4 : 1];
   };

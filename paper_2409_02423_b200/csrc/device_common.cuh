@@ -86,6 +86,12 @@ __device__ __forceinline__ void ld_vals(const float* p, float (&v)[8]) {
   }
 }
 
+template <int kDst>
+__device__ __forceinline__ void st_word(uint32_t* p, uint32_t v) {
+  if constexpr (kDst == 0) stg_u32(p, v);
+  else *p = v;
+}
+
 // ---- flags (system scope: visible across NVLink peers) ---------------------
 
 __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {

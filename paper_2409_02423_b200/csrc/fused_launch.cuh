@@ -1,0 +1,28 @@
+// fused_launch.cuh -- cooperative launch of ring_fused_kernel<Codec>; included
+// by the per-rate-range translation units.
+#pragma once
+#include <atomic>
+#include <mutex>
+#include <unordered_map>
+
+#include "ring_fused.cuh"
+
+namespace hccx {
+
+// Co-resident CTAs of the fused kernel on this device (cooperative-launch cap).
+int fused_capacity(const void* kernel);
+
+template <class Codec>
+cudaError_t launch_fused_codec(const FusedParams& p, cudaStream_t stream) {
+  const void* k = reinterpret_cast<const void*>(&ring_fused_kernel<Codec>);
+  const uint64_t groups = (p.n_chunk + kGroupVals - 1) / kGroupVals;
+  const uint64_t nseg = (groups + kSegGroups - 1) / kSegGroups;
+  if (nseg == 0) return cudaSuccess;
+  const uint64_t cap = static_cast<uint64_t>(fused_capacity(k));
+  const int grid = static_cast<int>(nseg < cap ? nseg : cap);
+  void* args[] = {const_cast<FusedParams*>(&p)};
+  count_launch();
+  return cudaLaunchCooperativeKernel(k, dim3(grid), dim3(kFusedThreads), args, 0, stream);
+}
+
+}  // namespace hccx
