@@ -104,12 +104,12 @@ extern "C" hccx_status_t hccx_comm_create(int rank, int nranks, int device, uint
   c->chunk_cap = align_up((max_n + nranks - 1) / nranks, kSegVals);
   c->slot_bytes = align_up((c->chunk_cap / 64) * 257, 256);
   c->max_seg = static_cast<uint32_t>(c->chunk_cap / kSegVals);
-  const uint64_t nslots = 6ull * nranks - 2;  // data flags + consumption acks (ring_fused.cuh)
+  const uint64_t nslots = 3ull * nranks - 1;  // data-flag slots; the acks use kAckIdx per slot
   c->rs_off = 0;
   c->ag_off = c->rs_off + (nranks - 1) * c->slot_bytes;
   c->pp_off = c->ag_off + nranks * c->slot_bytes;
   c->flag_off = c->pp_off + nranks * c->slot_bytes;
-  c->win_bytes = c->flag_off + align_up(nslots * c->max_seg * 4, 256);
+  c->win_bytes = c->flag_off + align_up(nslots * (c->max_seg + kAckIdx) * 4, 256);
   if (cudaMalloc(&c->win, c->win_bytes) != cudaSuccess || cudaMalloc(&c->d_err, 4) != cudaSuccess) {
     cudaFree(c->win);
     delete c;

@@ -62,20 +62,31 @@ struct FusedSmem {
   uint8_t stage[kFusedWarps][kStageBytes];
 };
 
-// Flag classes in every window (max_seg u32 flags per slot):
-//   0 rs[t]      data ready, written by the left neighbour      (p-1 slots)
-//   1 ag[i]      data ready, written by rank i                  (p)
-//   2 pp[i]      data ready, written by rank i                  (p)
-//   3 ack_rs[t]  slot rs[t] of the RIGHT neighbour consumed     (p-1)
-//   4 ack_ag[r]  receiver r consumed our ag slot in its window  (p)
-//   5 ack_pp[r]  receiver r consumed our pp slot in its window  (p)
-// Senders wait on the ack of the slot's previous use before overwriting it,
-// so back-to-back collectives never race a slow receiver.
-__device__ __forceinline__ uint32_t* flag_ptr(const FusedParams& P, int rank, int cls, int slot, uint32_t seg) {
+// Flag classes in every window:
+//   0 rs[t]      data ready, written by the left neighbour      (p-1 slots x max_seg)
+//   1 ag[i]      data ready, written by rank i                  (p x max_seg)
+//   2 pp[i]      data ready, written by rank i                  (p x max_seg)
+//   3 ack_rs[t]  rs[t] of the RIGHT neighbour consumed           (p-1 x kAckIdx)
+//   4 ack_ag[r]  receiver r consumed our shard in its ag slot   (p x kAckIdx)
+//   5 ack_pp[r]  receiver r consumed our pp message              (p x kAckIdx)
+// Acks are per CTA index, not per segment: after a receiver CTA b (grid G)
+// has consumed all of its segments of a slot it acks every index b, b+G, ...
+// below kAckIdx, so each call acks the whole index space whatever its grid.
+// A sender CTA waits once per slot per call on its own index's ack of the
+// slot's previous use before overwriting it -- back-to-back collectives
+// never race a slow receiver.
+constexpr uint32_t kAckIdx = 2048;  // > any co-resident grid (148 SMs x 8 CTAs)
+
+__device__ __forceinline__ uint32_t* flag_ptr(const FusedParams& P, int rank, int cls, int slot, uint32_t idx) {
   const int p = P.p;
-  const int base[6] = {0, p - 1, 2 * p - 1, 3 * p - 1, 4 * p - 2, 5 * p - 2};
-  return reinterpret_cast<uint32_t*>(P.win[rank] + P.flag_off) +
-         static_cast<uint64_t>(base[cls] + slot) * P.max_seg + seg;
+  uint32_t* f = reinterpret_cast<uint32_t*>(P.win[rank] + P.flag_off);
+  if (cls < 3) {
+    const int base[3] = {0, p - 1, 2 * p - 1};
+    return f + static_cast<uint64_t>(base[cls] + slot) * P.max_seg + idx;
+  }
+  const int base[3] = {0, p - 1, 2 * p - 1};
+  return f + static_cast<uint64_t>(3 * p - 1) * P.max_seg + static_cast<uint64_t>(base[cls - 3] + slot) * kAckIdx +
+         idx;
 }
 
 __device__ __forceinline__ uint8_t* slot_ptr(const FusedParams& P, int rank, int slot_class, int slot) {
@@ -125,9 +136,12 @@ __device__ __forceinline__ void signal(uint32_t* flag, uint32_t epoch) {
   st_release_sys(flag, epoch);
 }
 
-// Consumption ack: the reads of this segment (all warps, ordered by the
-// preceding barrier) happen before the release store.
-__device__ __forceinline__ void ack(uint32_t* flag, uint32_t epoch) { st_release_sys(flag, epoch); }
+// Consumption ack for this CTA's indices (see kAckIdx).  Call after a CTA
+// barrier that follows the last read of the slot.
+__device__ __forceinline__ void ack_all(uint32_t* flags, uint32_t epoch) {
+  for (uint32_t k = blockIdx.x + threadIdx.x * gridDim.x; k < kAckIdx; k += gridDim.x * blockDim.x)
+    st_release_sys(flags + k, epoch);
+}
 
 // One warp's group of a segment.
 //   kEnc  : values (src_vals [+ local]) -> encoded group written into the
@@ -202,16 +216,16 @@ __global__ void __launch_bounds__(kFusedThreads) ring_fused_kernel(const __grid_
     const bool ar = P.op == kFAllReduce;
     for (int t = 0; t < p; ++t) {  // t = p-1 is the final receive
       const bool last = t == p - 1;
+      // credit for the slot(s) this round pushes into (previous use consumed)
+      if (threadIdx.x == 0) {
+        if (!last) spin_ge(P, flag_ptr(P, j, 3, t, blockIdx.x), P.prev_rs);
+        if (last && ar)
+          for (int q = 1; q < p; ++q) spin_ge(P, flag_ptr(P, j, 4, (j + q) % p, blockIdx.x), P.prev_ag);
+      }
       for (uint32_t sg = blockIdx.x; sg < nseg; sg += gridDim.x) {
         const uint64_t soff = static_cast<uint64_t>(sg) * kSegGroups * GB;
         const uint64_t g = static_cast<uint64_t>(sg) * kSegGroups + warp;
-        // inbound data of round t-1, and credit for the slot we push into
-        if (threadIdx.x == 0) {
-          if (t > 0) spin_ge(P, flag_ptr(P, j, 0, t - 1, sg), P.epoch);
-          if (!last) spin_ge(P, flag_ptr(P, j, 3, t, sg), P.prev_rs);
-          if (last && ar)
-            for (int q = 1; q < p; ++q) spin_ge(P, flag_ptr(P, j, 4, (j + q) % p, sg), P.prev_ag);
-        }
+        if (threadIdx.x == 0 && t > 0) spin_ge(P, flag_ptr(P, j, 0, t - 1, sg), P.epoch);
         __syncthreads();
         const uint8_t* rx = t > 0 ? slot_ptr(P, j, 0, t - 1) : nullptr;
         const float* local = chunk_in(j - 1 - t);
@@ -228,7 +242,6 @@ __global__ void __launch_bounds__(kFusedThreads) ring_fused_kernel(const __grid_
           }
         }
         __syncthreads();
-        if (t > 0 && threadIdx.x == 0) ack(flag_ptr(P, left, 3, t - 1, sg), P.epoch);
         if (last && !ar) continue;  // reduce-scatter: the shard is fp32, nothing to push
         const uint32_t nb = seg_bytes(sg);
         if (!last) {
@@ -242,6 +255,10 @@ __global__ void __launch_bounds__(kFusedThreads) ring_fused_kernel(const __grid_
         }
         __syncthreads();
       }
+      if (t > 0) {
+        __syncthreads();
+        ack_all(flag_ptr(P, left, 3, t - 1, 0), P.epoch);
+      }
     }
     if (ar) {
       for (int q = 1; q < p; ++q) {
@@ -252,9 +269,9 @@ __global__ void __launch_bounds__(kFusedThreads) ring_fused_kernel(const __grid_
           if (g < ngroups)
             fused_group<Codec, false, false>(P, slot_ptr(P, j, 1, i), nullptr, nullptr, chunk_out(i), false,
                                              nullptr, g, sm, lane, bad);
-          __syncthreads();
-          if (threadIdx.x == 0) ack(flag_ptr(P, i, 4, j, sg), P.epoch);
         }
+        __syncthreads();
+        ack_all(flag_ptr(P, i, 4, j, 0), P.epoch);
       }
     }
   } else {
@@ -265,16 +282,16 @@ __global__ void __launch_bounds__(kFusedThreads) ring_fused_kernel(const __grid_
     const bool origin = ag || j == P.root;
     float* own_out = ag ? P.out + static_cast<uint64_t>(j) * c : (P.op == kFBroadcast ? P.out : nullptr);
     if (origin) {
+      if (threadIdx.x == 0) {
+        for (int q = 1; q < p; ++q) {
+          const int d = (j + q) % p;
+          if (P.op == kFP2P && d != P.dst) continue;
+          spin_ge(P, flag_ptr(P, j, ag ? 4 : 5, d, blockIdx.x), ag ? P.prev_ag : P.pp_epoch[d] - 1u);
+        }
+      }
+      __syncthreads();
       for (uint32_t sg = blockIdx.x; sg < nseg; sg += gridDim.x) {
         const uint64_t soff = static_cast<uint64_t>(sg) * kSegGroups * GB;
-        if (threadIdx.x == 0) {
-          for (int q = 1; q < p; ++q) {
-            const int d = (j + q) % p;
-            if (P.op == kFP2P && d != P.dst) continue;
-            spin_ge(P, flag_ptr(P, j, ag ? 4 : 5, d, sg), ag ? P.prev_ag : P.pp_epoch[d] - 1u);
-          }
-        }
-        __syncthreads();
         const uint64_t g = static_cast<uint64_t>(sg) * kSegGroups + warp;
         if (g < ngroups)
           fused_group<Codec, true, false>(P, nullptr, P.in, nullptr, own_out, false, tile + warp * GB, g, sm, lane,
@@ -308,9 +325,9 @@ __global__ void __launch_bounds__(kFusedThreads) ring_fused_kernel(const __grid_
         if (g < ngroups)
           fused_group<Codec, false, false>(P, slot_ptr(P, j, cls, i), nullptr, nullptr, dst, true, nullptr, g, sm,
                                            lane, bad);
-        __syncthreads();
-        if (threadIdx.x == 0) ack(flag_ptr(P, i, ag ? 4 : 5, j, sg), ep);
       }
+      __syncthreads();
+      ack_all(flag_ptr(P, i, ag ? 4 : 5, j, 0), ep);
     }
   }
   if constexpr (Codec::kCheckFinite) {
