@@ -34,6 +34,7 @@ constexpr int kFusedWarps = 8;
 constexpr int kFusedThreads = kFusedWarps * 32;
 constexpr int kSegGroups = kFusedWarps;  // groups per segment
 constexpr uint32_t kSegVals = kSegGroups * kGroupVals;
+constexpr uint32_t kStepSegs = 16;  // segments per published step (one fence + flag)
 
 enum FusedOp : int { kFAllReduce = 0, kFReduceScatter = 1, kFAllGather = 2, kFBroadcast = 3, kFP2P = 4 };
 
@@ -212,48 +213,63 @@ __global__ void __launch_bounds__(kFusedThreads) ring_fused_kernel(const __grid_
   };
   const int right = (j + 1) % p, left = (j + p - 1) % p;
 
+  // This CTA's segments are sg = blockIdx.x + k*G, k < myseg.  They are
+  // processed in steps of kStepSegs segments; a step is published with ONE
+  // system-scope fence + flag (indexed by the step's first segment), which
+  // amortises the fence over up to kStepSegs x 8 groups.
+  const uint32_t G = gridDim.x;
+  const uint32_t myseg = nseg > blockIdx.x ? (nseg - blockIdx.x + G - 1) / G : 0;
+  auto seg_of = [&](uint32_t k) { return blockIdx.x + k * G; };
+
   if (P.op == kFAllReduce || P.op == kFReduceScatter) {
     const bool ar = P.op == kFAllReduce;
     for (int t = 0; t < p; ++t) {  // t = p-1 is the final receive
       const bool last = t == p - 1;
+      const bool push = !(last && !ar);
       // credit for the slot(s) this round pushes into (previous use consumed)
       if (threadIdx.x == 0) {
         if (!last) spin_ge(P, flag_ptr(P, j, 3, t, blockIdx.x), P.prev_rs);
         if (last && ar)
           for (int q = 1; q < p; ++q) spin_ge(P, flag_ptr(P, j, 4, (j + q) % p, blockIdx.x), P.prev_ag);
       }
-      for (uint32_t sg = blockIdx.x; sg < nseg; sg += gridDim.x) {
-        const uint64_t soff = static_cast<uint64_t>(sg) * kSegGroups * GB;
-        const uint64_t g = static_cast<uint64_t>(sg) * kSegGroups + warp;
-        if (threadIdx.x == 0 && t > 0) spin_ge(P, flag_ptr(P, j, 0, t - 1, sg), P.epoch);
+      const uint8_t* rx = t > 0 ? slot_ptr(P, j, 0, t - 1) : nullptr;
+      const float* local = chunk_in(j - 1 - t);
+      for (uint32_t k0 = 0; k0 < myseg; k0 += kStepSegs) {
+        const uint32_t k1 = min(k0 + kStepSegs, myseg);
+        if (threadIdx.x == 0 && t > 0) spin_ge(P, flag_ptr(P, j, 0, t - 1, seg_of(k0)), P.epoch);
         __syncthreads();
-        const uint8_t* rx = t > 0 ? slot_ptr(P, j, 0, t - 1) : nullptr;
-        const float* local = chunk_in(j - 1 - t);
-        if (g < ngroups) {
-          if (last && !ar) {
-            fused_group<Codec, false, true>(P, rx, nullptr, local, P.out, true, nullptr, g, sm, lane, bad);
-          } else {
-            uint8_t* tg = tile + warp * GB;
-            float* ov = last ? chunk_out(j) : nullptr;
-            if (t == 0)
-              fused_group<Codec, true, false>(P, nullptr, local, nullptr, ov, false, tg, g, sm, lane, bad);
-            else
-              fused_group<Codec, true, true>(P, rx, nullptr, local, ov, false, tg, g, sm, lane, bad);
+        for (uint32_t k = k0; k < k1; ++k) {
+          const uint32_t sg = seg_of(k);
+          const uint64_t g = static_cast<uint64_t>(sg) * kSegGroups + warp;
+          if (g < ngroups) {
+            if (!push) {
+              fused_group<Codec, false, true>(P, rx, nullptr, local, P.out, true, nullptr, g, sm, lane, bad);
+            } else {
+              uint8_t* tg = tile + warp * GB;
+              float* ov = last ? chunk_out(j) : nullptr;
+              if (t == 0)
+                fused_group<Codec, true, false>(P, nullptr, local, nullptr, ov, false, tg, g, sm, lane, bad);
+              else
+                fused_group<Codec, true, true>(P, rx, nullptr, local, ov, false, tg, g, sm, lane, bad);
+            }
+          }
+          if (!push) continue;  // reduce-scatter final: fp32 shard, nothing to push
+          __syncthreads();
+          const uint64_t soff = static_cast<uint64_t>(sg) * kSegGroups * GB;
+          const uint32_t nb = seg_bytes(sg);
+          if (!last)
+            push_tile(tile, slot_ptr(P, right, 0, t) + soff, nb);
+          else
+            for (int q = 1; q < p; ++q) push_tile(tile, slot_ptr(P, (j + q) % p, 1, j) + soff, nb);
+          __syncthreads();
+        }
+        if (push) {
+          if (!last) {
+            if (threadIdx.x == 0) signal(flag_ptr(P, right, 0, t, seg_of(k0)), P.epoch);
+          } else if (threadIdx.x < p - 1) {
+            signal(flag_ptr(P, (j + 1 + threadIdx.x) % p, 1, j, seg_of(k0)), P.epoch);
           }
         }
-        __syncthreads();
-        if (last && !ar) continue;  // reduce-scatter: the shard is fp32, nothing to push
-        const uint32_t nb = seg_bytes(sg);
-        if (!last) {
-          push_tile(tile, slot_ptr(P, right, 0, t) + soff, nb);
-          __syncthreads();
-          if (threadIdx.x == 0) signal(flag_ptr(P, right, 0, t, sg), P.epoch);
-        } else {
-          for (int q = 1; q < p; ++q) push_tile(tile, slot_ptr(P, (j + q) % p, 1, j) + soff, nb);
-          __syncthreads();
-          if (threadIdx.x < p - 1) signal(flag_ptr(P, (j + 1 + threadIdx.x) % p, 1, j, sg), P.epoch);
-        }
-        __syncthreads();
       }
       if (t > 0) {
         __syncthreads();
@@ -263,12 +279,15 @@ __global__ void __launch_bounds__(kFusedThreads) ring_fused_kernel(const __grid_
     if (ar) {
       for (int q = 1; q < p; ++q) {
         const int i = (j - q + p) % p;
-        for (uint32_t sg = blockIdx.x; sg < nseg; sg += gridDim.x) {
-          seg_wait(P, flag_ptr(P, j, 1, i, sg), P.epoch);
-          const uint64_t g = static_cast<uint64_t>(sg) * kSegGroups + warp;
-          if (g < ngroups)
-            fused_group<Codec, false, false>(P, slot_ptr(P, j, 1, i), nullptr, nullptr, chunk_out(i), false,
-                                             nullptr, g, sm, lane, bad);
+        for (uint32_t k0 = 0; k0 < myseg; k0 += kStepSegs) {
+          const uint32_t k1 = min(k0 + kStepSegs, myseg);
+          seg_wait(P, flag_ptr(P, j, 1, i, seg_of(k0)), P.epoch);
+          for (uint32_t k = k0; k < k1; ++k) {
+            const uint64_t g = static_cast<uint64_t>(seg_of(k)) * kSegGroups + warp;
+            if (g < ngroups)
+              fused_group<Codec, false, false>(P, slot_ptr(P, j, 1, i), nullptr, nullptr, chunk_out(i), false,
+                                               nullptr, g, sm, lane, bad);
+          }
         }
         __syncthreads();
         ack_all(flag_ptr(P, i, 4, j, 0), P.epoch);
@@ -290,27 +309,29 @@ __global__ void __launch_bounds__(kFusedThreads) ring_fused_kernel(const __grid_
         }
       }
       __syncthreads();
-      for (uint32_t sg = blockIdx.x; sg < nseg; sg += gridDim.x) {
-        const uint64_t soff = static_cast<uint64_t>(sg) * kSegGroups * GB;
-        const uint64_t g = static_cast<uint64_t>(sg) * kSegGroups + warp;
-        if (g < ngroups)
-          fused_group<Codec, true, false>(P, nullptr, P.in, nullptr, own_out, false, tile + warp * GB, g, sm, lane,
-                                          bad);
-        __syncthreads();
-        const uint32_t nb = seg_bytes(sg);
-        if (P.op == kFP2P) {
-          push_tile(tile, slot_ptr(P, P.dst, cls, j) + soff, nb);
+      for (uint32_t k0 = 0; k0 < myseg; k0 += kStepSegs) {
+        const uint32_t k1 = min(k0 + kStepSegs, myseg);
+        for (uint32_t k = k0; k < k1; ++k) {
+          const uint32_t sg = seg_of(k);
+          const uint64_t g = static_cast<uint64_t>(sg) * kSegGroups + warp;
+          if (g < ngroups)
+            fused_group<Codec, true, false>(P, nullptr, P.in, nullptr, own_out, false, tile + warp * GB, g, sm,
+                                            lane, bad);
           __syncthreads();
-          if (threadIdx.x == 0) signal(flag_ptr(P, P.dst, cls, j, sg), P.pp_epoch[P.dst]);
-        } else {
-          for (int q = 1; q < p; ++q) push_tile(tile, slot_ptr(P, (j + q) % p, cls, j) + soff, nb);
+          const uint64_t soff = static_cast<uint64_t>(sg) * kSegGroups * GB;
+          const uint32_t nb = seg_bytes(sg);
+          if (P.op == kFP2P)
+            push_tile(tile, slot_ptr(P, P.dst, cls, j) + soff, nb);
+          else
+            for (int q = 1; q < p; ++q) push_tile(tile, slot_ptr(P, (j + q) % p, cls, j) + soff, nb);
           __syncthreads();
-          if (threadIdx.x < p - 1) {
-            const int d = (j + 1 + threadIdx.x) % p;
-            signal(flag_ptr(P, d, cls, j, sg), ag ? P.epoch : P.pp_epoch[d]);
-          }
         }
-        __syncthreads();
+        if (P.op == kFP2P) {
+          if (threadIdx.x == 0) signal(flag_ptr(P, P.dst, cls, j, seg_of(k0)), P.pp_epoch[P.dst]);
+        } else if (threadIdx.x < p - 1) {
+          const int d = (j + 1 + threadIdx.x) % p;
+          signal(flag_ptr(P, d, cls, j, seg_of(k0)), ag ? P.epoch : P.pp_epoch[d]);
+        }
       }
     }
     for (int q = 1; q < p; ++q) {
@@ -319,12 +340,15 @@ __global__ void __launch_bounds__(kFusedThreads) ring_fused_kernel(const __grid_
       if (P.op == kFP2P && j != P.dst) continue;
       const uint32_t ep = ag ? P.epoch : P.pp_epoch[i];
       float* dst = ag ? P.out + static_cast<uint64_t>(i) * c : P.out;
-      for (uint32_t sg = blockIdx.x; sg < nseg; sg += gridDim.x) {
-        seg_wait(P, flag_ptr(P, j, cls, i, sg), ep);
-        const uint64_t g = static_cast<uint64_t>(sg) * kSegGroups + warp;
-        if (g < ngroups)
-          fused_group<Codec, false, false>(P, slot_ptr(P, j, cls, i), nullptr, nullptr, dst, true, nullptr, g, sm,
-                                           lane, bad);
+      for (uint32_t k0 = 0; k0 < myseg; k0 += kStepSegs) {
+        const uint32_t k1 = min(k0 + kStepSegs, myseg);
+        seg_wait(P, flag_ptr(P, j, cls, i, seg_of(k0)), ep);
+        for (uint32_t k = k0; k < k1; ++k) {
+          const uint64_t g = static_cast<uint64_t>(seg_of(k)) * kSegGroups + warp;
+          if (g < ngroups)
+            fused_group<Codec, false, false>(P, slot_ptr(P, j, cls, i), nullptr, nullptr, dst, true, nullptr, g,
+                                             sm, lane, bad);
+        }
       }
       __syncthreads();
       ack_all(flag_ptr(P, i, ag ? 4 : 5, j, 0), ep);
