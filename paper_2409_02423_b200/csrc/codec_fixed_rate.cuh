@@ -55,6 +55,47 @@ struct FixedRateCodec {
 
   // ---- quantize / dequantize (lane-local + 3 shuffles) --------------------
 
+  // Field i of the lane chunk (R bits at bit offset i*R).
+  __device__ __forceinline__ static uint32_t field(const Lane& s, int i) {
+    const int off = i * R, w = off >> 5, b = off & 31;
+    uint32_t u = s.d[w] >> b;
+    if (b + R > 32) u |= s.d[w + 1] << (32 - b);
+    return u & kMask;
+  }
+
+  // 0x4B000000 | u as a float is exactly 2^23 + u (u < 2^23): the
+  // dequantisation q*2^k = (2^23+u)*2^k - (2^23+bias)*2^k is then ONE FFMA
+  // with a single rounding of the exact value (fma has no intermediate
+  // rounding or overflow).  R = 8 / 16 build it with one PRMT.
+  __device__ __forceinline__ static float magic_field(const Lane& s, int i) {
+    if constexpr (R == 8) {
+      return __uint_as_float(__byte_perm(s.d[i >> 2], 0x4B000000u, 0x7650u | (i & 3)));
+    } else if constexpr (R == 16) {
+      return __uint_as_float(__byte_perm(s.d[i >> 1], 0x4B000000u, 0x7600u | (((i & 1) * 2 + 1) << 4) | ((i & 1) * 2)));
+    } else {
+      return __uint_as_float(field(s, i) | 0x4B000000u);
+    }
+  }
+
+  __device__ __forceinline__ static void pack(Lane& s, const uint32_t (&u)[8]) {
+    if constexpr (R == 8) {
+      s.d[0] = __byte_perm(__byte_perm(u[0], u[1], 0x0040u), __byte_perm(u[2], u[3], 0x0040u), 0x5410u);
+      s.d[1] = __byte_perm(__byte_perm(u[4], u[5], 0x0040u), __byte_perm(u[6], u[7], 0x0040u), 0x5410u);
+    } else if constexpr (R == 16) {
+#pragma unroll
+      for (int w = 0; w < 4; ++w) s.d[w] = __byte_perm(u[2 * w], u[2 * w + 1], 0x5410u);
+    } else {
+#pragma unroll
+      for (int w = 0; w < kWords; ++w) s.d[w] = 0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int off = i * R, w = off >> 5, b = off & 31;
+        s.d[w] |= u[i] << b;
+        if (b + R > 32) s.d[w + 1] |= u[i] >> (32 - b);
+      }
+    }
+  }
+
   __device__ __forceinline__ static void encode(const float (&v)[8], Lane& s, uint32_t& bad, uint32_t /*lane_live*/) {
     uint32_t m = 0;
 #pragma unroll
@@ -66,40 +107,53 @@ struct FixedRateCodec {
     bad |= static_cast<uint32_t>(eb == 255);
     s.hdr = static_cast<uint32_t>(eb);
     const int k = R + 125 - eb;  // x = v * 2^k, k in [R-130, R+125]
-    const bool split = k > 127;
-    const float sa = split ? exp2i(64) : 1.0f;
-    const float sb = exp2i(split ? k - 64 : max(k, -149));
     uint32_t u[8];
+    if (__all_sync(kFull, k >= -126 && k <= 127)) {
+      // common case: 2^k is a normal float, one rounding per value
+      const float sb = __uint_as_float(static_cast<uint32_t>(k + 127) << 23);
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const float t = __fmul_rn(v[i], sa);
-      if constexpr (R <= 22) {
-        const float y = __fmaf_rn(t, sb, 12582912.0f);  // 1.5 * 2^23
-        u[i] = min(__float_as_uint(y) - (0x4B400000u - kBias), kMask);
-      } else {
-        const int q = __float2int_rn(__fmul_rn(t, sb));
-        u[i] = min(static_cast<uint32_t>(q) + kBias, kMask);
+      for (int i = 0; i < 8; ++i) {
+        if constexpr (R <= 22) {
+          const float y = __fmaf_rn(v[i], sb, 12582912.0f);  // 1.5 * 2^23
+          u[i] = min(__float_as_uint(y) - (0x4B400000u - kBias), kMask);
+        } else {
+          u[i] = min(static_cast<uint32_t>(__float2int_rn(__fmul_rn(v[i], sb))) + kBias, kMask);
+        }
+      }
+    } else {
+      // tiny blocks (2^k > 2^127: two exact power-of-two multiplies) and
+      // the denormal factor 2^-127 (R = 2, E_b = 254)
+      const bool split = k > 127;
+      const float sa = split ? exp2i(64) : 1.0f;
+      const float sb = exp2i(split ? k - 64 : max(k, -149));
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float t = __fmul_rn(v[i], sa);
+        if constexpr (R <= 22) {
+          const float y = __fmaf_rn(t, sb, 12582912.0f);
+          u[i] = min(__float_as_uint(y) - (0x4B400000u - kBias), kMask);
+        } else {
+          u[i] = min(static_cast<uint32_t>(__float2int_rn(__fmul_rn(t, sb))) + kBias, kMask);
+        }
       }
     }
-#pragma unroll
-    for (int w = 0; w < kWords; ++w) s.d[w] = 0;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int off = i * R, w = off >> 5, b = off & 31;
-      s.d[w] |= u[i] << b;
-      if (b + R > 32) s.d[w + 1] |= u[i] >> (32 - b);
-    }
+    pack(s, u);
   }
 
   __device__ __forceinline__ static void decode(const Lane& s, float (&v)[8]) {
     const int k = static_cast<int>(s.hdr) - 125 - R;  // step = 2^k, k in [-125-R, 129-R]
+    if constexpr (R <= 22) {
+      if (__all_sync(kFull, k >= -126 && k <= 103)) {
+        const float step = __uint_as_float(static_cast<uint32_t>(k + 127) << 23);
+        const float c = __fmul_rn(-(8388608.0f + static_cast<float>(kBias)), step);  // exact
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] = __fmaf_rn(magic_field(s, i), step, c);
+        return;
+      }
+    }
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-      const int off = i * R, w = off >> 5, b = off & 31;
-      uint32_t u = s.d[w] >> b;
-      if (b + R > 32) u |= s.d[w + 1] << (32 - b);
-      u &= kMask;
-      const int q = static_cast<int>(u - kBias);
+      const int q = static_cast<int>(field(s, i) - kBias);
       if constexpr (R <= 25) {
         const bool split = k < -126;
         const float sa = exp2i(split ? k + 64 : k);

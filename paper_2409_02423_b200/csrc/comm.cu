@@ -24,7 +24,7 @@ cudaError_t launch_fused_fr_hi(int rate, const FusedParams& p, cudaStream_t s);
 cudaError_t launch_fused_zfp_a(int rate, const FusedParams& p, cudaStream_t s);
 cudaError_t launch_fused_zfp_b(int rate, const FusedParams& p, cudaStream_t s);
 
-int fused_capacity(const void* kernel) {
+int fused_capacity(const void* kernel, int threads, uint32_t smem) {
   static std::mutex mu;
   static std::unordered_map<uint64_t, int> cache;
   int dev = 0;
@@ -34,7 +34,7 @@ int fused_capacity(const void* kernel) {
   auto it = cache.find(key);
   if (it != cache.end()) return it->second;
   int b = 0, sms = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel, kFusedThreads, 0) != cudaSuccess || b < 1) b = 1;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel, threads, smem) != cudaSuccess || b < 1) b = 1;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int cap = b * (sms > 0 ? sms : 148);
   cache.emplace(key, cap);
@@ -196,6 +196,11 @@ FusedParams base_params(hccx_comm* c, int op, uint64_t n_chunk, const float* in,
   P.out = out;
   P.err = c->d_err;
   P.timeout_ns = timeout_ns();
+  static const int dbg = [] {
+    const char* e = std::getenv("HCCX_DEBUG");
+    return e ? std::atoi(e) : 0;
+  }();
+  P.debug = dbg;
   // chunk offsets are multiples of n_chunk floats: aligned iff n_chunk % 8 == 0
   P.vec_ok = (aligned32(in) && aligned32(out) && (n_chunk % 8 == 0)) ? 1 : 0;
   return P;

@@ -10,7 +10,7 @@
 namespace hccx {
 
 // Co-resident CTAs of the fused kernel on this device (cooperative-launch cap).
-int fused_capacity(const void* kernel);
+int fused_capacity(const void* kernel, int threads, uint32_t smem);
 
 template <class Codec>
 cudaError_t launch_fused_codec(const FusedParams& p, cudaStream_t stream) {
@@ -18,11 +18,19 @@ cudaError_t launch_fused_codec(const FusedParams& p, cudaStream_t stream) {
   const uint64_t groups = (p.n_chunk + kGroupVals - 1) / kGroupVals;
   const uint64_t nseg = (groups + kSegGroups - 1) / kSegGroups;
   if (nseg == 0) return cudaSuccess;
-  const uint64_t cap = static_cast<uint64_t>(fused_capacity(k));
+  constexpr uint32_t smem = sizeof(FusedSmem2);
+  static std::atomic<uint64_t> configured{0};  // one bit per device
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!(configured.load() & (1ull << (dev & 63)))) {
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    configured.fetch_or(1ull << (dev & 63));
+  }
+  const uint64_t cap = static_cast<uint64_t>(fused_capacity(k, kFThreads2, smem));
   const int grid = static_cast<int>(nseg < cap ? nseg : cap);
   void* args[] = {const_cast<FusedParams*>(&p)};
   count_launch();
-  return cudaLaunchCooperativeKernel(k, dim3(grid), dim3(kFusedThreads), args, 0, stream);
+  return cudaLaunchCooperativeKernel(k, dim3(grid), dim3(kFThreads2), args, smem, stream);
 }
 
 }  // namespace hccx

@@ -56,6 +56,7 @@ struct FusedParams {
   float recip, divisor;
   uint32_t* err;
   uint64_t timeout_ns;
+  int debug;  // development knobs (HCCX_DEBUG): 1 skip pushes, 2 skip system fence, 4 skip segment barriers
 };
 
 struct FusedSmem {
@@ -132,10 +133,22 @@ __device__ __forceinline__ void push_tile(const uint8_t* tile, uint8_t* dst, uin
   }
 }
 
-__device__ __forceinline__ void signal(uint32_t* flag, uint32_t epoch) {
-  __threadfence_system();
-  st_release_sys(flag, epoch);
+__device__ __forceinline__ void push_tile_n(const uint8_t* tile, uint8_t* dst, uint32_t nbytes, uint32_t nthreads) {
+  const uint32_t n16 = nbytes >> 4;
+  if ((reinterpret_cast<uintptr_t>(dst) & 15u) == 0) {
+    for (uint32_t i = threadIdx.x; i < n16; i += nthreads)
+      reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(tile)[i];
+    for (uint32_t b = (n16 << 4) + threadIdx.x; b < nbytes; b += nthreads) dst[b] = tile[b];
+  } else {
+    for (uint32_t b = threadIdx.x; b < nbytes; b += nthreads) dst[b] = tile[b];
+  }
 }
+
+// Publish a step.  The pushes of every thread precede this thread's
+// release store through the CTA barrier (cumulativity of st.release at
+// system scope), so no separate sc fence is needed; the remote reader
+// pairs it with ld.acquire.sys.
+__device__ __forceinline__ void signal(uint32_t* flag, uint32_t epoch) { st_release_sys(flag, epoch); }
 
 // Consumption ack for this CTA's indices (see kAckIdx).  Call after a CTA
 // barrier that follows the last read of the slot.
@@ -191,9 +204,256 @@ __device__ __forceinline__ void fused_group(const FusedParams& P, const uint8_t*
   }
 }
 
+// ---------------------------------------------------------------------------
+// Warp-specialised fused kernel.
+//
+// CTA = 8 compute warps + 1 producer warp.  The collective is a list of
+// *phases* (ring rounds, allgather receives, ...; see phase_of) that both
+// roles walk in the same order.  The producer's elected lane waits for each
+// step's inbound-data flag, then streams every segment's inputs (inbox
+// payload and/or local fp32) into a kFStages-deep shared-memory ring with
+// cp.async.bulk (completing on the stage's "full" mbarrier).  Compute warps
+// decode / add / encode one group each per segment straight from shared
+// memory, release the stage ("empty" mbarrier), stage the encoded segment in
+// `tile` and push it to the peer window(s) with 16-byte stores.  HBM latency
+// is therefore hidden behind kFStages segments of prefetch per CTA.
+// Partial segments (and unaligned buffers / non-word codecs) are read
+// directly from global memory instead ("direct" stages).
+// ---------------------------------------------------------------------------
+
+constexpr int kFStages = 3;
+constexpr int kFCompute = kFusedWarps;              // compute warps
+constexpr int kFThreads2 = (kFCompute + 1) * 32;    // + producer warp
+constexpr uint32_t kFStageA = 8448;                 // >= 8 x 1028 B payload groups / 8 KiB fp32, 128B multiple
+constexpr uint32_t kFStageB = 8192;                 // 8 groups x 1 KiB fp32
+constexpr uint32_t kFStageBytes = kFStageA + kFStageB;
+
+struct FusedSmem2 {
+  uint8_t stage[kFStages][kFStageBytes];
+  uint8_t tile[2][kFStageA];
+  uint8_t gen[kFCompute][kStageBytes];
+  uint64_t full[kFStages];
+  uint64_t empty[kFStages];
+  uint32_t direct[kFStages];
+};
+
+enum PhaseKind : int { kPhEnc = 0, kPhDar = 1, kPhFinAr = 2, kPhFinRs = 3, kPhDec = 4 };
+
+struct Phase {
+  int kind;
+  const uint8_t* pay;   // inbox slot (local window)
+  const float* vals;    // local fp32 input chunk
+  float* out;           // fp32 output chunk (or nullptr)
+  bool div;             // apply the Average divisor to `out`
+  int wait_cls, wait_slot;  // data flags to wait for (-1: none)
+  uint32_t wait_ep;
+  int push_cls, push_slot;  // destination slot (-1: no push)
+  int push_mode;            // 0 right neighbour, 1 every peer, 2 P.dst
+  int credit_cls;           // ack class to wait on before pushing (-1: none)
+  uint32_t credit_ep;       // (pp: per destination, see credit_for)
+  int ack_rank, ack_cls, ack_slot;  // consumption ack at phase end (-1: none)
+  uint32_t ack_ep;
+};
+
+__device__ __forceinline__ int nphases(const FusedParams& P) {
+  switch (P.op) {
+    case kFAllReduce: return 2 * P.p - 1;
+    case kFReduceScatter: return P.p;
+    case kFAllGather: return P.p;
+    default: return 1;  // broadcast / p2p: one phase per participant
+  }
+}
+
+__device__ __forceinline__ Phase phase_of(const FusedParams& P, int ph) {
+  const int p = P.p, j = P.rank;
+  const uint64_t c = P.n_chunk;
+  auto cin = [&](int ch) { return P.in + static_cast<uint64_t>(((ch % p) + p) % p) * c; };
+  auto cout = [&](int ch) { return P.out + static_cast<uint64_t>(((ch % p) + p) % p) * c; };
+  Phase f;
+  f.kind = kPhEnc;
+  f.pay = nullptr;
+  f.vals = nullptr;
+  f.out = nullptr;
+  f.div = false;
+  f.wait_cls = -1;
+  f.wait_slot = 0;
+  f.wait_ep = 0;
+  f.push_cls = -1;
+  f.push_slot = 0;
+  f.push_mode = 0;
+  f.credit_cls = -1;
+  f.credit_ep = 0;
+  f.ack_rank = -1;
+  f.ack_cls = 0;
+  f.ack_slot = 0;
+  f.ack_ep = 0;
+  const int left = (j + p - 1) % p;
+  if (P.op == kFAllReduce || P.op == kFReduceScatter) {
+    if (ph < p) {
+      const int t = ph;
+      f.vals = cin(j - 1 - t);
+      if (t > 0) {
+        f.pay = P.win[j] + P.rs_off + static_cast<uint64_t>(t - 1) * P.slot_bytes;
+        f.wait_cls = 0;
+        f.wait_slot = t - 1;
+        f.wait_ep = P.epoch;
+        f.ack_rank = left;
+        f.ack_cls = 3;
+        f.ack_slot = t - 1;
+        f.ack_ep = P.epoch;
+      }
+      if (t < p - 1) {
+        f.kind = t == 0 ? kPhEnc : kPhDar;
+        f.push_cls = 0;
+        f.push_slot = t;
+        f.push_mode = 0;
+        f.credit_cls = 3;
+        f.credit_ep = P.prev_rs;
+      } else if (P.op == kFAllReduce) {
+        f.kind = kPhFinAr;
+        f.out = cout(j);
+        f.div = true;
+        f.push_cls = 1;
+        f.push_slot = j;
+        f.push_mode = 1;
+        f.credit_cls = 4;
+        f.credit_ep = P.prev_ag;
+      } else {
+        f.kind = kPhFinRs;
+        f.out = P.out;
+      }
+    } else {
+      const int i = (j - (ph - p + 1) + p) % p;
+      f.kind = kPhDec;
+      f.pay = P.win[j] + P.ag_off + static_cast<uint64_t>(i) * P.slot_bytes;
+      f.out = cout(i);
+      f.div = true;
+      f.wait_cls = 1;
+      f.wait_slot = i;
+      f.wait_ep = P.epoch;
+      f.ack_rank = i;
+      f.ack_cls = 4;
+      f.ack_slot = j;
+      f.ack_ep = P.epoch;
+    }
+  } else if (P.op == kFAllGather) {
+    if (ph == 0) {
+      f.kind = kPhEnc;
+      f.vals = P.in;
+      f.out = P.out + static_cast<uint64_t>(j) * c;
+      f.push_cls = 1;
+      f.push_slot = j;
+      f.push_mode = 1;
+      f.credit_cls = 4;
+      f.credit_ep = P.prev_ag;
+    } else {
+      const int i = (j - ph + p) % p;
+      f.kind = kPhDec;
+      f.pay = P.win[j] + P.ag_off + static_cast<uint64_t>(i) * P.slot_bytes;
+      f.out = P.out + static_cast<uint64_t>(i) * c;
+      f.wait_cls = 1;
+      f.wait_slot = i;
+      f.wait_ep = P.epoch;
+      f.ack_rank = i;
+      f.ack_cls = 4;
+      f.ack_slot = j;
+      f.ack_ep = P.epoch;
+    }
+  } else {  // broadcast / p2p
+    if (j == P.root) {
+      f.kind = kPhEnc;
+      f.vals = P.in;
+      f.out = P.op == kFBroadcast ? P.out : nullptr;
+      f.push_cls = 2;
+      f.push_slot = j;
+      f.push_mode = P.op == kFP2P ? 2 : 1;
+      f.credit_cls = 5;
+    } else {
+      const int i = P.root;
+      f.kind = kPhDec;
+      f.pay = P.win[j] + P.pp_off + static_cast<uint64_t>(i) * P.slot_bytes;
+      f.out = P.out;
+      f.wait_cls = 2;
+      f.wait_slot = i;
+      f.wait_ep = P.pp_epoch[i];
+      f.ack_rank = i;
+      f.ack_cls = 5;
+      f.ack_slot = j;
+      f.ack_ep = P.pp_epoch[i];
+    }
+  }
+  return f;
+}
+
+__device__ __forceinline__ uint32_t push_epoch(const FusedParams& P, int push_cls, int d) {
+  return push_cls == 2 ? P.pp_epoch[d] : P.epoch;
+}
+
+__device__ __forceinline__ void consumer_bar() { asm volatile("bar.sync 1, %0;" ::"n"(kFCompute * 32) : "memory"); }
+
 template <class Codec>
-__global__ void __launch_bounds__(kFusedThreads) ring_fused_kernel(const __grid_constant__ FusedParams P) {
-  __shared__ __align__(16) FusedSmem S;
+__device__ __forceinline__ void compute_group(const FusedParams& P, const Phase& f, uint64_t g, bool direct,
+                                              const uint8_t* sa, const uint8_t* sb, uint8_t* tile_g, uint8_t* gen,
+                                              int lane, uint32_t& bad) {
+  const uint64_t base = g * kGroupVals;
+  const uint32_t live = static_cast<uint32_t>(P.n_chunk - base < kGroupVals ? P.n_chunk - base : kGroupVals);
+  const bool vec = P.vec_ok != 0;
+  typename Codec::Lane s;
+  float v[8];
+  // ---- inputs
+  if (f.kind == kPhEnc) {
+    if (direct)
+      load_vals<false>(f.vals, base, live, vec, lane, v);
+    else
+      ld_vals<2>(reinterpret_cast<const float*>(sa) + 8 * lane, v);
+  } else {
+    bool loaded = false;
+    if constexpr (Codec::kFastPath) {
+      if (!direct) {
+        typename Codec::Raw raw;
+        Codec::template load_raw<2>(raw, reinterpret_cast<const uint32_t*>(sa), lane);
+        Codec::assemble(s, raw, lane);
+        loaded = true;
+      }
+    }
+    if (!loaded) group_load<Codec, false>(s, f.pay + g * Codec::kGroupBytes, live, true, gen, lane);
+    Codec::decode(s, v);
+    if (f.kind != kPhDec) {
+      float loc[8];
+      if (direct)
+        load_vals<false>(f.vals, base, live, vec, lane, loc);
+      else
+        ld_vals<2>(reinterpret_cast<const float*>(sb) + 8 * lane, loc);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[i] = __fadd_rn(v[i], loc[i]);
+    }
+  }
+  // ---- outputs
+  if (f.kind == kPhDec || f.kind == kPhFinRs) {
+    if (f.div) apply_div(v, P.div_mode, P.recip, P.divisor);
+    store_vals(f.out, base, live, vec, lane, v);
+    return;
+  }
+  Codec::encode(v, s, bad, lane_live(live, lane));
+  bool done = false;
+  if constexpr (Codec::kFastPath) {
+    if (live == kGroupVals && (reinterpret_cast<uintptr_t>(tile_g) & (Codec::kKind == 0 ? 31u : 3u)) == 0) {
+      Codec::store_fast_generic(s, reinterpret_cast<uint32_t*>(tile_g), lane);
+      done = true;
+    }
+  }
+  if (!done) Codec::to_stage(s, tile_g, lane);
+  if (f.out) {
+    Codec::decode(s, v);
+    if (f.div) apply_div(v, P.div_mode, P.recip, P.divisor);
+    store_vals(f.out, base, live, vec, lane, v);
+  }
+}
+
+template <class Codec>
+__global__ void __launch_bounds__(kFThreads2) ring_fused_kernel(const __grid_constant__ FusedParams P) {
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  FusedSmem2& S = *reinterpret_cast<FusedSmem2*>(smem_raw);
   const int lane = static_cast<int>(lane_id()), warp = static_cast<int>(threadIdx.x >> 5);
   const int p = P.p, j = P.rank;
   const uint64_t c = P.n_chunk;
@@ -201,157 +461,148 @@ __global__ void __launch_bounds__(kFusedThreads) ring_fused_kernel(const __grid_
   const uint32_t nseg = static_cast<uint32_t>((ngroups + kSegGroups - 1) / kSegGroups);
   const uint64_t GB = Codec::kGroupBytes;
   const uint64_t wire = Codec::wire_bytes(c);
-  uint8_t* tile = S.tile;
-  uint8_t* sm = S.stage[warp];
-  uint32_t bad = 0;
-  auto chunk_in = [&](int ch) { return P.in + static_cast<uint64_t>(((ch % p) + p) % p) * c; };
-  auto chunk_out = [&](int ch) { return P.out + static_cast<uint64_t>(((ch % p) + p) % p) * c; };
-  auto seg_bytes = [&](uint32_t sg) {
-    const uint64_t start = static_cast<uint64_t>(sg) * kSegGroups * GB;
-    const uint64_t rem = wire - start;
-    return static_cast<uint32_t>(rem < kSegGroups * GB ? rem : kSegGroups * GB);
-  };
-  const int right = (j + 1) % p, left = (j + p - 1) % p;
-
-  // This CTA's segments are sg = blockIdx.x + k*G, k < myseg.  They are
-  // processed in steps of kStepSegs segments; a step is published with ONE
-  // system-scope fence + flag (indexed by the step's first segment), which
-  // amortises the fence over up to kStepSegs x 8 groups.
   const uint32_t G = gridDim.x;
   const uint32_t myseg = nseg > blockIdx.x ? (nseg - blockIdx.x + G - 1) / G : 0;
+  const int nph = nphases(P);
+  // TMA needs whole 16B-multiple segments at 16B-aligned addresses: word
+  // codecs with 32B-aligned fp32 chunks (payload segments are 8*GB bytes,
+  // a multiple of 16, at 256B-aligned slot offsets).
+  const bool tma_ok = Codec::kFastPath && P.vec_ok;
   auto seg_of = [&](uint32_t k) { return blockIdx.x + k * G; };
+  auto seg_full = [&](uint32_t sg) { return (static_cast<uint64_t>(sg) + 1) * kSegVals <= c; };
 
-  if (P.op == kFAllReduce || P.op == kFReduceScatter) {
-    const bool ar = P.op == kFAllReduce;
-    for (int t = 0; t < p; ++t) {  // t = p-1 is the final receive
-      const bool last = t == p - 1;
-      const bool push = !(last && !ar);
-      // credit for the slot(s) this round pushes into (previous use consumed)
-      if (threadIdx.x == 0) {
-        if (!last) spin_ge(P, flag_ptr(P, j, 3, t, blockIdx.x), P.prev_rs);
-        if (last && ar)
-          for (int q = 1; q < p; ++q) spin_ge(P, flag_ptr(P, j, 4, (j + q) % p, blockIdx.x), P.prev_ag);
-      }
-      const uint8_t* rx = t > 0 ? slot_ptr(P, j, 0, t - 1) : nullptr;
-      const float* local = chunk_in(j - 1 - t);
-      for (uint32_t k0 = 0; k0 < myseg; k0 += kStepSegs) {
-        const uint32_t k1 = min(k0 + kStepSegs, myseg);
-        if (threadIdx.x == 0 && t > 0) spin_ge(P, flag_ptr(P, j, 0, t - 1, seg_of(k0)), P.epoch);
-        __syncthreads();
-        for (uint32_t k = k0; k < k1; ++k) {
-          const uint32_t sg = seg_of(k);
-          const uint64_t g = static_cast<uint64_t>(sg) * kSegGroups + warp;
-          if (g < ngroups) {
-            if (!push) {
-              fused_group<Codec, false, true>(P, rx, nullptr, local, P.out, true, nullptr, g, sm, lane, bad);
-            } else {
-              uint8_t* tg = tile + warp * GB;
-              float* ov = last ? chunk_out(j) : nullptr;
-              if (t == 0)
-                fused_group<Codec, true, false>(P, nullptr, local, nullptr, ov, false, tg, g, sm, lane, bad);
-              else
-                fused_group<Codec, true, true>(P, rx, nullptr, local, ov, false, tg, g, sm, lane, bad);
-            }
-          }
-          if (!push) continue;  // reduce-scatter final: fp32 shard, nothing to push
-          __syncthreads();
-          const uint64_t soff = static_cast<uint64_t>(sg) * kSegGroups * GB;
-          const uint32_t nb = seg_bytes(sg);
-          if (!last)
-            push_tile(tile, slot_ptr(P, right, 0, t) + soff, nb);
-          else
-            for (int q = 1; q < p; ++q) push_tile(tile, slot_ptr(P, (j + q) % p, 1, j) + soff, nb);
-          __syncthreads();
-        }
-        if (push) {
-          if (!last) {
-            if (threadIdx.x == 0) signal(flag_ptr(P, right, 0, t, seg_of(k0)), P.epoch);
-          } else if (threadIdx.x < p - 1) {
-            signal(flag_ptr(P, (j + 1 + threadIdx.x) % p, 1, j, seg_of(k0)), P.epoch);
-          }
-        }
-      }
-      if (t > 0) {
-        __syncthreads();
-        ack_all(flag_ptr(P, left, 3, t - 1, 0), P.epoch);
-      }
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < kFStages; ++st) {
+      mbar_init(&S.full[st], 1);
+      mbar_init(&S.empty[st], kFCompute);
     }
-    if (ar) {
-      for (int q = 1; q < p; ++q) {
-        const int i = (j - q + p) % p;
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (warp == kFCompute) {
+    // ------------------------------------------------------------ producer
+    if (lane == 0) {
+      int st = 0;
+      uint32_t phase_bit = 0;
+      for (int ph = 0; ph < nph; ++ph) {
+        const Phase f = phase_of(P, ph);
         for (uint32_t k0 = 0; k0 < myseg; k0 += kStepSegs) {
           const uint32_t k1 = min(k0 + kStepSegs, myseg);
-          seg_wait(P, flag_ptr(P, j, 1, i, seg_of(k0)), P.epoch);
+          if (f.wait_cls >= 0) {
+            spin_ge(P, flag_ptr(P, j, f.wait_cls, f.wait_slot, seg_of(k0)), f.wait_ep);
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+          }
           for (uint32_t k = k0; k < k1; ++k) {
-            const uint64_t g = static_cast<uint64_t>(seg_of(k)) * kSegGroups + warp;
-            if (g < ngroups)
-              fused_group<Codec, false, false>(P, slot_ptr(P, j, 1, i), nullptr, nullptr, chunk_out(i), false,
-                                               nullptr, g, sm, lane, bad);
+            const uint32_t sg = seg_of(k);
+            mbar_wait(&S.empty[st], phase_bit ^ 1u);
+            const bool full_seg = tma_ok && seg_full(sg);
+            S.direct[st] = full_seg ? 0u : 1u;
+            if (full_seg) {
+              const uint32_t a_bytes = f.kind == kPhEnc ? kSegVals * 4u : static_cast<uint32_t>(kSegGroups * GB);
+              const uint32_t b_bytes = (f.kind == kPhDar || f.kind == kPhFinAr || f.kind == kPhFinRs) ? kSegVals * 4u : 0u;
+              mbar_arrive_expect_tx(&S.full[st], a_bytes + b_bytes);
+              if (f.kind == kPhEnc)
+                bulk_g2s(S.stage[st], f.vals + static_cast<uint64_t>(sg) * kSegVals, a_bytes, &S.full[st]);
+              else
+                bulk_g2s(S.stage[st], f.pay + static_cast<uint64_t>(sg) * kSegGroups * GB, a_bytes, &S.full[st]);
+              if (b_bytes)
+                bulk_g2s(S.stage[st] + kFStageA, f.vals + static_cast<uint64_t>(sg) * kSegVals, b_bytes, &S.full[st]);
+            } else {
+              mbar_arrive(&S.full[st]);  // consumers read this segment from global memory
+            }
+            if (++st == kFStages) {
+              st = 0;
+              phase_bit ^= 1u;
+            }
           }
         }
-        __syncthreads();
-        ack_all(flag_ptr(P, i, 4, j, 0), P.epoch);
       }
     }
-  } else {
-    // allgather: every rank is an origin (its shard, ag slots); broadcast /
-    // p2p: the root is the origin (pp slots, pairwise epochs).
-    const bool ag = P.op == kFAllGather;
-    const int cls = ag ? 1 : 2;
-    const bool origin = ag || j == P.root;
-    float* own_out = ag ? P.out + static_cast<uint64_t>(j) * c : (P.op == kFBroadcast ? P.out : nullptr);
-    if (origin) {
-      if (threadIdx.x == 0) {
-        for (int q = 1; q < p; ++q) {
-          const int d = (j + q) % p;
-          if (P.op == kFP2P && d != P.dst) continue;
-          spin_ge(P, flag_ptr(P, j, ag ? 4 : 5, d, blockIdx.x), ag ? P.prev_ag : P.pp_epoch[d] - 1u);
-        }
+    return;
+  }
+
+  // -------------------------------------------------------------- compute
+  uint32_t bad = 0;
+  int st = 0;
+  uint32_t phase_bit = 0;
+  int tb = 0;  // tile buffer in use (double-buffered for the bulk pushes)
+  uint8_t* gen = S.gen[warp];
+  const bool bulk = (P.debug & 8) != 0;
+  for (int ph = 0; ph < nph; ++ph) {
+    const Phase f = phase_of(P, ph);
+    const bool push = f.push_cls >= 0;
+    if (push && threadIdx.x == 0) {  // credit: previous use of the destination slot(s) consumed
+      for (int q = 1; q < p; ++q) {
+        const int d = (j + q) % p;
+        if (f.push_mode == 0 && d != (j + 1) % p) continue;
+        if (f.push_mode == 2 && d != P.dst) continue;
+        const uint32_t need = f.push_cls == 2 ? P.pp_epoch[d] - 1u : f.credit_ep;
+        spin_ge(P, flag_ptr(P, j, f.credit_cls, f.push_mode == 0 ? f.push_slot : d, blockIdx.x), need);
       }
-      __syncthreads();
-      for (uint32_t k0 = 0; k0 < myseg; k0 += kStepSegs) {
-        const uint32_t k1 = min(k0 + kStepSegs, myseg);
-        for (uint32_t k = k0; k < k1; ++k) {
-          const uint32_t sg = seg_of(k);
-          const uint64_t g = static_cast<uint64_t>(sg) * kSegGroups + warp;
-          if (g < ngroups)
-            fused_group<Codec, true, false>(P, nullptr, P.in, nullptr, own_out, false, tile + warp * GB, g, sm,
-                                            lane, bad);
-          __syncthreads();
+    }
+    consumer_bar();
+    for (uint32_t k0 = 0; k0 < myseg; k0 += kStepSegs) {
+      const uint32_t k1 = min(k0 + kStepSegs, myseg);
+      for (uint32_t k = k0; k < k1; ++k) {
+        const uint32_t sg = seg_of(k);
+        mbar_wait(&S.full[st], phase_bit);
+        const bool direct = S.direct[st] != 0;
+        const uint64_t g = static_cast<uint64_t>(sg) * kSegGroups + warp;
+        const uint8_t* sa = S.stage[st] + (f.kind == kPhEnc ? warp * 1024u : warp * static_cast<uint32_t>(GB));
+        const uint8_t* sb = S.stage[st] + kFStageA + warp * 1024u;
+        uint8_t* tile = S.tile[tb];
+        if (g < ngroups) compute_group<Codec>(P, f, g, direct, sa, sb, tile + warp * GB, gen, lane, bad);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&S.empty[st]);
+        if (++st == kFStages) {
+          st = 0;
+          phase_bit ^= 1u;
+        }
+        if (push && !(P.debug & 1)) {
+          consumer_bar();
           const uint64_t soff = static_cast<uint64_t>(sg) * kSegGroups * GB;
-          const uint32_t nb = seg_bytes(sg);
-          if (P.op == kFP2P)
-            push_tile(tile, slot_ptr(P, P.dst, cls, j) + soff, nb);
-          else
-            for (int q = 1; q < p; ++q) push_tile(tile, slot_ptr(P, (j + q) % p, cls, j) + soff, nb);
-          __syncthreads();
+          const uint64_t rem = wire - soff;
+          const uint32_t nb = static_cast<uint32_t>(rem < kSegGroups * GB ? rem : kSegGroups * GB);
+          if (bulk && (nb & 15u) == 0) {
+            // one thread hands the whole segment to the TMA engine per destination
+            if (threadIdx.x == 0) {
+              for (int q = 1; q < p; ++q) {
+                const int d = (j + q) % p;
+                if (f.push_mode == 0 && q != 1) break;
+                if (f.push_mode == 2 && d != P.dst) continue;
+                bulk_s2g(slot_ptr(P, d, f.push_cls, f.push_slot) + soff, tile, nb);
+              }
+              bulk_commit();
+              bulk_wait_read<1>();  // the other tile buffer is free again
+            }
+            tb ^= 1;
+          } else {
+            if (bulk && threadIdx.x == 0) bulk_wait_read<0>();
+            for (int q = 1; q < p; ++q) {
+              const int d = (j + q) % p;
+              if (f.push_mode == 0 && q != 1) break;
+              if (f.push_mode == 2 && d != P.dst) continue;
+              push_tile_n(tile, slot_ptr(P, d, f.push_cls, f.push_slot) + soff, nb, kFCompute * 32);
+            }
+          }
+          consumer_bar();
         }
-        if (P.op == kFP2P) {
-          if (threadIdx.x == 0) signal(flag_ptr(P, P.dst, cls, j, seg_of(k0)), P.pp_epoch[P.dst]);
-        } else if (threadIdx.x < p - 1) {
+      }
+      if (push) {  // publish the step: one release store per destination
+        if (bulk && threadIdx.x == 0) bulk_wait_all();
+        if (bulk) consumer_bar();
+        if (threadIdx.x < static_cast<unsigned>(p - 1)) {
           const int d = (j + 1 + threadIdx.x) % p;
-          signal(flag_ptr(P, d, cls, j, seg_of(k0)), ag ? P.epoch : P.pp_epoch[d]);
+          const bool tgt = f.push_mode == 1 || (f.push_mode == 0 && threadIdx.x == 0) || (f.push_mode == 2 && d == P.dst);
+          if (tgt) signal(flag_ptr(P, d, f.push_cls, f.push_slot, seg_of(k0)), push_epoch(P, f.push_cls, d));
         }
       }
     }
-    for (int q = 1; q < p; ++q) {
-      const int i = (j - q + p) % p;
-      if (!ag && i != P.root) continue;
-      if (P.op == kFP2P && j != P.dst) continue;
-      const uint32_t ep = ag ? P.epoch : P.pp_epoch[i];
-      float* dst = ag ? P.out + static_cast<uint64_t>(i) * c : P.out;
-      for (uint32_t k0 = 0; k0 < myseg; k0 += kStepSegs) {
-        const uint32_t k1 = min(k0 + kStepSegs, myseg);
-        seg_wait(P, flag_ptr(P, j, cls, i, seg_of(k0)), ep);
-        for (uint32_t k = k0; k < k1; ++k) {
-          const uint64_t g = static_cast<uint64_t>(seg_of(k)) * kSegGroups + warp;
-          if (g < ngroups)
-            fused_group<Codec, false, false>(P, slot_ptr(P, j, cls, i), nullptr, nullptr, dst, true, nullptr, g,
-                                             sm, lane, bad);
-        }
-      }
-      __syncthreads();
-      ack_all(flag_ptr(P, i, ag ? 4 : 5, j, 0), ep);
+    if (f.ack_rank >= 0) {
+      consumer_bar();
+      for (uint32_t kk = blockIdx.x + threadIdx.x * G; kk < kAckIdx; kk += G * kFCompute * 32)
+        st_release_sys(flag_ptr(P, f.ack_rank, f.ack_cls, f.ack_slot, 0) + kk, f.ack_ep);
     }
   }
   if constexpr (Codec::kCheckFinite) {
