@@ -187,6 +187,12 @@ HCCX_API hccx_status_t hccx_p2p(hccx_comm_t c, int src, int dst, const float* d_
 /* Synchronise and report this rank's error flag (non-finite, peer timeout). */
 HCCX_API hccx_status_t hccx_comm_status(hccx_comm_t c, void* stream);
 
+/* Timeline of CTA 0 of the fused kernel (development / performance
+ * analysis: ncu cannot replay a multi-rank kernel).  capacity in 64-bit
+ * words (0 disables).  Read returns [count, (tag, t_ns) x count]. */
+HCCX_API hccx_status_t hccx_comm_trace_enable(hccx_comm_t c, uint64_t capacity);
+HCCX_API hccx_status_t hccx_comm_trace_read(hccx_comm_t c, uint64_t* host, uint64_t max_words, uint64_t* words);
+
 /* Kernel launches issued by this library since it was loaded. */
 HCCX_API uint64_t hccx_launch_count(void);
 

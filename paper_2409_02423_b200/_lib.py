@@ -69,6 +69,8 @@ hccx_allgather = _sig("hccx_allgather", _st, _p, _p, _p, _u64, Codec, _p)
 hccx_broadcast = _sig("hccx_broadcast", _st, _p, C.c_int, _p, _p, _u64, Codec, _p)
 hccx_p2p = _sig("hccx_p2p", _st, _p, C.c_int, C.c_int, _p, _p, _u64, Codec, _p)
 hccx_comm_status = _sig("hccx_comm_status", _st, _p, _p)
+hccx_comm_trace_enable = _sig("hccx_comm_trace_enable", _st, _p, _u64)
+hccx_comm_trace_read = _sig("hccx_comm_trace_read", _st, _p, C.POINTER(_u64), _u64, C.POINTER(_u64))
 hccx_launch_count = _sig("hccx_launch_count", _u64)
 
 #: every symbol include/hccx.h declares (checked by tests/test_abi.py)

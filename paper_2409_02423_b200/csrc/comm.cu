@@ -91,6 +91,8 @@ struct hccx_comm {
   uint32_t last_rs = 0, last_ag = 0;   // epoch of the last collective that used rs / ag slots
   uint32_t send_ep[kMaxRanks] = {};    // p2p / broadcast messages sent to rank d
   uint32_t recv_ep[kMaxRanks] = {};    // ... received from rank s
+  uint64_t* d_trace = nullptr;         // optional CTA-0 timeline (hccx_comm_trace_enable)
+  uint64_t trace_cap = 0;
 };
 
 extern "C" hccx_status_t hccx_comm_create(int rank, int nranks, int device, uint64_t max_n, hccx_comm_t* out) {
@@ -201,6 +203,8 @@ FusedParams base_params(hccx_comm* c, int op, uint64_t n_chunk, const float* in,
     return e ? std::atoi(e) : 0;
   }();
   P.debug = dbg;
+  P.trace = c->d_trace;
+  P.trace_cap = c->trace_cap;
   // chunk offsets are multiples of n_chunk floats: aligned iff n_chunk % 8 == 0
   P.vec_ok = (aligned32(in) && aligned32(out) && (n_chunk % 8 == 0)) ? 1 : 0;
   return P;
@@ -335,4 +339,28 @@ extern "C" hccx_status_t hccx_comm_status(hccx_comm_t c, void* stream) {
   if (!c) return HCCX_ERR_INVALID_ARGUMENT;
   DeviceGuard guard(c->device);
   return read_flag(c->d_err, static_cast<cudaStream_t>(stream));
+}
+
+extern "C" hccx_status_t hccx_comm_trace_enable(hccx_comm_t c, uint64_t capacity) {
+  if (!c) return HCCX_ERR_INVALID_ARGUMENT;
+  DeviceGuard guard(c->device);
+  cudaFree(c->d_trace);
+  c->d_trace = nullptr;
+  c->trace_cap = 0;
+  if (capacity == 0) return HCCX_OK;
+  if (cudaMalloc(&c->d_trace, capacity * 8) != cudaSuccess) return HCCX_ERR_CUDA;
+  c->trace_cap = capacity;
+  return cuda_status(cudaMemset(c->d_trace, 0, capacity * 8));
+}
+
+extern "C" hccx_status_t hccx_comm_trace_read(hccx_comm_t c, uint64_t* host, uint64_t max_words, uint64_t* words) {
+  if (!c || !host || !words) return HCCX_ERR_INVALID_ARGUMENT;
+  DeviceGuard guard(c->device);
+  *words = 0;
+  if (!c->d_trace) return HCCX_OK;
+  if (cudaDeviceSynchronize() != cudaSuccess) return HCCX_ERR_CUDA;
+  const uint64_t n = max_words < c->trace_cap ? max_words : c->trace_cap;
+  if (cudaMemcpy(host, c->d_trace, n * 8, cudaMemcpyDeviceToHost) != cudaSuccess) return HCCX_ERR_CUDA;
+  *words = n;
+  return cuda_status(cudaMemset(c->d_trace, 0, c->trace_cap * 8));
 }

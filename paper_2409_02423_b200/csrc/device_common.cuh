@@ -156,6 +156,11 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
+// Bulk prefetch of [src, src+bytes) into L2 (no completion tracking).
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+
 // Shared -> global bulk copy (TMA engine) into local or peer-mapped memory,
 // tracked by the issuing thread's bulk-group; 16B-aligned, size % 16 == 0.
 __device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {

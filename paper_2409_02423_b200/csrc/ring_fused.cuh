@@ -56,6 +56,8 @@ struct FusedParams {
   float recip, divisor;
   uint32_t* err;
   uint64_t timeout_ns;
+  uint64_t* trace;  // optional event log (hccx_comm_trace_enable): [0] = count, then (tag, t_ns) pairs
+  uint64_t trace_cap;
   int debug;  // development knobs (HCCX_DEBUG): 1 skip pushes, 2 skip system fence, 4 skip segment barriers
 };
 
@@ -222,18 +224,22 @@ __device__ __forceinline__ void fused_group(const FusedParams& P, const uint8_t*
 // ---------------------------------------------------------------------------
 
 constexpr int kFStages = 3;
+constexpr int kFTiles = 3;
+constexpr uint32_t kFPrefetch = 4;  // L2 prefetch distance (segments)
 constexpr int kFCompute = kFusedWarps;              // compute warps
-constexpr int kFThreads2 = (kFCompute + 1) * 32;    // + producer warp
+constexpr int kFThreads2 = (kFCompute + 2) * 32;    // + producer warp + pusher warp
 constexpr uint32_t kFStageA = 8448;                 // >= 8 x 1028 B payload groups / 8 KiB fp32, 128B multiple
 constexpr uint32_t kFStageB = 8192;                 // 8 groups x 1 KiB fp32
 constexpr uint32_t kFStageBytes = kFStageA + kFStageB;
+static_assert(kFStageA >= kFCompute * kStageBytes, "direct-mode staging aliases stage A");
 
 struct FusedSmem2 {
   uint8_t stage[kFStages][kFStageBytes];
-  uint8_t tile[2][kFStageA];
-  uint8_t gen[kFCompute][kStageBytes];
+  uint8_t tile[kFTiles][kFStageA];
   uint64_t full[kFStages];
   uint64_t empty[kFStages];
+  uint64_t tfull[kFTiles];
+  uint64_t tempty[kFTiles];
   uint32_t direct[kFStages];
 };
 
@@ -385,6 +391,17 @@ __device__ __forceinline__ Phase phase_of(const FusedParams& P, int ph) {
   return f;
 }
 
+// Event log for CTA 0 (timeline of one CTA; ncu cannot replay a multi-rank
+// kernel).  tag = (event << 32) | (phase << 16) | segment.
+__device__ __forceinline__ void trace_ev(const FusedParams& P, uint32_t ev, uint32_t ph, uint32_t seg) {
+  if (P.trace == nullptr || blockIdx.x != 0) return;
+  const unsigned long long i = atomicAdd(reinterpret_cast<unsigned long long*>(P.trace), 1ull);
+  if (2 * i + 2 < P.trace_cap) {
+    P.trace[1 + 2 * i] = (static_cast<uint64_t>(ev) << 32) | (static_cast<uint64_t>(ph) << 16) | seg;
+    P.trace[2 + 2 * i] = globaltimer_ns();
+  }
+}
+
 __device__ __forceinline__ uint32_t push_epoch(const FusedParams& P, int push_cls, int d) {
   return push_cls == 2 ? P.pp_epoch[d] : P.epoch;
 }
@@ -451,7 +468,7 @@ __device__ __forceinline__ void compute_group(const FusedParams& P, const Phase&
 }
 
 template <class Codec>
-__global__ void __launch_bounds__(kFThreads2) ring_fused_kernel(const __grid_constant__ FusedParams P) {
+__global__ void __launch_bounds__(kFThreads2, 3) ring_fused_kernel(const __grid_constant__ FusedParams P) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   FusedSmem2& S = *reinterpret_cast<FusedSmem2*>(smem_raw);
   const int lane = static_cast<int>(lane_id()), warp = static_cast<int>(threadIdx.x >> 5);
@@ -476,6 +493,10 @@ __global__ void __launch_bounds__(kFThreads2) ring_fused_kernel(const __grid_con
       mbar_init(&S.full[st], 1);
       mbar_init(&S.empty[st], kFCompute);
     }
+    for (int tt = 0; tt < kFTiles; ++tt) {
+      mbar_init(&S.tfull[tt], kFCompute);
+      mbar_init(&S.tempty[tt], 1);
+    }
     fence_mbar_init();
   }
   __syncthreads();
@@ -490,24 +511,42 @@ __global__ void __launch_bounds__(kFThreads2) ring_fused_kernel(const __grid_con
         for (uint32_t k0 = 0; k0 < myseg; k0 += kStepSegs) {
           const uint32_t k1 = min(k0 + kStepSegs, myseg);
           if (f.wait_cls >= 0) {
+            trace_ev(P, 10, ph, k0);
             spin_ge(P, flag_ptr(P, j, f.wait_cls, f.wait_slot, seg_of(k0)), f.wait_ep);
             asm volatile("fence.proxy.async.global;" ::: "memory");
+            trace_ev(P, 11, ph, k0);
           }
           for (uint32_t k = k0; k < k1; ++k) {
             const uint32_t sg = seg_of(k);
+            // L2 prefetch kFPrefetch segments ahead (same phase), so the
+            // bulk load issued when the stage frees up hits L2
+            if (tma_ok && k + kFPrefetch < k1) {
+              const uint32_t sp = seg_of(k + kFPrefetch);
+              if (seg_full(sp)) {
+                if (f.kind == kPhEnc) {
+                  bulk_prefetch_l2(f.vals + static_cast<uint64_t>(sp) * kSegVals, kSegVals * 4u);
+                } else {
+                  bulk_prefetch_l2(f.pay + static_cast<uint64_t>(sp) * kSegGroups * GB,
+                                   static_cast<uint32_t>(kSegGroups * GB));
+                  if (f.kind != kPhDec) bulk_prefetch_l2(f.vals + static_cast<uint64_t>(sp) * kSegVals, kSegVals * 4u);
+                }
+              }
+            }
             mbar_wait(&S.empty[st], phase_bit ^ 1u);
             const bool full_seg = tma_ok && seg_full(sg);
             S.direct[st] = full_seg ? 0u : 1u;
             if (full_seg) {
               const uint32_t a_bytes = f.kind == kPhEnc ? kSegVals * 4u : static_cast<uint32_t>(kSegGroups * GB);
-              const uint32_t b_bytes = (f.kind == kPhDar || f.kind == kPhFinAr || f.kind == kPhFinRs) ? kSegVals * 4u : 0u;
+              const uint32_t b_bytes =
+                  (f.kind == kPhDar || f.kind == kPhFinAr || f.kind == kPhFinRs) ? kSegVals * 4u : 0u;
               mbar_arrive_expect_tx(&S.full[st], a_bytes + b_bytes);
               if (f.kind == kPhEnc)
                 bulk_g2s(S.stage[st], f.vals + static_cast<uint64_t>(sg) * kSegVals, a_bytes, &S.full[st]);
               else
                 bulk_g2s(S.stage[st], f.pay + static_cast<uint64_t>(sg) * kSegGroups * GB, a_bytes, &S.full[st]);
               if (b_bytes)
-                bulk_g2s(S.stage[st] + kFStageA, f.vals + static_cast<uint64_t>(sg) * kSegVals, b_bytes, &S.full[st]);
+                bulk_g2s(S.stage[st] + kFStageA, f.vals + static_cast<uint64_t>(sg) * kSegVals, b_bytes,
+                         &S.full[st]);
             } else {
               mbar_arrive(&S.full[st]);  // consumers read this segment from global memory
             }
@@ -522,87 +561,130 @@ __global__ void __launch_bounds__(kFThreads2) ring_fused_kernel(const __grid_con
     return;
   }
 
-  // -------------------------------------------------------------- compute
-  uint32_t bad = 0;
-  int st = 0;
-  uint32_t phase_bit = 0;
-  int tb = 0;  // tile buffer in use (double-buffered for the bulk pushes)
-  uint8_t* gen = S.gen[warp];
-  const bool bulk = (P.debug & 8) != 0;
-  for (int ph = 0; ph < nph; ++ph) {
-    const Phase f = phase_of(P, ph);
-    const bool push = f.push_cls >= 0;
-    if (push && threadIdx.x == 0) {  // credit: previous use of the destination slot(s) consumed
-      for (int q = 1; q < p; ++q) {
-        const int d = (j + q) % p;
-        if (f.push_mode == 0 && d != (j + 1) % p) continue;
-        if (f.push_mode == 2 && d != P.dst) continue;
-        const uint32_t need = f.push_cls == 2 ? P.pp_epoch[d] - 1u : f.credit_ep;
-        spin_ge(P, flag_ptr(P, j, f.credit_cls, f.push_mode == 0 ? f.push_slot : d, blockIdx.x), need);
-      }
-    }
-    consumer_bar();
-    for (uint32_t k0 = 0; k0 < myseg; k0 += kStepSegs) {
-      const uint32_t k1 = min(k0 + kStepSegs, myseg);
-      for (uint32_t k = k0; k < k1; ++k) {
-        const uint32_t sg = seg_of(k);
-        mbar_wait(&S.full[st], phase_bit);
-        const bool direct = S.direct[st] != 0;
-        const uint64_t g = static_cast<uint64_t>(sg) * kSegGroups + warp;
-        const uint8_t* sa = S.stage[st] + (f.kind == kPhEnc ? warp * 1024u : warp * static_cast<uint32_t>(GB));
-        const uint8_t* sb = S.stage[st] + kFStageA + warp * 1024u;
-        uint8_t* tile = S.tile[tb];
-        if (g < ngroups) compute_group<Codec>(P, f, g, direct, sa, sb, tile + warp * GB, gen, lane, bad);
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&S.empty[st]);
-        if (++st == kFStages) {
-          st = 0;
-          phase_bit ^= 1u;
+  if (warp == kFCompute + 1) {
+    // -------------------------------------------------------------- pusher
+    // Takes each computed segment from the tile ring, hands it to the TMA
+    // engine (one bulk store per destination window), recycles the tile
+    // once the engine has read it, and publishes every step with one
+    // release store per destination after its bulk writes completed.
+    int tt = 0;
+    uint32_t tbit = 0;
+    int pending = -1;  // tile whose bulk read may still be in flight
+    for (int ph = 0; ph < nph; ++ph) {
+      const Phase f = phase_of(P, ph);
+      const bool push = f.push_cls >= 0;
+      if (push && lane == 0) {  // credit: previous use of the destination slot(s) consumed
+        for (int q = 1; q < p; ++q) {
+          const int d = (j + q) % p;
+          if (f.push_mode == 0 && d != (j + 1) % p) continue;
+          if (f.push_mode == 2 && d != P.dst) continue;
+          const uint32_t need = f.push_cls == 2 ? P.pp_epoch[d] - 1u : f.credit_ep;
+          spin_ge(P, flag_ptr(P, j, f.credit_cls, f.push_mode == 0 ? f.push_slot : d, blockIdx.x), need);
         }
-        if (push && !(P.debug & 1)) {
-          consumer_bar();
-          const uint64_t soff = static_cast<uint64_t>(sg) * kSegGroups * GB;
-          const uint64_t rem = wire - soff;
-          const uint32_t nb = static_cast<uint32_t>(rem < kSegGroups * GB ? rem : kSegGroups * GB);
-          if (bulk && (nb & 15u) == 0) {
-            // one thread hands the whole segment to the TMA engine per destination
-            if (threadIdx.x == 0) {
+      }
+      __syncwarp();
+      for (uint32_t k0 = 0; k0 < myseg; k0 += kStepSegs) {
+        const uint32_t k1 = min(k0 + kStepSegs, myseg);
+        for (uint32_t k = k0; k < k1; ++k) {
+          const uint32_t sg = seg_of(k);
+          mbar_wait(&S.tfull[tt], tbit);
+          if (push) {
+            const uint64_t soff = static_cast<uint64_t>(sg) * kSegGroups * GB;
+            const uint64_t rem = wire - soff;
+            const uint32_t nb = static_cast<uint32_t>(rem < kSegGroups * GB ? rem : kSegGroups * GB);
+            if ((nb & 15u) == 0 && !(P.debug & 16)) {
+              if (lane == 0) {
+                for (int q = 1; q < p; ++q) {
+                  const int d = (j + q) % p;
+                  if (f.push_mode == 0 && q != 1) break;
+                  if (f.push_mode == 2 && d != P.dst) continue;
+                  bulk_s2g(slot_ptr(P, d, f.push_cls, f.push_slot) + soff, S.tile[tt], nb);
+                }
+                bulk_commit();
+              }
+            } else {
               for (int q = 1; q < p; ++q) {
                 const int d = (j + q) % p;
                 if (f.push_mode == 0 && q != 1) break;
                 if (f.push_mode == 2 && d != P.dst) continue;
-                bulk_s2g(slot_ptr(P, d, f.push_cls, f.push_slot) + soff, tile, nb);
+                uint8_t* dst = slot_ptr(P, d, f.push_cls, f.push_slot) + soff;
+                const uint32_t n16 = (nb & 15u) == 0 && (reinterpret_cast<uintptr_t>(dst) & 15u) == 0 ? nb >> 4 : 0;
+                for (uint32_t i = lane; i < n16; i += 32)
+                  reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(S.tile[tt])[i];
+                for (uint32_t b = (n16 << 4) + lane; b < nb; b += 32) dst[b] = S.tile[tt][b];
               }
-              bulk_commit();
-              bulk_wait_read<1>();  // the other tile buffer is free again
+              __syncwarp();
             }
-            tb ^= 1;
-          } else {
-            if (bulk && threadIdx.x == 0) bulk_wait_read<0>();
-            for (int q = 1; q < p; ++q) {
-              const int d = (j + q) % p;
-              if (f.push_mode == 0 && q != 1) break;
-              if (f.push_mode == 2 && d != P.dst) continue;
-              push_tile_n(tile, slot_ptr(P, d, f.push_cls, f.push_slot) + soff, nb, kFCompute * 32);
-            }
+            if (threadIdx.x == (kFCompute + 1) * 32 && lane == 0) trace_ev(P, 3, ph, k);
           }
-          consumer_bar();
+          // recycle the previous tile once its bulk read is done
+          if (lane == 0) {
+            if (push) bulk_wait_read<1>();
+            if (pending >= 0) mbar_arrive(&S.tempty[pending]);
+          }
+          pending = tt;
+          if (++tt == kFTiles) {
+            tt = 0;
+            tbit ^= 1u;
+          }
+        }
+        if (push) {  // publish the step after its bulk writes completed
+          if (lane == 0) bulk_wait_all();
+          __syncwarp();
+          if (lane < p - 1) {
+            const int d = (j + 1 + lane) % p;
+            const bool tgt =
+                f.push_mode == 1 || (f.push_mode == 0 && lane == 0) || (f.push_mode == 2 && d == P.dst);
+            if (tgt) signal(flag_ptr(P, d, f.push_cls, f.push_slot, seg_of(k0)), push_epoch(P, f.push_cls, d));
+          }
+          if (lane == 0) trace_ev(P, 5, ph, k0);
         }
       }
-      if (push) {  // publish the step: one release store per destination
-        if (bulk && threadIdx.x == 0) bulk_wait_all();
-        if (bulk) consumer_bar();
-        if (threadIdx.x < static_cast<unsigned>(p - 1)) {
-          const int d = (j + 1 + threadIdx.x) % p;
-          const bool tgt = f.push_mode == 1 || (f.push_mode == 0 && threadIdx.x == 0) || (f.push_mode == 2 && d == P.dst);
-          if (tgt) signal(flag_ptr(P, d, f.push_cls, f.push_slot, seg_of(k0)), push_epoch(P, f.push_cls, d));
-        }
+      // every segment of the phase has been computed (tfull) -> its inbox
+      // inputs are consumed: acknowledge for this CTA's index space
+      if (f.ack_rank >= 0) {
+        for (uint32_t kk = blockIdx.x + lane * G; kk < kAckIdx; kk += G * 32)
+          st_release_sys(flag_ptr(P, f.ack_rank, f.ack_cls, f.ack_slot, 0) + kk, f.ack_ep);
       }
     }
-    if (f.ack_rank >= 0) {
-      consumer_bar();
-      for (uint32_t kk = blockIdx.x + threadIdx.x * G; kk < kAckIdx; kk += G * kFCompute * 32)
-        st_release_sys(flag_ptr(P, f.ack_rank, f.ack_cls, f.ack_slot, 0) + kk, f.ack_ep);
+    if (lane == 0) {
+      bulk_wait_all();
+      if (pending >= 0) mbar_arrive(&S.tempty[pending]);
+    }
+    return;
+  }
+
+  // -------------------------------------------------------------- compute
+  uint32_t bad = 0;
+  int st = 0, tt = 0;
+  uint32_t phase_bit = 0, tbit = 0;
+  for (int ph = 0; ph < nph; ++ph) {
+    const Phase f = phase_of(P, ph);
+    for (uint32_t k = 0; k < myseg; ++k) {
+      const uint32_t sg = seg_of(k);
+      mbar_wait(&S.full[st], phase_bit);
+      if (threadIdx.x == 0) trace_ev(P, 1, ph, k);
+      mbar_wait(&S.tempty[tt], tbit ^ 1u);
+      const bool direct = S.direct[st] != 0;
+      const uint64_t g = static_cast<uint64_t>(sg) * kSegGroups + warp;
+      const uint8_t* sa = S.stage[st] + (f.kind == kPhEnc ? warp * 1024u : warp * static_cast<uint32_t>(GB));
+      const uint8_t* sb = S.stage[st] + kFStageA + warp * 1024u;
+      uint8_t* gen = S.stage[st] + warp * kStageBytes;  // free in direct mode
+      if (g < ngroups) compute_group<Codec>(P, f, g, direct, sa, sb, S.tile[tt] + warp * GB, gen, lane, bad);
+      __syncwarp();
+      if (threadIdx.x == 0) trace_ev(P, 2, ph, k);
+      if (lane == 0) {
+        mbar_arrive(&S.empty[st]);
+        mbar_arrive(&S.tfull[tt]);
+      }
+      if (++st == kFStages) {
+        st = 0;
+        phase_bit ^= 1u;
+      }
+      if (++tt == kFTiles) {
+        tt = 0;
+        tbit ^= 1u;
+      }
     }
   }
   if constexpr (Codec::kCheckFinite) {
