@@ -1,0 +1,240 @@
+// hcc_b200.hpp -- the reference's C++ host API (namespace hcc), implemented
+// over the C ABI of libhccx.so (include/hccx.h) by libhcc_b200.so.
+//
+// Drop-in for the hot path of arxiv/paper_2409_02423 ("hybridcomm",
+// /root/reference/proj): a program written against
+//   hcc/errors.hpp  hcc/codec.hpp  hcc/comm_path.hpp  hcc/netsim.hpp
+//   hcc/collectives.hpp  hcc/parallel3d.hpp
+// compiles against the forwarding headers of the same names in this
+// directory and links libhcc_b200.so instead of the reference library.
+// Signatures, value semantics, byte accounting and exception types are the
+// reference's; the arithmetic runs in sm_100a kernels and the results are
+// bit-identical (fixed-rate / identity).  Differences, all additive:
+//   * CodecKind::ZfpRate ("zfp-rate:N") -- ZFP-style transform codec;
+//   * broadcast() collective and CollectiveKind::Broadcast;
+//   * TraceEvent::duration_s is the measured device time (no alpha-beta
+//     model); Topology keeps the shape (world size, rank -> node) only.
+// Not on the device path yet: the LosslessPredictor codec
+// (compress/decompress throw hcc::Error; collectives with it throw too).
+#ifndef HCC_B200_HPP
+#define HCC_B200_HPP
+
+#include <array>
+#include <cstdint>
+#include <map>
+#include <ostream>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace hcc {
+
+// ----------------------------------------------------------------- errors --
+// Exception hierarchy of proj/include/hcc/errors.hpp:10-60.
+
+class Error : public std::runtime_error {
+ public:
+  explicit Error(const std::string& msg) : std::runtime_error(msg) {}
+};
+class NonFiniteInputError : public Error {
+ public:
+  using Error::Error;
+};
+class CorruptPayloadError : public Error {
+ public:
+  using Error::Error;
+};
+class DataDependentSizeError : public Error {
+ public:
+  using Error::Error;
+};
+class BadChunkingError : public Error {
+ public:
+  using Error::Error;
+};
+class BadLayoutError : public Error {
+ public:
+  using Error::Error;
+};
+class InvalidSchemeError : public Error {
+ public:
+  using Error::Error;
+};
+class ConfigError : public Error {
+ public:
+  ConfigError(const std::string& field, const std::string& msg)
+      : Error("config field '" + field + "': " + msg), field_(field) {}
+  const std::string& field() const { return field_; }
+
+ private:
+  std::string field_;
+};
+
+// ------------------------------------------------------------------ codec --
+
+using FloatBuffer = std::vector<float>;
+
+enum class CodecKind : std::uint8_t { Identity = 0, LosslessPredictor = 1, FixedRate = 2, ZfpRate = 3 };
+
+struct CodecSpec {
+  CodecKind kind = CodecKind::Identity;
+  int rate_bits = 0;
+
+  static CodecSpec identity() { return {CodecKind::Identity, 0}; }
+  static CodecSpec lossless() { return {CodecKind::LosslessPredictor, 0}; }
+  static CodecSpec fixed_rate(int bits);  // [2, 32] else InvalidSchemeError
+  static CodecSpec zfp_rate(int bits);    // [3, 32] else InvalidSchemeError
+
+  bool is_lossy() const { return kind == CodecKind::FixedRate || kind == CodecKind::ZfpRate; }
+  bool operator==(const CodecSpec&) const = default;
+};
+
+std::string to_string(const CodecSpec& spec);
+CodecSpec codec_spec_from_string(const std::string& s);
+
+inline constexpr std::size_t kFixedRateBlock = 64;
+inline constexpr std::size_t kPredictorChunk = 4096;
+inline constexpr std::size_t kContainerHeaderBytes = 18;
+
+struct CompressedBuffer {
+  CodecSpec codec;
+  std::uint64_t original_len = 0;
+  std::uint32_t chunk_count = 0;
+  std::vector<std::uint8_t> payload;
+
+  std::uint64_t payload_bytes() const { return payload.size(); }
+};
+
+CompressedBuffer compress(const CodecSpec& spec, const FloatBuffer& buf);
+FloatBuffer decompress(const CompressedBuffer& cbuf);
+std::uint64_t wire_size_bytes(const CodecSpec& spec, std::uint64_t n);
+std::vector<std::uint8_t> to_bytes(const CompressedBuffer& cbuf);
+CompressedBuffer from_bytes(const std::vector<std::uint8_t>& bytes);
+
+// The reference keeps single-threaded oracles here; on B200 they are the same
+// device path (there is no second implementation to compare against).
+namespace serial {
+CompressedBuffer compress(const CodecSpec& spec, const FloatBuffer& buf);
+FloatBuffer decompress(const CompressedBuffer& cbuf);
+}  // namespace serial
+
+// -------------------------------------------------------------- comm path --
+
+enum class CommPath { DpAllReduce = 0, PpP2p, TpAllReduce, TpAllGather, Zero1AllGather, Zero1ReduceScatter };
+
+inline constexpr std::array<CommPath, 6> kAllCommPaths = {
+    CommPath::DpAllReduce, CommPath::PpP2p, CommPath::TpAllReduce,
+    CommPath::TpAllGather, CommPath::Zero1AllGather, CommPath::Zero1ReduceScatter};
+
+const char* to_string(CommPath p);
+CommPath comm_path_from_string(const std::string& s);
+
+// ------------------------------------------------------- clock and trace --
+
+struct Topology {
+  int num_nodes = 1;
+  int gpus_per_node = 1;
+  double intra_bw = 0, inter_bw = 0, intra_lat = 0, inter_lat = 0, codec_bw = 0, compute_flops = 0;
+
+  int world_size() const { return num_nodes * gpus_per_node; }
+  int node_of(int rank) const { return rank / gpus_per_node; }
+  static Topology lassen_like(int num_nodes = 2);
+  static Topology desk_2x2(int num_nodes = 2);
+  static Topology b200_box(int num_gpus = 8);
+  static Topology preset(const std::string& name, int num_nodes);
+};
+
+enum class CollectiveKind { AllReduce, AllGather, ReduceScatter, P2P, Broadcast };
+const char* to_string(CollectiveKind c);
+
+struct TraceEvent {
+  int step = 0;
+  CommPath path = CommPath::DpAllReduce;
+  CollectiveKind collective = CollectiveKind::AllReduce;
+  int comm_size = 0;
+  std::uint64_t raw_bytes = 0;   // per-rank sent bytes
+  std::uint64_t wire_bytes = 0;
+  double duration_s = 0;         // measured device time of the collective
+  int round_count = 0;
+};
+
+class SimClock {
+ public:
+  explicit SimClock(const Topology& topo) : topo_(topo), clock_(topo.world_size(), 0.0) {}
+  const Topology& topology() const { return topo_; }
+  double time(int rank) const { return clock_.at(rank); }
+  double max_time() const;
+  void advance(int rank, double dt);
+  void sync_to_max(std::span<const int> ranks);
+  void set_step(int step) { step_ = step; }
+  int step() const { return step_; }
+  void record(TraceEvent e);
+  const std::vector<TraceEvent>& trace() const { return trace_; }
+
+ private:
+  Topology topo_;
+  std::vector<double> clock_;
+  std::vector<TraceEvent> trace_;
+  int step_ = 0;
+};
+
+void write_trace_csv(std::ostream& os, const std::vector<TraceEvent>& trace);
+
+// ------------------------------------------------------------ collectives --
+
+struct Communicator {
+  std::vector<int> ranks;
+  int size() const { return static_cast<int>(ranks.size()); }
+};
+
+enum class ReduceMode { Sum, Average };
+
+FloatBuffer p2p(SimClock& clock, int src, int dst, const FloatBuffer& buf, const CodecSpec& spec, CommPath path);
+std::vector<FloatBuffer> ring_reduce_scatter(SimClock& clock, const Communicator& comm,
+                                             const std::vector<FloatBuffer>& inputs, const CodecSpec& spec,
+                                             CommPath path);
+std::vector<FloatBuffer> ring_allgather(SimClock& clock, const Communicator& comm,
+                                        const std::vector<FloatBuffer>& shards, const CodecSpec& spec,
+                                        CommPath path);
+std::vector<FloatBuffer> allreduce(SimClock& clock, const Communicator& comm, const std::vector<FloatBuffer>& inputs,
+                                   const CodecSpec& spec, CommPath path, ReduceMode mode = ReduceMode::Sum);
+// Addition: every member (root included) receives dec(comp(buf)).
+std::vector<FloatBuffer> broadcast(SimClock& clock, const Communicator& comm, int root, const FloatBuffer& buf,
+                                   const CodecSpec& spec, CommPath path);
+
+// ------------------------------------------------ layout and rate policy --
+
+struct ParallelLayout {
+  int dp = 1, pp = 1, tp = 1;
+  int world() const { return dp * pp * tp; }
+  int rank_of(int d, int p, int t) const { return d * (pp * tp) + p * tp + t; }
+  struct Coord {
+    int d, p, t;
+  };
+  Coord coord_of(int rank) const { return {rank / (pp * tp), (rank / tp) % pp, rank % tp}; }
+  std::vector<int> dp_group(int rank) const;
+  std::vector<int> tp_group(int rank) const;
+  std::vector<int> pp_chain(int rank) const;
+};
+
+ParallelLayout build_layout(int dp, int pp, int tp, const Topology& topo);
+
+struct SchemeTable {
+  std::string name;
+  std::map<CommPath, CodecSpec> paths;
+  const CodecSpec& at(CommPath p) const { return paths.at(p); }
+};
+
+SchemeTable scheme_no_compression();
+SchemeTable scheme_naive(const CodecSpec& spec);
+SchemeTable scheme_mz_hybrid(int dp_rate);
+SchemeTable scheme_z_hybrid(int mp_rate, int dp_rate);
+SchemeTable scheme_from_name(const std::string& name);
+
+// Device the shim runs on (default: the current CUDA device / 0).
+void set_device(int device);
+
+}  // namespace hcc
+
+#endif  // HCC_B200_HPP

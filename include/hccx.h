@@ -5,7 +5,7 @@
  * (arxiv/paper_2409_02423, "hybridcomm", /root/reference/proj).  The
  * reference has no C ABI: its interface is the C++ header API quoted beside
  * each entry point below.  The C++ host mirror of that API (namespace hcc,
- * include/hcc/*.hpp, paper_2409_02423_b200/host/) is a thin shim over these
+ * include/hcc/hcc_b200.hpp, paper_2409_02423_b200/host/) is a thin shim over these
  * functions, and INTEGRATION.md shows the ctypes/extern "C" bindings.
  *
  * Conventions
@@ -150,6 +150,22 @@ HCCX_API hccx_status_t hccx_group_broadcast(hccx_group_t g, int root, const floa
  * d_out = dec(comp(d_in)). */
 HCCX_API hccx_status_t hccx_group_p2p(hccx_group_t g, const float* d_in, float* d_out, uint64_t n,
                              hccx_codec_t codec, void* stream);
+/* Host-buffer variants (the reference's value semantics: host vectors in,
+ * host vectors out).  Members' buffers are copied to the group's device,
+ * the same kernels run, results are copied back; *device_seconds (nullable)
+ * receives the device time of the collective itself (CUDA events). */
+HCCX_API hccx_status_t hccx_group_allreduce_host(hccx_group_t g, const float* const* h_in, float* const* h_out,
+                                                 uint64_t n, hccx_codec_t codec, int mode, double* device_seconds);
+HCCX_API hccx_status_t hccx_group_reduce_scatter_host(hccx_group_t g, const float* const* h_in,
+                                                      float* const* h_shard, uint64_t n, hccx_codec_t codec,
+                                                      double* device_seconds);
+HCCX_API hccx_status_t hccx_group_allgather_host(hccx_group_t g, const float* const* h_shard, float* const* h_out,
+                                                 uint64_t shard_n, hccx_codec_t codec, double* device_seconds);
+HCCX_API hccx_status_t hccx_group_broadcast_host(hccx_group_t g, int root, const float* h_in, float* const* h_out,
+                                                 uint64_t n, hccx_codec_t codec, double* device_seconds);
+HCCX_API hccx_status_t hccx_group_p2p_host(hccx_group_t g, const float* h_in, float* h_out, uint64_t n,
+                                           hccx_codec_t codec, double* device_seconds);
+
 /* Synchronise and report the group's device error flag (see hccx_flag_status). */
 HCCX_API hccx_status_t hccx_group_status(hccx_group_t g, void* stream);
 

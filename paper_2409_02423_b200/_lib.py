@@ -59,6 +59,12 @@ hccx_group_allgather = _sig("hccx_group_allgather", _st, _p, _pp, _pp, _u64, Cod
 hccx_group_broadcast = _sig("hccx_group_broadcast", _st, _p, C.c_int, _p, _pp, _u64, Codec, _p)
 hccx_group_p2p = _sig("hccx_group_p2p", _st, _p, _p, _p, _u64, Codec, _p)
 hccx_group_status = _sig("hccx_group_status", _st, _p, _p)
+_dp = C.POINTER(C.c_double)
+hccx_group_allreduce_host = _sig("hccx_group_allreduce_host", _st, _p, _pp, _pp, _u64, Codec, C.c_int, _dp)
+hccx_group_reduce_scatter_host = _sig("hccx_group_reduce_scatter_host", _st, _p, _pp, _pp, _u64, Codec, _dp)
+hccx_group_allgather_host = _sig("hccx_group_allgather_host", _st, _p, _pp, _pp, _u64, Codec, _dp)
+hccx_group_broadcast_host = _sig("hccx_group_broadcast_host", _st, _p, C.c_int, _p, _pp, _u64, Codec, _dp)
+hccx_group_p2p_host = _sig("hccx_group_p2p_host", _st, _p, _p, _p, _u64, Codec, _dp)
 hccx_comm_create = _sig("hccx_comm_create", _st, C.c_int, C.c_int, C.c_int, _u64, C.POINTER(_p))
 hccx_comm_export = _sig("hccx_comm_export", _st, _p, _p)
 hccx_comm_connect = _sig("hccx_comm_connect", _st, _p, _p)

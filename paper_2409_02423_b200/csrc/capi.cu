@@ -601,3 +601,147 @@ extern "C" hccx_status_t hccx_group_status(hccx_group_t g, void* stream) {
   DeviceGuard guard(g->device);
   return read_flag(g->d_err, static_cast<cudaStream_t>(stream));
 }
+
+// ----------------------------------------- host-buffer group variants ----
+
+namespace {
+
+struct DevBufs {
+  std::vector<float*> ptrs;
+  ~DevBufs() {
+    for (float* p : ptrs) cudaFree(p);
+  }
+  float* add(uint64_t n) {
+    float* p = nullptr;
+    if (cudaMalloc(&p, 4 * (n ? n : 1)) != cudaSuccess) return nullptr;
+    ptrs.push_back(p);
+    return p;
+  }
+};
+
+template <class F>
+hccx_status_t timed_run(hccx_group* g, double* secs, F&& body) {
+  cudaStream_t s = nullptr;
+  cudaEvent_t a = nullptr, b = nullptr;
+  if (cudaEventCreate(&a) != cudaSuccess || cudaEventCreate(&b) != cudaSuccess) return HCCX_ERR_CUDA;
+  cudaEventRecord(a, s);
+  hccx_status_t st = body(s);
+  cudaEventRecord(b, s);
+  if (st == HCCX_OK) st = hccx_group_status(g, s);
+  float ms = 0.0f;
+  if (cudaEventSynchronize(b) == cudaSuccess) cudaEventElapsedTime(&ms, a, b);
+  if (secs) *secs = ms * 1e-3;
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  return st;
+}
+
+hccx_status_t h2d(float* d, const float* h, uint64_t n) {
+  return n ? cuda_status(cudaMemcpy(d, h, 4 * n, cudaMemcpyHostToDevice)) : HCCX_OK;
+}
+hccx_status_t d2h(float* h, const float* d, uint64_t n) {
+  return n ? cuda_status(cudaMemcpy(h, d, 4 * n, cudaMemcpyDeviceToHost)) : HCCX_OK;
+}
+
+}  // namespace
+
+extern "C" hccx_status_t hccx_group_allreduce_host(hccx_group_t g, const float* const* h_in, float* const* h_out,
+                                                   uint64_t n, hccx_codec_t codec, int mode, double* secs) {
+  hccx_status_t st = check_group(g, codec);
+  if (st != HCCX_OK) return st;
+  if (n % static_cast<uint64_t>(g->p) != 0) return HCCX_ERR_BAD_CHUNKING;
+  DeviceGuard guard(g->device);
+  DevBufs B;
+  std::vector<float*> din(g->p), dout(g->p);
+  for (int j = 0; j < g->p; ++j) {
+    if (!(din[j] = B.add(n)) || !(dout[j] = B.add(n))) return HCCX_ERR_CUDA;
+    if ((st = h2d(din[j], h_in[j], n)) != HCCX_OK) return st;
+  }
+  st = timed_run(g, secs, [&](cudaStream_t s) {
+    return hccx_group_allreduce(g, din.data(), dout.data(), n, codec, mode, s);
+  });
+  if (st != HCCX_OK) return st;
+  for (int j = 0; j < g->p; ++j)
+    if ((st = d2h(h_out[j], dout[j], n)) != HCCX_OK) return st;
+  return HCCX_OK;
+}
+
+extern "C" hccx_status_t hccx_group_reduce_scatter_host(hccx_group_t g, const float* const* h_in,
+                                                        float* const* h_shard, uint64_t n, hccx_codec_t codec,
+                                                        double* secs) {
+  hccx_status_t st = check_group(g, codec);
+  if (st != HCCX_OK) return st;
+  if (n % static_cast<uint64_t>(g->p) != 0) return HCCX_ERR_BAD_CHUNKING;
+  DeviceGuard guard(g->device);
+  const uint64_t c = n / g->p;
+  DevBufs B;
+  std::vector<float*> din(g->p), dsh(g->p);
+  for (int j = 0; j < g->p; ++j) {
+    if (!(din[j] = B.add(n)) || !(dsh[j] = B.add(c))) return HCCX_ERR_CUDA;
+    if ((st = h2d(din[j], h_in[j], n)) != HCCX_OK) return st;
+  }
+  st = timed_run(g, secs, [&](cudaStream_t s) {
+    return hccx_group_reduce_scatter(g, din.data(), dsh.data(), n, codec, s);
+  });
+  if (st != HCCX_OK) return st;
+  for (int j = 0; j < g->p; ++j)
+    if ((st = d2h(h_shard[j], dsh[j], g->p == 1 ? n : c)) != HCCX_OK) return st;
+  return HCCX_OK;
+}
+
+extern "C" hccx_status_t hccx_group_allgather_host(hccx_group_t g, const float* const* h_shard, float* const* h_out,
+                                                   uint64_t shard_n, hccx_codec_t codec, double* secs) {
+  hccx_status_t st = check_group(g, codec);
+  if (st != HCCX_OK) return st;
+  DeviceGuard guard(g->device);
+  const uint64_t n = shard_n * g->p;
+  DevBufs B;
+  std::vector<float*> dsh(g->p), dout(g->p);
+  for (int j = 0; j < g->p; ++j) {
+    if (!(dsh[j] = B.add(shard_n)) || !(dout[j] = B.add(n))) return HCCX_ERR_CUDA;
+    if ((st = h2d(dsh[j], h_shard[j], shard_n)) != HCCX_OK) return st;
+  }
+  st = timed_run(g, secs, [&](cudaStream_t s) {
+    return hccx_group_allgather(g, dsh.data(), dout.data(), shard_n, codec, s);
+  });
+  if (st != HCCX_OK) return st;
+  for (int j = 0; j < g->p; ++j)
+    if ((st = d2h(h_out[j], dout[j], n)) != HCCX_OK) return st;
+  return HCCX_OK;
+}
+
+extern "C" hccx_status_t hccx_group_broadcast_host(hccx_group_t g, int root, const float* h_in, float* const* h_out,
+                                                   uint64_t n, hccx_codec_t codec, double* secs) {
+  hccx_status_t st = check_group(g, codec);
+  if (st != HCCX_OK) return st;
+  DeviceGuard guard(g->device);
+  DevBufs B;
+  float* din = B.add(n);
+  std::vector<float*> dout(g->p);
+  if (!din) return HCCX_ERR_CUDA;
+  for (int j = 0; j < g->p; ++j)
+    if (!(dout[j] = B.add(n))) return HCCX_ERR_CUDA;
+  if ((st = h2d(din, h_in, n)) != HCCX_OK) return st;
+  st = timed_run(g, secs, [&](cudaStream_t s) {
+    return hccx_group_broadcast(g, root, din, dout.data(), n, codec, s);
+  });
+  if (st != HCCX_OK) return st;
+  for (int j = 0; j < g->p; ++j)
+    if ((st = d2h(h_out[j], dout[j], n)) != HCCX_OK) return st;
+  return HCCX_OK;
+}
+
+extern "C" hccx_status_t hccx_group_p2p_host(hccx_group_t g, const float* h_in, float* h_out, uint64_t n,
+                                             hccx_codec_t codec, double* secs) {
+  hccx_status_t st = check_group(g, codec);
+  if (st != HCCX_OK) return st;
+  DeviceGuard guard(g->device);
+  DevBufs B;
+  float* din = B.add(n);
+  float* dout = B.add(n);
+  if (!din || !dout) return HCCX_ERR_CUDA;
+  if ((st = h2d(din, h_in, n)) != HCCX_OK) return st;
+  st = timed_run(g, secs, [&](cudaStream_t s) { return hccx_group_p2p(g, din, dout, n, codec, s); });
+  if (st != HCCX_OK) return st;
+  return d2h(h_out, dout, n);
+}

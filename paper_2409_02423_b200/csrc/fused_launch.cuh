@@ -27,7 +27,8 @@ cudaError_t launch_fused_codec(const FusedParams& p, cudaStream_t stream) {
     configured.fetch_or(1ull << (dev & 63));
   }
   const uint64_t cap = static_cast<uint64_t>(fused_capacity(k, kFThreads2, smem));
-  const int grid = static_cast<int>(nseg < cap ? nseg : cap);
+  const uint64_t cap_ack = cap < kAckIdx ? cap : kAckIdx;
+  const int grid = static_cast<int>(nseg < cap_ack ? nseg : cap_ack);
   void* args[] = {const_cast<FusedParams*>(&p)};
   count_launch();
   return cudaLaunchCooperativeKernel(k, dim3(grid), dim3(kFThreads2), args, smem, stream);

@@ -79,7 +79,7 @@ struct FusedSmem {
 // A sender CTA waits once per slot per call on its own index's ack of the
 // slot's previous use before overwriting it -- back-to-back collectives
 // never race a slow receiver.
-constexpr uint32_t kAckIdx = 2048;  // > any co-resident grid (148 SMs x 8 CTAs)
+constexpr uint32_t kAckIdx = 1024;  // >= any co-resident grid of the fused kernel (148 SMs x 3 CTAs)
 
 __device__ __forceinline__ uint32_t* flag_ptr(const FusedParams& P, int rank, int cls, int slot, uint32_t idx) {
   const int p = P.p;
@@ -642,9 +642,10 @@ __global__ void __launch_bounds__(kFThreads2, 3) ring_fused_kernel(const __grid_
       }
       // every segment of the phase has been computed (tfull) -> its inbox
       // inputs are consumed: acknowledge for this CTA's index space
-      if (f.ack_rank >= 0) {
+      if (f.ack_rank >= 0) {  // one fence, then relaxed stores of the ack words
+        fence_acq_rel_sys();
         for (uint32_t kk = blockIdx.x + lane * G; kk < kAckIdx; kk += G * 32)
-          st_release_sys(flag_ptr(P, f.ack_rank, f.ack_cls, f.ack_slot, 0) + kk, f.ack_ep);
+          st_relaxed_sys(flag_ptr(P, f.ack_rank, f.ack_cls, f.ack_slot, 0) + kk, f.ack_ep);
       }
     }
     if (lane == 0) {
