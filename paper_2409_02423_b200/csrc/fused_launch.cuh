@@ -2,6 +2,7 @@
 // by the per-rate-range translation units.
 #pragma once
 #include <atomic>
+#include <cstdio>
 #include <mutex>
 #include <unordered_map>
 
@@ -18,7 +19,7 @@ cudaError_t launch_fused_codec(const FusedParams& p, cudaStream_t stream) {
   const uint64_t groups = (p.n_chunk + kGroupVals - 1) / kGroupVals;
   const uint64_t nseg = (groups + kSegGroups - 1) / kSegGroups;
   if (nseg == 0) return cudaSuccess;
-  constexpr uint32_t smem = sizeof(FusedSmem2);
+  constexpr uint32_t smem = sizeof(FusedSmem2<Codec>);
   static std::atomic<uint64_t> configured{0};  // one bit per device
   int dev = 0;
   cudaGetDevice(&dev);
@@ -31,6 +32,13 @@ cudaError_t launch_fused_codec(const FusedParams& p, cudaStream_t stream) {
   const int grid = static_cast<int>(nseg < cap_ack ? nseg : cap_ack);
   void* args[] = {const_cast<FusedParams*>(&p)};
   count_launch();
+  if (p.debug & 64) {
+    int b = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k, kFThreads2, smem);
+    std::fprintf(stderr, "hccx fused launch rank %d: op %d n_chunk %llu nseg %llu cap %llu grid %d smem %u occ %d\n",
+                 p.rank, p.op, static_cast<unsigned long long>(p.n_chunk), static_cast<unsigned long long>(nseg),
+                 static_cast<unsigned long long>(cap), grid, smem, b);
+  }
   return cudaLaunchCooperativeKernel(k, dim3(grid), dim3(kFThreads2), args, smem, stream);
 }
 

@@ -58,7 +58,7 @@ struct FusedParams {
   uint64_t timeout_ns;
   uint64_t* trace;  // optional event log (hccx_comm_trace_enable): [0] = count, then (tag, t_ns) pairs
   uint64_t trace_cap;
-  int debug;  // development knobs (HCCX_DEBUG): 1 skip pushes, 2 skip system fence, 4 skip segment barriers
+  int debug;  // development knobs (HCCX_DEBUG): 16 = warp-store pushes, 32 = synchronous tile release, 64 = log launches
 };
 
 struct FusedSmem {
@@ -99,9 +99,22 @@ __device__ __forceinline__ uint8_t* slot_ptr(const FusedParams& P, int rank, int
 }
 
 // Thread 0 spins until *flag >= epoch (wrap-safe) or the timeout expires.
+// Expired waits are logged (trace words 4000..4090: cta << 32 | who) so the
+// wait chain of a stalled collective can be read back.
+__device__ __forceinline__ void trace_timeout(const FusedParams& P, uint32_t who, const uint32_t* prog = nullptr) {
+  if (!P.trace) return;
+  unsigned long long* t = reinterpret_cast<unsigned long long*>(P.trace);
+  const unsigned long long i = atomicAdd(t + 4000, 1ull);
+  if (i < 90) t[4001 + i] = (static_cast<unsigned long long>(blockIdx.x) << 32) | who;
+  if (atomicCAS(t + 4095, 0ull, (static_cast<unsigned long long>(blockIdx.x) << 32) | who) == 0ull && prog) {
+    for (int w = 0; w < 10; ++w) t[4200 + w] = prog[w];
+  }
+}
+
 // Once any wait of this rank has timed out (err word), later waits return at
 // once, so a dead peer costs one timeout, not one per segment.
-__device__ __forceinline__ void spin_ge(const FusedParams& P, const uint32_t* flag, uint32_t epoch) {
+__device__ __forceinline__ void spin_ge(const FusedParams& P, const uint32_t* flag, uint32_t epoch,
+                                        uint32_t who = 0x600u) {
   if (static_cast<int32_t>(ld_acquire_sys(flag) - epoch) >= 0) return;
   if (P.err && (ldg_u32_coherent(P.err) & kErrTimeout)) return;
   const uint64_t t0 = globaltimer_ns();
@@ -111,6 +124,38 @@ __device__ __forceinline__ void spin_ge(const FusedParams& P, const uint32_t* fl
       if (P.err && (ldg_u32_coherent(P.err) & kErrTimeout)) return;
       if (globaltimer_ns() - t0 > P.timeout_ns) {
         if (P.err) atomicOr(P.err, kErrTimeout);
+        trace_timeout(P, who | (epoch << 12));
+        return;
+      }
+    }
+  }
+}
+
+// Bounded mbarrier wait for the fused kernel: a pipeline that stops making
+// progress (a bug, or a peer that died mid-collective) turns into
+// kErrTimeout + an identifying trace word instead of a hung GPU.
+__device__ __forceinline__ void mbar_wait_to(const FusedParams& P, uint64_t* bar, uint32_t parity, uint32_t who,
+                                             const uint32_t* prog = nullptr) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  if (ok) return;
+  const uint64_t t0 = globaltimer_ns();
+  for (uint32_t spins = 0;; ++spins) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (ok) return;
+    if ((spins & 255u) == 255u) {
+      if (P.err && (ldg_u32_coherent(P.err) & kErrTimeout)) return;
+      if (globaltimer_ns() - t0 > P.timeout_ns) {
+        if (P.err) atomicOr(P.err, kErrTimeout);
+        trace_timeout(P, who, prog);
         return;
       }
     }
@@ -213,34 +258,47 @@ __device__ __forceinline__ void fused_group(const FusedParams& P, const uint8_t*
 // *phases* (ring rounds, allgather receives, ...; see phase_of) that both
 // roles walk in the same order.  The producer's elected lane waits for each
 // step's inbound-data flag, then streams every segment's inputs (inbox
-// payload and/or local fp32) into a kFStages-deep shared-memory ring with
+// payload and/or local fp32) into a per-phase carved (up to kFMaxStages deep) shared-memory ring with
 // cp.async.bulk (completing on the stage's "full" mbarrier).  Compute warps
 // decode / add / encode one group each per segment straight from shared
 // memory, release the stage ("empty" mbarrier), stage the encoded segment in
 // `tile` and push it to the peer window(s) with 16-byte stores.  HBM latency
-// is therefore hidden behind kFStages segments of prefetch per CTA.
+// is therefore hidden behind several segments of prefetch per CTA.
 // Partial segments (and unaligned buffers / non-word codecs) are read
 // directly from global memory instead ("direct" stages).
 // ---------------------------------------------------------------------------
 
-constexpr int kFStages = 3;
-constexpr int kFTiles = 3;
-constexpr uint32_t kFPrefetch = 4;  // L2 prefetch distance (segments)
-constexpr int kFCompute = kFusedWarps;              // compute warps
-constexpr int kFThreads2 = (kFCompute + 2) * 32;    // + producer warp + pusher warp
-constexpr uint32_t kFStageA = 8448;                 // >= 8 x 1028 B payload groups / 8 KiB fp32, 128B multiple
-constexpr uint32_t kFStageB = 8192;                 // 8 groups x 1 KiB fp32
-constexpr uint32_t kFStageBytes = kFStageA + kFStageB;
-static_assert(kFStageA >= kFCompute * kStageBytes, "direct-mode staging aliases stage A");
+constexpr int kFMaxStages = 8;                      // input ring depth cap (mbarrier pairs)
+constexpr uint32_t kFArena = 49152;                  // input ring bytes, carved per phase
+constexpr int kFMaxTiles = 8;                        // output (push) ring depth cap
+constexpr uint32_t kFTileBudget = 17408;             // output ring bytes
+constexpr int kFReadsInFlight = 4;                   // bulk pushes whose smem read may be pending
+constexpr uint32_t kFPrefetch = 4;                   // L2 prefetch distance (segments)
+constexpr int kFCompute = kFusedWarps;               // compute warps
+constexpr int kFThreads2 = (kFCompute + 2) * 32;     // + producer warp + pusher warp
+constexpr uint32_t kFTileBytes = 8448;               // >= 8 x 1028 B groups, 128B multiple
+constexpr uint32_t kFGenBytes = kFCompute * kStageBytes;
 
+// Output tiles hold one encoded segment (8 groups) each; their size follows
+// the codec (2 KiB at r8), so the ring is as deep as the budget allows.
+template <class Codec>
+struct TileGeom {
+  static constexpr uint32_t kBytes = (kSegGroups * Codec::kGroupBytes + 127u) / 128u * 128u;
+  static constexpr int kFit = static_cast<int>(kFTileBudget / kBytes);
+  static constexpr int kTiles = kFit > kFMaxTiles ? kFMaxTiles : (kFit < 2 ? 2 : kFit);
+};
+
+template <class Codec>
 struct FusedSmem2 {
-  uint8_t stage[kFStages][kFStageBytes];
-  uint8_t tile[kFTiles][kFStageA];
-  uint64_t full[kFStages];
-  uint64_t empty[kFStages];
-  uint64_t tfull[kFTiles];
-  uint64_t tempty[kFTiles];
-  uint32_t direct[kFStages];
+  uint8_t arena[kFArena];
+  uint8_t tile[TileGeom<Codec>::kTiles][TileGeom<Codec>::kBytes];
+  uint8_t gen[kFGenBytes];
+  uint64_t full[kFMaxStages];
+  uint64_t empty[kFMaxStages];
+  uint64_t tfull[kFMaxTiles];
+  uint64_t tempty[kFMaxTiles];
+  uint32_t direct[kFMaxStages];
+  uint32_t prog[kFCompute + 2];  // debug: per-warp progress word (phase << 20 | segment << 4 | state)
 };
 
 enum PhaseKind : int { kPhEnc = 0, kPhDar = 1, kPhFinAr = 2, kPhFinRs = 3, kPhDec = 4 };
@@ -260,6 +318,24 @@ struct Phase {
   int ack_rank, ack_cls, ack_slot;  // consumption ack at phase end (-1: none)
   uint32_t ack_ep;
 };
+
+// Per-phase input stage geometry: A = the phase's primary input of one
+// segment (fp32 for Enc, payload otherwise), B = local fp32 for the adds.
+struct StageGeom {
+  uint32_t a, b, stride;
+  int n;
+};
+
+template <class Codec>
+__device__ __forceinline__ StageGeom stage_geom(int kind) {
+  StageGeom g;
+  g.a = kind == kPhEnc ? kSegVals * 4u : (kSegGroups * Codec::kGroupBytes + 127u) / 128u * 128u;
+  g.b = (kind == kPhDar || kind == kPhFinAr || kind == kPhFinRs) ? kSegVals * 4u : 0u;
+  g.stride = g.a + g.b;
+  const uint32_t fit = kFArena / g.stride;
+  g.n = static_cast<int>(fit < kFMaxStages ? fit : kFMaxStages);
+  return g;
+}
 
 __device__ __forceinline__ int nphases(const FusedParams& P) {
   switch (P.op) {
@@ -396,10 +472,17 @@ __device__ __forceinline__ Phase phase_of(const FusedParams& P, int ph) {
 __device__ __forceinline__ void trace_ev(const FusedParams& P, uint32_t ev, uint32_t ph, uint32_t seg) {
   if (P.trace == nullptr || blockIdx.x != 0) return;
   const unsigned long long i = atomicAdd(reinterpret_cast<unsigned long long*>(P.trace), 1ull);
-  if (2 * i + 2 < P.trace_cap) {
+  if (2 * i + 2 < 4000 && 2 * i + 2 < P.trace_cap) {
     P.trace[1 + 2 * i] = (static_cast<uint64_t>(ev) << 32) | (static_cast<uint64_t>(ph) << 16) | seg;
     P.trace[2 + 2 * i] = globaltimer_ns();
   }
+}
+
+// Cycle accumulators for CTA 0 (written once at the end, slots 1..): a
+// breakdown of where each role's time goes without per-event round trips.
+__device__ __forceinline__ void trace_acc(const FusedParams& P, uint32_t slot, uint64_t cycles) {
+  if (P.trace == nullptr || blockIdx.x != 0) return;
+  atomicAdd(reinterpret_cast<unsigned long long*>(P.trace) + 4096 + slot, static_cast<unsigned long long>(cycles));
 }
 
 __device__ __forceinline__ uint32_t push_epoch(const FusedParams& P, int push_cls, int d) {
@@ -470,7 +553,11 @@ __device__ __forceinline__ void compute_group(const FusedParams& P, const Phase&
 template <class Codec>
 __global__ void __launch_bounds__(kFThreads2, 3) ring_fused_kernel(const __grid_constant__ FusedParams P) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
-  FusedSmem2& S = *reinterpret_cast<FusedSmem2*>(smem_raw);
+  FusedSmem2<Codec>& S = *reinterpret_cast<FusedSmem2<Codec>*>(smem_raw);
+  constexpr int kT = TileGeom<Codec>::kTiles;
+  // Compute needs tile (s mod kT) back before segment s; the pusher frees
+  // tiles up to seq - kRd after segment seq-1, so kRd must stay below kT.
+  constexpr int kRd = kFReadsInFlight < kT - 1 ? kFReadsInFlight : kT - 1;
   const int lane = static_cast<int>(lane_id()), warp = static_cast<int>(threadIdx.x >> 5);
   const int p = P.p, j = P.rank;
   const uint64_t c = P.n_chunk;
@@ -489,11 +576,11 @@ __global__ void __launch_bounds__(kFThreads2, 3) ring_fused_kernel(const __grid_
   auto seg_full = [&](uint32_t sg) { return (static_cast<uint64_t>(sg) + 1) * kSegVals <= c; };
 
   if (threadIdx.x == 0) {
-    for (int st = 0; st < kFStages; ++st) {
+    for (int st = 0; st < kFMaxStages; ++st) {
       mbar_init(&S.full[st], 1);
       mbar_init(&S.empty[st], kFCompute);
     }
-    for (int tt = 0; tt < kFTiles; ++tt) {
+    for (int tt = 0; tt < kT; ++tt) {
       mbar_init(&S.tfull[tt], kFCompute);
       mbar_init(&S.tempty[tt], 1);
     }
@@ -504,21 +591,25 @@ __global__ void __launch_bounds__(kFThreads2, 3) ring_fused_kernel(const __grid_
   if (warp == kFCompute) {
     // ------------------------------------------------------------ producer
     if (lane == 0) {
-      int st = 0;
-      uint32_t phase_bit = 0;
+      uint64_t c_empty = 0, c_flag = 0, c_total = clock64();
+      uint32_t pu = 0;  // per-barrier fill parity
       for (int ph = 0; ph < nph; ++ph) {
         const Phase f = phase_of(P, ph);
+        const StageGeom sg_ = stage_geom<Codec>(f.kind);
+        // the arena is re-carved for this phase: every earlier fill must be consumed
+        for (int b = 0; b < kFMaxStages; ++b) mbar_wait_to(P, &S.empty[b], ((pu >> b) & 1u) ^ 1u, 0x100u | b, S.prog);
+        int st = 0;
         for (uint32_t k0 = 0; k0 < myseg; k0 += kStepSegs) {
           const uint32_t k1 = min(k0 + kStepSegs, myseg);
           if (f.wait_cls >= 0) {
-            trace_ev(P, 10, ph, k0);
-            spin_ge(P, flag_ptr(P, j, f.wait_cls, f.wait_slot, seg_of(k0)), f.wait_ep);
+            const uint64_t t0 = clock64();
+            spin_ge(P, flag_ptr(P, j, f.wait_cls, f.wait_slot, seg_of(k0)), f.wait_ep, 0x700u | (ph << 4) | f.wait_cls);
             asm volatile("fence.proxy.async.global;" ::: "memory");
-            trace_ev(P, 11, ph, k0);
+            c_flag += clock64() - t0;
           }
           for (uint32_t k = k0; k < k1; ++k) {
             const uint32_t sg = seg_of(k);
-            // L2 prefetch kFPrefetch segments ahead (same phase), so the
+            // L2 prefetch kFPrefetch segments ahead (same step), so the
             // bulk load issued when the stage frees up hits L2
             if (tma_ok && k + kFPrefetch < k1) {
               const uint32_t sp = seg_of(k + kFPrefetch);
@@ -532,31 +623,32 @@ __global__ void __launch_bounds__(kFThreads2, 3) ring_fused_kernel(const __grid_
                 }
               }
             }
-            mbar_wait(&S.empty[st], phase_bit ^ 1u);
+            S.prog[kFCompute] = (ph << 20) | (k << 4) | 3u;
+            const uint64_t t1 = clock64();
+            mbar_wait_to(P, &S.empty[st], ((pu >> st) & 1u) ^ 1u, 0x200u | st, S.prog);
+            c_empty += clock64() - t1;
+            pu ^= 1u << st;
             const bool full_seg = tma_ok && seg_full(sg);
             S.direct[st] = full_seg ? 0u : 1u;
+            uint8_t* base = S.arena + st * sg_.stride;
             if (full_seg) {
               const uint32_t a_bytes = f.kind == kPhEnc ? kSegVals * 4u : static_cast<uint32_t>(kSegGroups * GB);
-              const uint32_t b_bytes =
-                  (f.kind == kPhDar || f.kind == kPhFinAr || f.kind == kPhFinRs) ? kSegVals * 4u : 0u;
-              mbar_arrive_expect_tx(&S.full[st], a_bytes + b_bytes);
+              mbar_arrive_expect_tx(&S.full[st], a_bytes + sg_.b);
               if (f.kind == kPhEnc)
-                bulk_g2s(S.stage[st], f.vals + static_cast<uint64_t>(sg) * kSegVals, a_bytes, &S.full[st]);
+                bulk_g2s(base, f.vals + static_cast<uint64_t>(sg) * kSegVals, a_bytes, &S.full[st]);
               else
-                bulk_g2s(S.stage[st], f.pay + static_cast<uint64_t>(sg) * kSegGroups * GB, a_bytes, &S.full[st]);
-              if (b_bytes)
-                bulk_g2s(S.stage[st] + kFStageA, f.vals + static_cast<uint64_t>(sg) * kSegVals, b_bytes,
-                         &S.full[st]);
+                bulk_g2s(base, f.pay + static_cast<uint64_t>(sg) * kSegGroups * GB, a_bytes, &S.full[st]);
+              if (sg_.b) bulk_g2s(base + sg_.a, f.vals + static_cast<uint64_t>(sg) * kSegVals, sg_.b, &S.full[st]);
             } else {
               mbar_arrive(&S.full[st]);  // consumers read this segment from global memory
             }
-            if (++st == kFStages) {
-              st = 0;
-              phase_bit ^= 1u;
-            }
+            if (++st == sg_.n) st = 0;
           }
         }
       }
+      trace_acc(P, 0, clock64() - c_total);
+      trace_acc(P, 1, c_empty);
+      trace_acc(P, 2, c_flag);
     }
     return;
   }
@@ -567,33 +659,57 @@ __global__ void __launch_bounds__(kFThreads2, 3) ring_fused_kernel(const __grid_
     // engine (one bulk store per destination window), recycles the tile
     // once the engine has read it, and publishes every step with one
     // release store per destination after its bulk writes completed.
+    // Control flow is uniform across the warp: lane 0 alone waits on and
+    // arrives at mbarriers, spins on credits and writes flags; the other
+    // lanes only join the 16-byte store loops.  Every lane passes exactly
+    // the same sequence of __syncwarp() calls (divergent lane-0 blocks plus
+    // __syncwarp at different sites let lanes drift a segment apart).
     int tt = 0;
     uint32_t tbit = 0;
-    int pending = -1;  // tile whose bulk read may still be in flight
+    uint32_t seq = 0, released = 0;  // segments seen / tiles handed back (ring order)
+    uint64_t c_tfull = 0, c_read = 0, c_pub = 0, c_credit = 0, c_total = clock64();
+    auto release_upto = [&](uint32_t upto) {
+      for (; released < upto; ++released) mbar_arrive(&S.tempty[released % kT]);
+    };
     for (int ph = 0; ph < nph; ++ph) {
       const Phase f = phase_of(P, ph);
       const bool push = f.push_cls >= 0;
+      const uint64_t tc = clock64();
       if (push && lane == 0) {  // credit: previous use of the destination slot(s) consumed
         for (int q = 1; q < p; ++q) {
           const int d = (j + q) % p;
           if (f.push_mode == 0 && d != (j + 1) % p) continue;
           if (f.push_mode == 2 && d != P.dst) continue;
           const uint32_t need = f.push_cls == 2 ? P.pp_epoch[d] - 1u : f.credit_ep;
-          spin_ge(P, flag_ptr(P, j, f.credit_cls, f.push_mode == 0 ? f.push_slot : d, blockIdx.x), need);
+          spin_ge(P, flag_ptr(P, j, f.credit_cls, f.push_mode == 0 ? f.push_slot : d, blockIdx.x), need,
+                  0x800u | (ph << 4) | f.credit_cls);
         }
       }
       __syncwarp();
+      c_credit += clock64() - tc;
       for (uint32_t k0 = 0; k0 < myseg; k0 += kStepSegs) {
         const uint32_t k1 = min(k0 + kStepSegs, myseg);
         for (uint32_t k = k0; k < k1; ++k) {
           const uint32_t sg = seg_of(k);
-          mbar_wait(&S.tfull[tt], tbit);
+          if (lane == 0) {
+            S.prog[kFCompute + 1] = (ph << 20) | (k << 4) | 2u;
+            const uint64_t t0 = clock64();
+            mbar_wait_to(P, &S.tfull[tt], tbit, 0x300u | tt, S.prog);
+            c_tfull += clock64() - t0;
+          }
+          __syncwarp();  // the tile is complete for every lane
+          bool bulk_issued = false;
           if (push) {
             const uint64_t soff = static_cast<uint64_t>(sg) * kSegGroups * GB;
             const uint64_t rem = wire - soff;
             const uint32_t nb = static_cast<uint32_t>(rem < kSegGroups * GB ? rem : kSegGroups * GB);
+            // TMA bulk push (one instruction per destination); HCCX_DEBUG
+            // bit 16 selects the warp's 16-byte stores instead.
             if ((nb & 15u) == 0 && !(P.debug & 16)) {
               if (lane == 0) {
+                // the tile was written through the generic proxy; the bulk
+                // copy reads it through the async proxy
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 for (int q = 1; q < p; ++q) {
                   const int d = (j + q) % p;
                   if (f.push_mode == 0 && q != 1) break;
@@ -602,6 +718,7 @@ __global__ void __launch_bounds__(kFThreads2, 3) ring_fused_kernel(const __grid_
                 }
                 bulk_commit();
               }
+              bulk_issued = true;
             } else {
               for (int q = 1; q < p; ++q) {
                 const int d = (j + q) % p;
@@ -613,31 +730,41 @@ __global__ void __launch_bounds__(kFThreads2, 3) ring_fused_kernel(const __grid_
                   reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(S.tile[tt])[i];
                 for (uint32_t b = (n16 << 4) + lane; b < nb; b += 32) dst[b] = S.tile[tt][b];
               }
-              __syncwarp();
             }
-            if (threadIdx.x == (kFCompute + 1) * 32 && lane == 0) trace_ev(P, 3, ph, k);
           }
-          // recycle the previous tile once its bulk read is done
+          ++seq;
+          __syncwarp();  // every lane's reads of the tile are done
           if (lane == 0) {
-            if (push) bulk_wait_read<1>();
-            if (pending >= 0) mbar_arrive(&S.tempty[pending]);
+            const uint64_t t1 = clock64();
+            if (bulk_issued && !(P.debug & 32)) {
+              bulk_wait_read<kRd>();  // hand tiles back once the TMA engine has read them
+              release_upto(seq > static_cast<uint32_t>(kRd) ? seq - kRd : 0);
+            } else {
+              if (bulk_issued) bulk_wait_read<0>();
+              release_upto(seq);
+            }
+            c_read += clock64() - t1;
           }
-          pending = tt;
-          if (++tt == kFTiles) {
+          if (++tt == kT) {
             tt = 0;
             tbit ^= 1u;
           }
         }
-        if (push) {  // publish the step after its bulk writes completed
-          if (lane == 0) bulk_wait_all();
-          __syncwarp();
+        if (push) {  // publish the step once its stores are complete
+          const uint64_t t2 = clock64();
+          if (lane == 0) {
+            bulk_wait_all();
+            release_upto(seq);
+          }
+          c_pub += clock64() - t2;
+          __syncwarp();  // all lanes' stores precede the release below (warp barrier + release cumulativity)
           if (lane < p - 1) {
             const int d = (j + 1 + lane) % p;
             const bool tgt =
                 f.push_mode == 1 || (f.push_mode == 0 && lane == 0) || (f.push_mode == 2 && d == P.dst);
             if (tgt) signal(flag_ptr(P, d, f.push_cls, f.push_slot, seg_of(k0)), push_epoch(P, f.push_cls, d));
           }
-          if (lane == 0) trace_ev(P, 5, ph, k0);
+          __syncwarp();
         }
       }
       // every segment of the phase has been computed (tfull) -> its inbox
@@ -647,46 +774,68 @@ __global__ void __launch_bounds__(kFThreads2, 3) ring_fused_kernel(const __grid_
         for (uint32_t kk = blockIdx.x + lane * G; kk < kAckIdx; kk += G * 32)
           st_relaxed_sys(flag_ptr(P, f.ack_rank, f.ack_cls, f.ack_slot, 0) + kk, f.ack_ep);
       }
+      __syncwarp();
     }
     if (lane == 0) {
       bulk_wait_all();
-      if (pending >= 0) mbar_arrive(&S.tempty[pending]);
+      release_upto(seq);
+      trace_acc(P, 8, clock64() - c_total);
+      trace_acc(P, 9, c_tfull);
+      trace_acc(P, 10, c_read);
+      trace_acc(P, 11, c_pub);
+      trace_acc(P, 12, c_credit);
     }
     return;
   }
 
   // -------------------------------------------------------------- compute
   uint32_t bad = 0;
-  int st = 0, tt = 0;
-  uint32_t phase_bit = 0, tbit = 0;
+  uint32_t cu = 0;  // per-barrier consume parity
+  int tt = 0;
+  uint32_t tbit = 0;
+  uint8_t* gen = S.gen + warp * kStageBytes;
+  uint64_t c_full = 0, c_tile = 0, c_comp = 0, c_total = clock64();
   for (int ph = 0; ph < nph; ++ph) {
     const Phase f = phase_of(P, ph);
+    const StageGeom sg_ = stage_geom<Codec>(f.kind);
+    int st = 0;
     for (uint32_t k = 0; k < myseg; ++k) {
       const uint32_t sg = seg_of(k);
-      mbar_wait(&S.full[st], phase_bit);
-      if (threadIdx.x == 0) trace_ev(P, 1, ph, k);
-      mbar_wait(&S.tempty[tt], tbit ^ 1u);
+      if (lane == 0) S.prog[warp] = (ph << 20) | (k << 4) | 1u;
+      const uint64_t t0 = clock64();
+      mbar_wait_to(P, &S.full[st], (cu >> st) & 1u, 0x400u | st, S.prog);
+      cu ^= 1u << st;
+      if (lane == 0) S.prog[warp] = (ph << 20) | (k << 4) | 2u;
+      const uint64_t t1 = clock64();
+      mbar_wait_to(P, &S.tempty[tt], tbit ^ 1u, 0x500u | tt, S.prog);
+      const uint64_t t2 = clock64();
+      c_full += t1 - t0;
+      c_tile += t2 - t1;
       const bool direct = S.direct[st] != 0;
       const uint64_t g = static_cast<uint64_t>(sg) * kSegGroups + warp;
-      const uint8_t* sa = S.stage[st] + (f.kind == kPhEnc ? warp * 1024u : warp * static_cast<uint32_t>(GB));
-      const uint8_t* sb = S.stage[st] + kFStageA + warp * 1024u;
-      uint8_t* gen = S.stage[st] + warp * kStageBytes;  // free in direct mode
+      const uint8_t* base = S.arena + st * sg_.stride;
+      const uint8_t* sa = base + (f.kind == kPhEnc ? warp * 1024u : warp * static_cast<uint32_t>(GB));
+      const uint8_t* sb = base + sg_.a + warp * 1024u;
       if (g < ngroups) compute_group<Codec>(P, f, g, direct, sa, sb, S.tile[tt] + warp * GB, gen, lane, bad);
       __syncwarp();
-      if (threadIdx.x == 0) trace_ev(P, 2, ph, k);
+      c_comp += clock64() - t2;
+      if (lane == 0) S.prog[warp] = (ph << 20) | (k << 4) | 3u;
       if (lane == 0) {
         mbar_arrive(&S.empty[st]);
         mbar_arrive(&S.tfull[tt]);
       }
-      if (++st == kFStages) {
-        st = 0;
-        phase_bit ^= 1u;
-      }
-      if (++tt == kFTiles) {
+      if (++st == sg_.n) st = 0;
+      if (++tt == kT) {
         tt = 0;
         tbit ^= 1u;
       }
     }
+  }
+  if (lane == 0 && warp == 0) {
+    trace_acc(P, 16, clock64() - c_total);
+    trace_acc(P, 17, c_full);
+    trace_acc(P, 18, c_tile);
+    trace_acc(P, 19, c_comp);
   }
   if constexpr (Codec::kCheckFinite) {
     if (__any_sync(kFull, bad) && lane == 0 && P.err) atomicOr(P.err, kErrNonFinite);

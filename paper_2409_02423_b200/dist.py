@@ -35,7 +35,12 @@ def exchange_handles(blob: bytes, group=None) -> List[bytes]:
 
 
 class NvlinkComm:
-    """One hccx communicator over the ranks of a torch.distributed group."""
+    """One hccx communicator over the ranks of a torch.distributed group.
+
+    Each collective is one cooperative kernel that occupies every SM and
+    spins on peer flags; do not keep NCCL (or other peer-waiting) kernels in
+    flight on other streams across a call -- synchronise first, as
+    ``timed()`` in the tools and bench.py do."""
 
     def __init__(self, max_n: int, group=None, device: Optional[int] = None):
         import torch
@@ -57,7 +62,13 @@ class NvlinkComm:
         allb = exchange_handles(bytes(blob), group)
         buf = (C.c_uint8 * (_lib.HANDLE_BYTES * self.size)).from_buffer_copy(b"".join(allb))
         check(_lib.hccx_comm_connect(self.h, buf), "comm_connect")
+        # The fused collectives are cooperative kernels that occupy every SM
+        # and wait on peers; an NCCL kernel still in flight on another stream
+        # (this barrier's) could then never be scheduled on one rank while its
+        # peer waits for it.  Drain it before the first collective.
+        torch.cuda.synchronize(self.device)
         dist.barrier(group)
+        torch.cuda.synchronize(self.device)
 
     # ------------------------------------------------------------------
     def _stream(self) -> int:
@@ -155,6 +166,7 @@ def bench_allreduce_main(args, metric, ClockSampler, peaks, traffic_for, cpu_all
 
     def timed(fn, steps):
         t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()  # no fused kernel may be in flight across an NCCL call
         dist.barrier()
         torch.cuda.synchronize()
         torch.cuda._sleep(int(1e6))

@@ -31,6 +31,7 @@ def timed(fn, steps, warm=2):
         fn()
     s = torch.cuda.current_stream()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()  # no fused kernel may be in flight across an NCCL call
     dist.barrier()
     torch.cuda.synchronize()
     torch.cuda._sleep(int(2e6))

@@ -13,14 +13,16 @@ from paper_2409_02423_b200 import CodecSpec  # noqa: E402
 from paper_2409_02423_b200 import dist as D  # noqa: E402
 
 
-def timed(fn, steps=10, warm=3):
+def timed(fn, steps=int(os.environ.get("SWEEP_STEPS", "10")), warm=int(os.environ.get("SWEEP_WARM", "3"))):
     for _ in range(warm):
         fn()
     s = torch.cuda.current_stream()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()  # no fused kernel may be in flight across an NCCL call
     dist.barrier()
     torch.cuda.synchronize()
-    torch.cuda._sleep(int(2e6))
+    if not int(os.environ.get("SWEEP_NOSLEEP", "0")):
+        torch.cuda._sleep(int(2e6))
     a.record(s)
     for _ in range(steps):
         fn()
@@ -38,6 +40,19 @@ def main():
     rank, p = dist.get_rank(), dist.get_world_size()
     sizes = [int(s) for s in os.environ.get("SWEEP_SIZES", str(1 << 26)).split(",")]
     comm = D.NvlinkComm(max(sizes))
+    import ctypes as C
+
+    from paper_2409_02423_b200 import _lib
+    cap = 1 << 16
+    _lib.hccx_comm_trace_enable(comm.h, cap)
+
+    def who():
+        buf = (C.c_uint64 * cap)()
+        nw = C.c_uint64()
+        _lib.hccx_comm_trace_read(comm.h, buf, cap, C.byref(nw))
+        n = min(buf[4000], 90)
+        prog = [hex(buf[4200 + w]) for w in range(10)]
+        return [hex(buf[4001 + i]) for i in range(n)][:3] + ["first:", hex(buf[4095]), "prog:"] + prog
     codecs = os.environ.get("SWEEP_CODECS", "identity,fixed-rate:4,fixed-rate:8,fixed-rate:16").split(",")
     ops = os.environ.get("SWEEP_OPS", "ar,rs,ag,nccl").split(",")
     for n in sizes:
@@ -63,7 +78,11 @@ def main():
                 row["pp_GBps_raw"] = round(4 * n / (row["pp_ms"] * 1e-3) / 1e9, 1)
             if "ar_ms" in row:
                 row["ar_GBps"] = round(4 * n / (row["ar_ms"] * 1e-3) / 1e9, 1)
-            comm.status()
+            try:
+                comm.status()
+            except Exception as e:
+                print(f"rank {rank} {cs} n={n}: {e} who={who()}", flush=True)
+                raise
             if rank == 0:
                 print(json.dumps({k: (round(v, 4) if isinstance(v, float) else v) for k, v in row.items()}), flush=True)
         if "sendrecv" in ops:

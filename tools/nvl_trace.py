@@ -27,15 +27,37 @@ torch.cuda.synchronize()
 cap = 1 << 16
 _lib.hccx_comm_trace_enable(comm.h, cap)
 dist.barrier()
+reps = int(os.environ.get("TRACE_REPS", "1"))
 if op == "ar":
-    comm.allreduce(x, spec, 0, out)
+    for _ in range(reps):
+        comm.allreduce(x, spec, 0, out)
 elif op == "pp":
-    comm.p2p(x, 0, 1, spec, out if rank == 1 else None)
+    for _ in range(reps):
+        comm.p2p(x, 0, 1, spec, out if rank == 1 else None)
 elif op == "ag":
-    comm.allgather(x[: n // p].contiguous(), spec, out)
+    for _ in range(reps):
+        comm.allgather(x[: n // p].contiguous(), spec, out)
+elif op == "rs":
+    for _ in range(reps):
+        comm.reduce_scatter(x, spec)
+torch.cuda.synchronize()
+try:
+    comm.status()
+    print(f"rank {rank} {op}: ok", flush=True)
+except Exception as e:
+    print(f"rank {rank} {op}: {e}", flush=True)
 buf = (C.c_uint64 * cap)()
 nw = C.c_uint64()
 _lib.hccx_comm_trace_read(comm.h, buf, cap, C.byref(nw))
+acc = {k: buf[4096 + k] for k in range(24)}
+if buf[4095]:
+    print(f"rank {rank}: pipeline wait timed out: cta {buf[4095] >> 32} who {hex(buf[4095] & 0xffffffff)}", flush=True)
+names = {0: "prod_total", 1: "prod_wait_empty", 2: "prod_wait_flag", 8: "push_total", 9: "push_wait_tfull",
+         10: "push_wait_read", 11: "push_publish", 12: "push_credit", 16: "comp_total", 17: "comp_wait_full",
+         18: "comp_wait_tile", 19: "comp_compute"}
+with open(f"gpurun_out/acc_r{rank}_{op}.txt", "w") as fh:
+    for k, nm in names.items():
+        fh.write(f"r{rank} {op} {nm:18s} {acc[k] / 1.9e3:10.1f} us (@1.9GHz)\n")
 cnt = buf[0]
 ev = sorted((buf[2 + 2 * i], buf[1 + 2 * i]) for i in range(min(cnt, (cap - 1) // 2)))
 if ev:
