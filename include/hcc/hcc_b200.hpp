@@ -14,8 +14,9 @@
 //   * broadcast() collective and CollectiveKind::Broadcast;
 //   * TraceEvent::duration_s is the measured device time (no alpha-beta
 //     model); Topology keeps the shape (world size, rank -> node) only.
-// Not on the device path yet: the LosslessPredictor codec
-// (compress/decompress throw hcc::Error; collectives with it throw too).
+//   * LosslessPredictor runs on the device (csrc/lossless.cu); collectives
+//     move its values through the identity ring (the codec is transparent)
+//     and size every hop's message with the device size pass.
 #ifndef HCC_B200_HPP
 #define HCC_B200_HPP
 

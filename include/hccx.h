@@ -62,7 +62,7 @@ typedef enum hccx_status {
 /* hcc::CodecKind (codec.hpp:16-20) plus the zfp-mode codec. */
 typedef enum hccx_codec_kind {
   HCCX_CODEC_IDENTITY = 0,
-  HCCX_CODEC_LOSSLESS = 1, /* LosslessPredictor: size law and host codec only */
+  HCCX_CODEC_LOSSLESS = 1, /* LosslessPredictor: hccx_lossless_* (data-dependent size) */
   HCCX_CODEC_FIXED_RATE = 2,
   HCCX_CODEC_ZFP_RATE = 3 /* NOT in the reference: 1-D zfp fixed-rate, 4*rate bits/block */
 } hccx_codec_kind_t;
@@ -118,6 +118,44 @@ HCCX_API hccx_status_t hccx_compress_host(hccx_codec_t codec, const float* h_in,
                                  int device);
 HCCX_API hccx_status_t hccx_decompress_host(hccx_codec_t codec, const uint8_t* h_in, uint64_t payload_bytes,
                                    uint64_t n, float* h_out, int device);
+
+/* ------------------------------------------------- lossless predictor -- */
+/* hcc::CodecKind::LosslessPredictor on the device (src/codec_kernels.hpp:
+ * 165-239 chunk coder, src/codec_serial.cpp:48-66 / :85-107 buffer layout):
+ * [ceil(nchunks/8) raw-fallback flag bytes][4096-value chunks].  The size is
+ * data-dependent, so these calls synchronise `stream` to report it. */
+
+/* Worst-case payload bytes for n values (every chunk raw): the capacity to
+ * pass to hccx_lossless_compress. */
+HCCX_API uint64_t hccx_lossless_max_bytes(uint64_t n);
+/* Exact payload bytes hcc::compress(LosslessPredictor) would produce
+ * (codec_kernels.hpp:203-215 per chunk + flag bytes).  Synchronises. */
+HCCX_API hccx_status_t hccx_lossless_size(const float* d_in, uint64_t n, uint64_t* bytes, void* stream);
+/* Device compress; *bytes = payload size.  capacity < size ->
+ * HCCX_ERR_INVALID_ARGUMENT (nothing written).  Synchronises. */
+HCCX_API hccx_status_t hccx_lossless_compress(const float* d_in, uint64_t n, uint8_t* d_out, uint64_t capacity,
+                                              uint64_t* bytes, void* stream);
+/* Device decompress of `bytes` payload bytes into n values.  A truncated or
+ * over-long stream -> HCCX_ERR_CORRUPT_PAYLOAD (codec_serial.cpp:91-104).
+ * Synchronises. */
+HCCX_API hccx_status_t hccx_lossless_decompress(const uint8_t* d_in, uint64_t bytes, uint64_t n, float* d_out,
+                                                void* stream);
+/* Host-buffer variants run on `device`. */
+HCCX_API hccx_status_t hccx_lossless_compress_host(const float* h_in, uint64_t n, uint8_t* h_out, uint64_t capacity,
+                                                   uint64_t* bytes, int device);
+HCCX_API hccx_status_t hccx_lossless_decompress_host(const uint8_t* h_in, uint64_t bytes, uint64_t n, float* h_out,
+                                                     int device);
+
+/* Ring wire bytes (TraceEvent::wire_bytes * p) under LosslessPredictor,
+ * which the size law cannot give: every hop's message is sized by the device
+ * size pass.  collective: 0 reduce-scatter (d_in[j] = member j's n values;
+ * the p(p-1) partial folds of collectives.cpp:34-61), 1 allgather (d_in[j] =
+ * member j's n-value shard, each crossing p-1 hops, :94-106), 2 allreduce
+ * (both).  Synchronises. */
+HCCX_API hccx_status_t hccx_lossless_ring_wire(const float* const* d_in, int p, uint64_t n, int collective,
+                                               uint64_t* wire, void* stream);
+HCCX_API hccx_status_t hccx_lossless_ring_wire_host(const float* const* h_in, int p, uint64_t n, int collective,
+                                                    uint64_t* wire, int device);
 
 /* ------------------------------------------- single-device ring (group) -- */
 /* All p members' buffers live on one device ("virtual ranks"): the value

@@ -51,6 +51,15 @@ hccx_decompress = _sig("hccx_decompress", _st, Codec, _p, _u64, _u64, _p, _p)
 hccx_flag_status = _sig("hccx_flag_status", _st, _p, _p)
 hccx_compress_host = _sig("hccx_compress_host", _st, Codec, _p, _u64, _p, C.c_int)
 hccx_decompress_host = _sig("hccx_decompress_host", _st, Codec, _p, _u64, _u64, _p, C.c_int)
+hccx_lossless_max_bytes = _sig("hccx_lossless_max_bytes", _u64, _u64)
+hccx_lossless_size = _sig("hccx_lossless_size", _st, _p, _u64, C.POINTER(_u64), _p)
+hccx_lossless_compress = _sig("hccx_lossless_compress", _st, _p, _u64, _p, _u64, C.POINTER(_u64), _p)
+hccx_lossless_decompress = _sig("hccx_lossless_decompress", _st, _p, _u64, _u64, _p, _p)
+hccx_lossless_compress_host = _sig("hccx_lossless_compress_host", _st, _p, _u64, _p, _u64, C.POINTER(_u64), C.c_int)
+hccx_lossless_decompress_host = _sig("hccx_lossless_decompress_host", _st, _p, _u64, _u64, _p, C.c_int)
+hccx_lossless_ring_wire = _sig("hccx_lossless_ring_wire", _st, _pp, C.c_int, _u64, C.c_int, C.POINTER(_u64), _p)
+hccx_lossless_ring_wire_host = _sig("hccx_lossless_ring_wire_host", _st, _pp, C.c_int, _u64, C.c_int,
+                                    C.POINTER(_u64), C.c_int)
 hccx_group_create = _sig("hccx_group_create", _st, C.c_int, C.c_int, C.POINTER(_p))
 hccx_group_destroy = _sig("hccx_group_destroy", _st, _p)
 hccx_group_allreduce = _sig("hccx_group_allreduce", _st, _p, _pp, _pp, _u64, Codec, C.c_int, _p)

@@ -32,7 +32,7 @@ import numpy as np
 
 from .codec import CodecKind, CodecSpec, wire_size_bytes
 from .comm_path import CommPath
-from .errors import BadChunkingError, UnsupportedError, check
+from .errors import BadChunkingError, check
 from .netsim import CollectiveKind, SimClock, TraceEvent
 
 
@@ -95,9 +95,29 @@ def _back(ts: list, host: bool) -> list:
 
 
 def _message_bytes(spec: CodecSpec, n: int) -> int:
-    if spec.kind == CodecKind.LosslessPredictor:
-        raise UnsupportedError("lossless accounting needs the device predictor size pass (not built yet)")
+    """Payload bytes of one n-value message (size law; lossless -> use the
+    data-dependent helpers below)."""
     return wire_size_bytes(spec, n)
+
+
+def _lossless(spec: CodecSpec) -> bool:
+    return spec.kind == CodecKind.LosslessPredictor
+
+
+def _lossless_ring_wire(ts: list, n: int, collective: int, stream) -> int:
+    """Wire bytes under LosslessPredictor, whose message sizes are
+    data-dependent: hccx_lossless_ring_wire sizes every hop's message on the
+    device (collective 0 = reduce-scatter partial folds, collectives.cpp:34-61;
+    1 = allgather shards, :94-106; 2 = allreduce, both)."""
+    import ctypes as C
+
+    from . import _lib
+
+    arr, _keep = _ptrs(ts)
+    out = C.c_uint64(0)
+    check(_lib.hccx_lossless_ring_wire(arr, len(ts), n, collective, C.byref(out), stream.cuda_stream),
+          "lossless wire accounting")
+    return int(out.value)
 
 
 class _Timer:
@@ -158,9 +178,12 @@ def ring_reduce_scatter(clock: SimClock, comm: Communicator, inputs: Sequence, s
     if p == 1:
         return [inputs[0].clone() if _is_cuda(inputs[0]) else np.array(inputs[0], np.float32)]
     c = n // p
-    msg = _message_bytes(spec, c)
     torch = _torch()
     ts, host, dev = _as_device(inputs)
+    if _lossless(spec):
+        wire = _lossless_ring_wire(ts, n, 0, torch.cuda.current_stream(dev))
+    else:
+        wire = (p - 1) * p * _message_bytes(spec, c)
     shards = [torch.empty(c, dtype=torch.float32, device=ts[0].device) for _ in range(p)]
     g = _group(p, dev)
     tin, _k1 = _ptrs(ts)
@@ -169,8 +192,7 @@ def ring_reduce_scatter(clock: SimClock, comm: Communicator, inputs: Sequence, s
         check(_lib.hccx_group_reduce_scatter(g, tin, tout, n, spec.c(), tm.stream.cuda_stream), "reduce_scatter")
     _finish(g, tm.stream, "reduce_scatter")
     rounds = p - 1
-    _commit(clock, comm, tm.seconds(), rounds * p * 4 * c, rounds * p * msg, rounds, path,
-            CollectiveKind.ReduceScatter)
+    _commit(clock, comm, tm.seconds(), rounds * p * 4 * c, wire, rounds, path, CollectiveKind.ReduceScatter)
     return _back(shards, host)
 
 
@@ -186,9 +208,12 @@ def ring_allgather(clock: SimClock, comm: Communicator, shards: Sequence, spec: 
         raise BadChunkingError("allgather: mismatched shard lengths")
     if p == 1:
         return [shards[0].clone() if _is_cuda(shards[0]) else np.array(shards[0], np.float32)]
-    msg = _message_bytes(spec, c)
     torch = _torch()
     ts, host, dev = _as_device(shards)
+    if _lossless(spec):
+        wire = _lossless_ring_wire(ts, c, 1, torch.cuda.current_stream(dev))
+    else:
+        wire = (p - 1) * p * _message_bytes(spec, c)
     outs = [torch.empty(p * c, dtype=torch.float32, device=ts[0].device) for _ in range(p)]
     g = _group(p, dev)
     tin, _k1 = _ptrs(ts)
@@ -197,8 +222,7 @@ def ring_allgather(clock: SimClock, comm: Communicator, shards: Sequence, spec: 
         check(_lib.hccx_group_allgather(g, tin, tout, c, spec.c(), tm.stream.cuda_stream), "allgather")
     _finish(g, tm.stream, "allgather")
     rounds = p - 1
-    _commit(clock, comm, tm.seconds(), rounds * p * 4 * c, rounds * p * msg, rounds, path,
-            CollectiveKind.AllGather)
+    _commit(clock, comm, tm.seconds(), rounds * p * 4 * c, wire, rounds, path, CollectiveKind.AllGather)
     return _back(outs, host)
 
 
@@ -217,9 +241,12 @@ def allreduce(clock: SimClock, comm: Communicator, inputs: Sequence, spec: Codec
     if p == 1:
         return [inputs[0].clone() if _is_cuda(inputs[0]) else np.array(inputs[0], np.float32)]
     c = n // p
-    msg = _message_bytes(spec, c)
     torch = _torch()
     ts, host, dev = _as_device(inputs)
+    if _lossless(spec):
+        wire = _lossless_ring_wire(ts, n, 2, torch.cuda.current_stream(dev))
+    else:
+        wire = 2 * (p - 1) * p * _message_bytes(spec, c)
     outs = [torch.empty(n, dtype=torch.float32, device=ts[0].device) for _ in range(p)]
     g = _group(p, dev)
     tin, _k1 = _ptrs(ts)
@@ -229,8 +256,7 @@ def allreduce(clock: SimClock, comm: Communicator, inputs: Sequence, spec: Codec
               "allreduce")
     _finish(g, tm.stream, "allreduce")
     rounds = p - 1
-    _commit(clock, comm, tm.seconds(), 2 * rounds * p * 4 * c, 2 * rounds * p * msg, 2 * rounds, path,
-            CollectiveKind.AllReduce)
+    _commit(clock, comm, tm.seconds(), 2 * rounds * p * 4 * c, wire, 2 * rounds, path, CollectiveKind.AllReduce)
     return _back(outs, host)
 
 
@@ -240,9 +266,14 @@ def p2p(clock: SimClock, src: int, dst: int, buf, spec: CodecSpec, path: CommPat
 
     assert src != dst
     n = len(buf)
-    msg = _message_bytes(spec, n)
     torch = _torch()
     (t,), host, dev = _as_device([buf])
+    if _lossless(spec):
+        from . import lossless
+
+        msg = lossless.size(t)
+    else:
+        msg = _message_bytes(spec, n)
     out = torch.empty(n, dtype=torch.float32, device=t.device)
     g = _group(2, dev)
     with _Timer(dev) as tm:
@@ -265,9 +296,14 @@ def broadcast(clock: SimClock, comm: Communicator, root: int, buf, spec: CodecSp
     n = len(buf)
     if p == 1:
         return [buf.clone() if _is_cuda(buf) else np.array(buf, np.float32)]
-    msg = _message_bytes(spec, n)
     torch = _torch()
     (t,), host, dev = _as_device([buf])
+    if _lossless(spec):
+        from . import lossless
+
+        msg = lossless.size(t)
+    else:
+        msg = _message_bytes(spec, n)
     outs = [torch.empty(n, dtype=torch.float32, device=t.device) for _ in range(p)]
     g = _group(p, dev)
     tout, _k = _ptrs(outs)

@@ -1,0 +1,509 @@
+// lossless.cu -- the reference's LosslessPredictor codec on the GPU
+// (format of /root/reference/proj/src/codec_kernels.hpp:165-239
+// and src/codec_serial.cpp:48-66, :85-107).
+//
+// Payload = [ceil(nchunks/8) fallback-flag bytes][chunk 0][chunk 1]...; a
+// 4096-value chunk is either its raw bytes (flag set, when the coded size
+// reaches 4*live) or, per value, the XOR residual against the previous
+// value (0 before the chunk) as a 5-bit leading-zero count capped at 31
+// followed by the 32-lzc low residual bits, LSB-first, flushed to a byte.
+//
+// compress: (1) size pass, one warp per chunk -> chunk bytes + flag;
+//           (2) exclusive scan of chunk bytes -> offsets (one CTA);
+//           (3) emit, one warp per chunk: lanes own 128 consecutive values,
+//               write their codes into a shared-memory copy of the chunk
+//               stream (word-exclusive stores + atomicOr on the 2 shared
+//               boundary words), the warp copies it to its byte offset.
+// decompress: the format stores no offsets, so a single-warp walk parses
+//           each coded chunk's 5-bit fields to find where the next chunk
+//           starts (fallback chunks cost O(1)); then one warp per chunk
+//           decodes in parallel from the recovered offsets.
+#include <cstdint>
+#include <cstring>
+
+#include "device_common.cuh"
+#include "hccx.h"
+#include "hccx_internal.h"
+#include "hccx_kernels.h"
+
+namespace hccx {
+namespace {
+
+constexpr int kChunk = 4096;
+constexpr int kLaneVals = kChunk / 32;  // 128
+constexpr int kLLWarps = 4;             // warps per CTA (16 KiB smem stream each)
+constexpr int kStreamWords = kChunk;    // >= 4096 codes * 37 bits / 32
+
+__device__ __forceinline__ uint32_t code_bits(uint32_t r) {
+  const uint32_t z = min(__clz(r), 31);
+  return 5u + 32u - z;
+}
+
+// (1) per-chunk coded bytes / fallback flag
+__global__ void __launch_bounds__(kLLWarps * 32) ll_size_kernel(const float* __restrict__ in, uint64_t n,
+                                                                uint64_t nchunks, uint32_t* __restrict__ sizes,
+                                                                uint8_t* __restrict__ fallback) {
+  const int lane = threadIdx.x & 31;
+  for (uint64_t c = (static_cast<uint64_t>(blockIdx.x) * kLLWarps + (threadIdx.x >> 5)); c < nchunks;
+       c += static_cast<uint64_t>(gridDim.x) * kLLWarps) {
+    const uint64_t base = c * kChunk;
+    const uint32_t live = static_cast<uint32_t>(n - base < kChunk ? n - base : kChunk);
+    const uint32_t* x = reinterpret_cast<const uint32_t*>(in) + base;
+    uint64_t bits = 0;
+    for (uint32_t i = lane; i < live; i += 32) {
+      const uint32_t prev = i ? x[i - 1] : 0u;
+      bits += code_bits(x[i] ^ prev);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) bits += __shfl_xor_sync(kFull, bits, o);
+    if (lane == 0) {
+      const uint64_t enc = (bits + 7) / 8;
+      const uint64_t raw = 4ull * live;
+      sizes[c] = static_cast<uint32_t>(enc < raw ? enc : raw);
+      fallback[c] = enc >= raw ? 1 : 0;
+    }
+  }
+}
+
+// (2) exclusive scan of sizes (+ flag bytes), single CTA; offsets[nchunks] = total
+__global__ void __launch_bounds__(1024) ll_scan_kernel(const uint32_t* __restrict__ sizes, uint64_t nchunks,
+                                                       uint64_t flag_bytes, uint64_t* __restrict__ offsets) {
+  __shared__ uint64_t part[1024];
+  const uint64_t per = (nchunks + blockDim.x - 1) / blockDim.x;
+  const uint64_t lo = threadIdx.x * per, hi = min(nchunks, lo + per);
+  uint64_t s = 0;
+  for (uint64_t i = lo; i < hi; ++i) s += sizes[i];
+  part[threadIdx.x] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint64_t acc = flag_bytes;
+    for (unsigned t = 0; t < blockDim.x; ++t) {
+      const uint64_t v = part[t];
+      part[t] = acc;
+      acc += v;
+    }
+    offsets[nchunks] = acc;
+  }
+  __syncthreads();
+  uint64_t acc = part[threadIdx.x];
+  for (uint64_t i = lo; i < hi; ++i) {
+    offsets[i] = acc;
+    acc += sizes[i];
+  }
+}
+
+// flag bytes: bit c%8 of byte c/8 (codec_serial.cpp:63)
+__global__ void ll_flags_kernel(const uint8_t* __restrict__ fallback, uint64_t nchunks, uint8_t* __restrict__ out) {
+  const uint64_t nb = (nchunks + 7) / 8;
+  for (uint64_t b = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; b < nb;
+       b += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    uint8_t v = 0;
+    for (int k = 0; k < 8; ++k) {
+      const uint64_t c = b * 8 + k;
+      if (c < nchunks && fallback[c]) v |= static_cast<uint8_t>(1u << k);
+    }
+    out[b] = v;
+  }
+}
+
+// Byte copy of `len` bytes from a word-aligned shared stream to an arbitrary
+// global byte offset: interior words stored whole (funnel-shifted), the
+// edges bytewise.
+__device__ void copy_stream_out(const uint32_t* sm, uint8_t* dst, uint32_t len, int lane) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(dst);
+  const uint32_t head = static_cast<uint32_t>((4 - (a & 3)) & 3) < len ? static_cast<uint32_t>((4 - (a & 3)) & 3) : len;
+  const uint8_t* sb = reinterpret_cast<const uint8_t*>(sm);
+  for (uint32_t b = lane; b < head; b += 32) dst[b] = sb[b];
+  const uint32_t nw = (len - head) / 4;
+  uint32_t* dw = reinterpret_cast<uint32_t*>(dst + head);
+  for (uint32_t w = lane; w < nw; w += 32) {
+    const uint32_t byte = head + 4 * w;  // source byte offset
+    const uint32_t lo = sm[byte >> 2], hi = (byte & 3) ? sm[(byte >> 2) + 1] : 0u;
+    dw[w] = __funnelshift_r(lo, hi, 8 * (byte & 3));
+  }
+  for (uint32_t b = head + 4 * nw + lane; b < len; b += 32) dst[b] = sb[b];
+}
+
+// (3) emit
+__global__ void __launch_bounds__(kLLWarps * 32) ll_emit_kernel(const float* __restrict__ in, uint64_t n,
+                                                                uint64_t nchunks, const uint64_t* __restrict__ offsets,
+                                                                const uint8_t* __restrict__ fallback,
+                                                                uint8_t* __restrict__ out) {
+  extern __shared__ uint32_t llsm[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t* sm = llsm + warp * (kStreamWords + 2);
+  for (uint64_t c = static_cast<uint64_t>(blockIdx.x) * kLLWarps + warp; c < nchunks;
+       c += static_cast<uint64_t>(gridDim.x) * kLLWarps) {
+    const uint64_t base = c * kChunk;
+    const uint32_t live = static_cast<uint32_t>(n - base < kChunk ? n - base : kChunk);
+    const uint32_t* x = reinterpret_cast<const uint32_t*>(in) + base;
+    uint8_t* dst = out + offsets[c];
+    if (fallback[c]) {  // raw chunk (codec_kernels.hpp:190-194)
+      copy_stream_out(x, dst, 4 * live, lane);
+      continue;
+    }
+    // lane's bit count and exclusive offset
+    const uint32_t i0 = lane * kLaneVals, i1 = min(live, i0 + kLaneVals);
+    uint32_t mybits = 0;
+    for (uint32_t i = i0; i < i1; ++i) mybits += code_bits(x[i] ^ (i ? x[i - 1] : 0u));
+    uint32_t incl = mybits;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(kFull, incl, o);
+      if (lane >= o) incl += t;
+    }
+    const uint32_t total = __shfl_sync(kFull, incl, 31);
+    const uint32_t words = (total + 31) / 32;
+    for (uint32_t w = lane; w < words + 1; w += 32) sm[w] = 0;
+    __syncwarp();
+    uint32_t pos = incl - mybits;  // bit offset of this lane's first code
+    uint64_t acc = 0;
+    uint32_t fill = pos & 31, wi = pos >> 5;
+    const uint32_t first_word = wi;
+    bool first = true;
+    auto put = [&](uint32_t v, uint32_t nb) {  // append nb (<= 32) bits
+      acc |= static_cast<uint64_t>(v) << fill;
+      fill += nb;
+      if (fill >= 32) {
+        const uint32_t wv = static_cast<uint32_t>(acc);
+        if (first && wi == first_word) atomicOr(&sm[wi], wv);  // shared with the previous lane
+        else sm[wi] = wv;
+        first = false;
+        ++wi;
+        acc >>= 32;
+        fill -= 32;
+      }
+    };
+    for (uint32_t i = i0; i < i1; ++i) {
+      const uint32_t r = x[i] ^ (i ? x[i - 1] : 0u);
+      const uint32_t z = min(__clz(r), 31);
+      put(z, 5);
+      const uint32_t nb = 32 - z;
+      put(nb == 32 ? r : (r & ((1u << nb) - 1u)), nb);
+    }
+    if (fill > 0) atomicOr(&sm[wi], static_cast<uint32_t>(acc));  // may be shared with the next lane
+    __syncwarp();
+    copy_stream_out(sm, dst, (total + 7) / 8, lane);
+    __syncwarp();
+  }
+}
+
+// decompress (a): offsets by walking coded chunks' 5-bit fields
+__global__ void ll_walk_kernel(const uint8_t* __restrict__ in, uint64_t in_bytes, uint64_t n, uint64_t nchunks,
+                               uint64_t* __restrict__ offsets, uint32_t* __restrict__ err) {
+  if (threadIdx.x != 0) return;
+  uint64_t pos = (nchunks + 7) / 8;
+  for (uint64_t c = 0; c < nchunks; ++c) {
+    offsets[c] = pos;
+    const uint32_t live = static_cast<uint32_t>(n - c * kChunk < kChunk ? n - c * kChunk : kChunk);
+    if ((in[c / 8] >> (c % 8)) & 1u) {
+      pos += 4ull * live;
+    } else {
+      uint64_t bit = pos * 8;
+      const uint64_t end_bit = 8 * in_bytes;
+      for (uint32_t i = 0; i < live && bit <= end_bit; ++i) {
+        if (bit + 5 > end_bit) {
+          bit = end_bit + 1;  // truncated inside a length field
+          break;
+        }
+        const uint64_t B = bit >> 3;
+        uint32_t w = in[B];
+        if (B + 1 < in_bytes) w |= static_cast<uint32_t>(in[B + 1]) << 8;
+        const uint32_t z = (w >> (bit & 7)) & 31u;
+        bit += 5 + (32 - z);
+      }
+      pos = bit > end_bit ? in_bytes + 1 : (bit + 7) / 8;
+    }
+    if (pos > in_bytes) {
+      atomicOr(err, 8u);  // truncated stream
+      pos = in_bytes;
+    }
+  }
+  offsets[nchunks] = pos;
+}
+
+// decompress (b): one warp per chunk from its offset (lane 0 decodes the
+// chain of codes; the warp stores the values)
+__global__ void __launch_bounds__(kLLWarps * 32) ll_decode_kernel(const uint8_t* __restrict__ in, uint64_t in_bytes,
+                                                                  uint64_t n, uint64_t nchunks,
+                                                                  const uint64_t* __restrict__ offsets,
+                                                                  float* __restrict__ out) {
+  extern __shared__ uint32_t llsm[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t* vals = llsm + warp * kChunk;
+  for (uint64_t c = static_cast<uint64_t>(blockIdx.x) * kLLWarps + warp; c < nchunks;
+       c += static_cast<uint64_t>(gridDim.x) * kLLWarps) {
+    const uint64_t base = c * kChunk;
+    const uint32_t live = static_cast<uint32_t>(n - base < kChunk ? n - base : kChunk);
+    const uint8_t* src = in + offsets[c];
+    uint32_t* o = reinterpret_cast<uint32_t*>(out) + base;
+    if ((in[c / 8] >> (c % 8)) & 1u) {
+      const uint64_t avail = in_bytes - offsets[c];
+      for (uint32_t i = lane; i < live && 4ull * i + 4 <= avail; i += 32) {
+        uint32_t v = 0;
+        memcpy(&v, src + 4 * i, 4);
+        o[i] = v;
+      }
+      continue;
+    }
+    const uint64_t avail = in_bytes - offsets[c];
+    if (lane == 0) {
+      uint64_t bit = 0;
+      uint32_t prev = 0;
+      auto get = [&](uint32_t nb) -> uint32_t {
+        if (nb == 0) return 0u;
+        const uint64_t B = bit >> 3;
+        uint64_t w = 0;
+        for (int k = 0; k < 6; ++k)
+          if (B + k < avail) w |= static_cast<uint64_t>(src[B + k]) << (8 * k);
+        const uint32_t v = static_cast<uint32_t>(w >> (bit & 7)) & (nb >= 32 ? 0xffffffffu : ((1u << nb) - 1u));
+        bit += nb;
+        return v;
+      };
+      for (uint32_t i = 0; i < live; ++i) {
+        const uint32_t z = get(5);
+        const uint32_t low = get(32 - z);
+        prev ^= low;
+        vals[i] = prev;
+      }
+    }
+    __syncwarp();
+    for (uint32_t i = lane; i < live; i += 32) o[i] = vals[i];
+    __syncwarp();
+  }
+}
+
+// part = part + x (the ring's "arriving partial on the left" fold,
+// collectives.cpp:50-52); plain IEEE fp32 adds.
+__global__ void ll_fold_kernel(float* __restrict__ part, const float* __restrict__ x, uint64_t n) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    part[i] = __fadd_rn(part[i], x[i]);
+}
+
+int grid_for(uint64_t work, int per_block) {
+  uint64_t g = (work + per_block - 1) / per_block;
+  return static_cast<int>(g < 148 * 16 ? (g ? g : 1) : 148 * 16);
+}
+
+struct Scratch {
+  uint32_t* sizes = nullptr;
+  uint8_t* fallback = nullptr;
+  uint64_t* offsets = nullptr;
+  uint32_t* err = nullptr;
+  uint64_t cap = 0;
+  ~Scratch() {
+    cudaFree(sizes);
+    cudaFree(fallback);
+    cudaFree(offsets);
+    cudaFree(err);
+  }
+  hccx_status_t ensure(uint64_t nchunks) {
+    if (nchunks + 1 <= cap && err) return HCCX_OK;
+    cudaFree(sizes);
+    cudaFree(fallback);
+    cudaFree(offsets);
+    if (!err && cudaMalloc(&err, 4) != cudaSuccess) return HCCX_ERR_CUDA;
+    const uint64_t c = nchunks + 1;
+    if (cudaMalloc(&sizes, 4 * c) != cudaSuccess || cudaMalloc(&fallback, c) != cudaSuccess ||
+        cudaMalloc(&offsets, 8 * c) != cudaSuccess)
+      return HCCX_ERR_CUDA;
+    cap = c;
+    return HCCX_OK;
+  }
+};
+
+hccx_status_t size_pass(const float* d_in, uint64_t n, Scratch& s, cudaStream_t st, uint64_t* total) {
+  const uint64_t nch = (n + kChunk - 1) / kChunk;
+  hccx_status_t r = s.ensure(nch);
+  if (r != HCCX_OK) return r;
+  ll_size_kernel<<<grid_for(nch, kLLWarps), kLLWarps * 32, 0, st>>>(d_in, n, nch, s.sizes, s.fallback);
+  ll_scan_kernel<<<1, 1024, 0, st>>>(s.sizes, nch, (nch + 7) / 8, s.offsets);
+  count_launch(2);
+  if (cudaGetLastError() != cudaSuccess) return HCCX_ERR_CUDA;
+  if (total) {
+    if (cudaMemcpyAsync(total, s.offsets + nch, 8, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess)
+      return HCCX_ERR_CUDA;
+  }
+  return HCCX_OK;
+}
+
+thread_local Scratch t_scratch;
+
+}  // namespace
+}  // namespace hccx
+
+using namespace hccx;
+
+extern "C" hccx_status_t hccx_lossless_size(const float* d_in, uint64_t n, uint64_t* bytes, void* stream) {
+  if (!bytes || (n && !d_in)) return HCCX_ERR_INVALID_ARGUMENT;
+  if (n == 0) {
+    *bytes = 0;
+    return HCCX_OK;
+  }
+  return size_pass(d_in, n, t_scratch, static_cast<cudaStream_t>(stream), bytes);
+}
+
+extern "C" hccx_status_t hccx_lossless_compress(const float* d_in, uint64_t n, uint8_t* d_out, uint64_t capacity,
+                                                uint64_t* bytes, void* stream) {
+  if (!bytes || (n && (!d_in || !d_out))) return HCCX_ERR_INVALID_ARGUMENT;
+  if (n == 0) {
+    *bytes = 0;
+    return HCCX_OK;
+  }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  hccx_status_t r = size_pass(d_in, n, t_scratch, st, bytes);
+  if (r != HCCX_OK) return r;
+  if (*bytes > capacity) return HCCX_ERR_INVALID_ARGUMENT;
+  const uint64_t nch = (n + kChunk - 1) / kChunk;
+  const size_t smem = sizeof(uint32_t) * kLLWarps * (kStreamWords + 2);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(ll_emit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    cudaFuncSetAttribute(ll_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(sizeof(uint32_t) * kLLWarps * kChunk));
+    attr = true;
+  }
+  ll_flags_kernel<<<grid_for((nch + 7) / 8, 256), 256, 0, st>>>(t_scratch.fallback, nch, d_out);
+  ll_emit_kernel<<<grid_for(nch, kLLWarps), kLLWarps * 32, smem, st>>>(d_in, n, nch, t_scratch.offsets,
+                                                                      t_scratch.fallback, d_out);
+  count_launch(2);
+  return cuda_status(cudaGetLastError());
+}
+
+extern "C" hccx_status_t hccx_lossless_decompress(const uint8_t* d_in, uint64_t in_bytes, uint64_t n, float* d_out,
+                                                  void* stream) {
+  if (n && (!d_in || !d_out)) return HCCX_ERR_INVALID_ARGUMENT;
+  if (n == 0) return HCCX_OK;
+  const uint64_t nch = (n + kChunk - 1) / kChunk;
+  if (in_bytes < (nch + 7) / 8) return HCCX_ERR_CORRUPT_PAYLOAD;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  hccx_status_t r = t_scratch.ensure(nch);
+  if (r != HCCX_OK) return r;
+  static bool attr = false;
+  const size_t smem = sizeof(uint32_t) * kLLWarps * kChunk;
+  if (!attr) {
+    cudaFuncSetAttribute(ll_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    attr = true;
+  }
+  cudaMemsetAsync(t_scratch.err, 0, 4, st);
+  ll_walk_kernel<<<1, 32, 0, st>>>(d_in, in_bytes, n, nch, t_scratch.offsets, t_scratch.err);
+  ll_decode_kernel<<<grid_for(nch, kLLWarps), kLLWarps * 32, smem, st>>>(d_in, in_bytes, n, nch, t_scratch.offsets,
+                                                                         d_out);
+  count_launch(2);
+  if (cudaGetLastError() != cudaSuccess) return HCCX_ERR_CUDA;
+  uint32_t e = 0;
+  uint64_t end = 0;
+  if (cudaMemcpyAsync(&e, t_scratch.err, 4, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      cudaMemcpyAsync(&end, t_scratch.offsets + nch, 8, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      cudaStreamSynchronize(st) != cudaSuccess)
+    return HCCX_ERR_CUDA;
+  (void)end;  // trailing bytes are ignored, as in codec_serial.cpp:85-107
+  if (e) return HCCX_ERR_CORRUPT_PAYLOAD;
+  return HCCX_OK;
+}
+
+extern "C" uint64_t hccx_lossless_max_bytes(uint64_t n) {
+  const uint64_t nch = (n + kChunk - 1) / kChunk;
+  return (nch + 7) / 8 + 4 * n;
+}
+
+extern "C" hccx_status_t hccx_lossless_compress_host(const float* h_in, uint64_t n, uint8_t* h_out,
+                                                     uint64_t capacity, uint64_t* bytes, int device) {
+  if (!bytes || (n && (!h_in || !h_out))) return HCCX_ERR_INVALID_ARGUMENT;
+  if (n == 0) {
+    *bytes = 0;
+    return HCCX_OK;
+  }
+  DeviceGuard g(device);
+  float* d_in = nullptr;
+  uint8_t* d_out = nullptr;
+  const uint64_t cap = hccx_lossless_max_bytes(n);
+  hccx_status_t r = HCCX_OK;
+  if (cudaMalloc(&d_in, 4 * n) != cudaSuccess || cudaMalloc(&d_out, cap) != cudaSuccess) r = HCCX_ERR_CUDA;
+  if (r == HCCX_OK && cudaMemcpy(d_in, h_in, 4 * n, cudaMemcpyHostToDevice) != cudaSuccess) r = HCCX_ERR_CUDA;
+  if (r == HCCX_OK) r = hccx_lossless_compress(d_in, n, d_out, cap, bytes, nullptr);
+  if (r == HCCX_OK && *bytes > capacity) r = HCCX_ERR_INVALID_ARGUMENT;
+  if (r == HCCX_OK && cudaMemcpy(h_out, d_out, *bytes, cudaMemcpyDeviceToHost) != cudaSuccess) r = HCCX_ERR_CUDA;
+  cudaFree(d_in);
+  cudaFree(d_out);
+  return r;
+}
+
+extern "C" hccx_status_t hccx_lossless_decompress_host(const uint8_t* h_in, uint64_t bytes, uint64_t n, float* h_out,
+                                                       int device) {
+  if (n && (!h_in || !h_out)) return HCCX_ERR_INVALID_ARGUMENT;
+  if (n == 0) return HCCX_OK;
+  DeviceGuard g(device);
+  uint8_t* d_in = nullptr;
+  float* d_out = nullptr;
+  hccx_status_t r = HCCX_OK;
+  if (cudaMalloc(&d_in, bytes ? bytes : 1) != cudaSuccess || cudaMalloc(&d_out, 4 * n) != cudaSuccess)
+    r = HCCX_ERR_CUDA;
+  if (r == HCCX_OK && bytes && cudaMemcpy(d_in, h_in, bytes, cudaMemcpyHostToDevice) != cudaSuccess)
+    r = HCCX_ERR_CUDA;
+  if (r == HCCX_OK) r = hccx_lossless_decompress(d_in, bytes, n, d_out, nullptr);
+  if (r == HCCX_OK && cudaMemcpy(h_out, d_out, 4 * n, cudaMemcpyDeviceToHost) != cudaSuccess) r = HCCX_ERR_CUDA;
+  cudaFree(d_in);
+  cudaFree(d_out);
+  return r;
+}
+
+// Ring wire bytes under LosslessPredictor (see hccx.h).
+extern "C" hccx_status_t hccx_lossless_ring_wire(const float* const* d_in, int p, uint64_t n, int collective,
+                                                 uint64_t* wire, void* stream) {
+  if (!wire || !d_in || p < 1 || p > 16 || collective < 0 || collective > 2) return HCCX_ERR_INVALID_ARGUMENT;
+  *wire = 0;
+  if (p == 1 || n == 0) return HCCX_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  uint64_t sz = 0;
+  hccx_status_t r = HCCX_OK;
+  if (collective == 1) {  // allgather: shard j's payload crosses p-1 hops (collectives.cpp:94-106)
+    for (int j = 0; j < p && r == HCCX_OK; ++j) {
+      r = hccx_lossless_size(d_in[j], n, &sz, stream);
+      *wire += static_cast<uint64_t>(p - 1) * sz;
+    }
+    return r;
+  }
+  if (n % p) return HCCX_ERR_BAD_CHUNKING;
+  const uint64_t c = n / p;
+  float* part = nullptr;
+  if (cudaMalloc(&part, 4 * c) != cudaSuccess) return HCCX_ERR_CUDA;
+  for (int k = 0; k < p && r == HCCX_OK; ++k) {
+    // chunk k: round-0 message is member k+1's chunk; each hop folds the next member in
+    if (cudaMemcpyAsync(part, d_in[(k + 1) % p] + k * c, 4 * c, cudaMemcpyDeviceToDevice, st) != cudaSuccess) {
+      r = HCCX_ERR_CUDA;
+      break;
+    }
+    for (int t = 0; t < p - 1 && r == HCCX_OK; ++t) {
+      r = hccx_lossless_size(part, c, &sz, stream);
+      *wire += sz;
+      ll_fold_kernel<<<grid_for(c, 256 * 4), 256, 0, st>>>(part, d_in[(k + 2 + t) % p] + k * c, c);
+      count_launch();
+    }
+    if (r == HCCX_OK && collective == 2) {  // allreduce: the folded shard crosses p-1 allgather hops
+      r = hccx_lossless_size(part, c, &sz, stream);
+      *wire += static_cast<uint64_t>(p - 1) * sz;
+    }
+  }
+  cudaStreamSynchronize(st);
+  cudaFree(part);
+  return r;
+}
+
+extern "C" hccx_status_t hccx_lossless_ring_wire_host(const float* const* h_in, int p, uint64_t n, int collective,
+                                                      uint64_t* wire, int device) {
+  if (!wire || !h_in || p < 1 || p > 16) return HCCX_ERR_INVALID_ARGUMENT;
+  DeviceGuard g(device);
+  float* d[16] = {};
+  hccx_status_t r = HCCX_OK;
+  for (int j = 0; j < p && r == HCCX_OK; ++j) {
+    if (cudaMalloc(&d[j], 4 * (n ? n : 1)) != cudaSuccess ||
+        (n && cudaMemcpy(d[j], h_in[j], 4 * n, cudaMemcpyHostToDevice) != cudaSuccess))
+      r = HCCX_ERR_CUDA;
+  }
+  if (r == HCCX_OK) r = hccx_lossless_ring_wire(d, p, n, collective, wire, nullptr);
+  for (int j = 0; j < p; ++j) cudaFree(d[j]);
+  return r;
+}

@@ -43,9 +43,25 @@ void check(hccx_status_t st, const std::string& what) {
 
 hccx_codec_t c_of(const CodecSpec& s) { return hccx_codec_t{static_cast<int32_t>(s.kind), s.rate_bits}; }
 
-void require_device_codec(const CodecSpec& s, const char* what) {
-  if (s.kind == CodecKind::LosslessPredictor)
-    throw Error(std::string(what) + ": the LosslessPredictor codec has no device implementation yet");
+bool lossless(const CodecSpec& s) { return s.kind == CodecKind::LosslessPredictor; }
+
+// Wire bytes of a ring collective: the size law, or under LosslessPredictor
+// the device-sized hop messages (hccx_lossless_ring_wire).
+std::uint64_t ring_wire(const CodecSpec& spec, const std::vector<const float*>& in, std::uint64_t n, int collective,
+                        std::uint64_t law_msgs, std::uint64_t law_n) {
+  if (!lossless(spec)) return law_msgs * wire_size_bytes(spec, law_n);
+  std::uint64_t w = 0;
+  check(hccx_lossless_ring_wire_host(in.data(), static_cast<int>(in.size()), n, collective, &w, g_device),
+        "lossless wire accounting");
+  return w;
+}
+
+std::uint64_t message_wire(const CodecSpec& spec, const FloatBuffer& buf) {
+  if (!lossless(spec)) return wire_size_bytes(spec, buf.size());
+  const float* two[2] = {buf.data(), buf.data()};
+  std::uint64_t w = 0;  // allgather over 2 members = one hop of this buffer
+  check(hccx_lossless_ring_wire_host(two, 2, buf.size(), 1, &w, g_device), "lossless wire accounting");
+  return w / 2;
 }
 
 // one device group per communicator size, created on first use
@@ -141,7 +157,6 @@ std::uint64_t wire_size_bytes(const CodecSpec& spec, std::uint64_t n) {
 }
 
 CompressedBuffer compress(const CodecSpec& spec, const FloatBuffer& buf) {
-  require_device_codec(spec, "compress");
   check(hccx_codec_validate(c_of(spec)), "compress");
   CompressedBuffer out;
   out.codec = spec;
@@ -149,6 +164,16 @@ CompressedBuffer compress(const CodecSpec& spec, const FloatBuffer& buf) {
   std::uint64_t cc = 0;
   check(hccx_chunk_count(c_of(spec), buf.size(), &cc), "compress");
   out.chunk_count = static_cast<std::uint32_t>(cc);
+  if (lossless(spec)) {  // data-dependent size (codec_serial.cpp:42-55)
+    out.payload.resize(hccx_lossless_max_bytes(buf.size()));
+    std::uint64_t nb = 0;
+    if (!buf.empty())
+      check(hccx_lossless_compress_host(buf.data(), buf.size(), out.payload.data(), out.payload.size(), &nb,
+                                        g_device),
+            "compress");
+    out.payload.resize(nb);
+    return out;
+  }
   out.payload.resize(wire_size_bytes(spec, buf.size()));
   if (!buf.empty())
     check(hccx_compress_host(c_of(spec), buf.data(), buf.size(), out.payload.data(), g_device), "compress");
@@ -156,9 +181,17 @@ CompressedBuffer compress(const CodecSpec& spec, const FloatBuffer& buf) {
 }
 
 FloatBuffer decompress(const CompressedBuffer& cbuf) {
-  require_device_codec(cbuf.codec, "decompress");
   std::uint64_t cc = 0;
   check(hccx_chunk_count(c_of(cbuf.codec), cbuf.original_len, &cc), "decompress");
+  if (lossless(cbuf.codec)) {  // codec_serial.cpp:85-107
+    if (cbuf.chunk_count != cc || cbuf.payload.size() < (cc + 7) / 8)
+      throw CorruptPayloadError("predictor payload header mismatch");
+    FloatBuffer out(cbuf.original_len);
+    if (!out.empty())
+      check(hccx_lossless_decompress_host(cbuf.payload.data(), cbuf.payload.size(), out.size(), out.data(), g_device),
+            "decompress");
+    return out;
+  }
   if (cbuf.codec.kind != CodecKind::Identity && cbuf.chunk_count != cc)
     throw CorruptPayloadError("payload does not match block count");
   if (cbuf.payload.size() != wire_size_bytes(cbuf.codec, cbuf.original_len))
@@ -277,10 +310,9 @@ void write_trace_csv(std::ostream& os, const std::vector<TraceEvent>& trace) {
 // ------------------------------------------------------------ collectives --
 
 FloatBuffer p2p(SimClock& clock, int src, int dst, const FloatBuffer& buf, const CodecSpec& spec, CommPath path) {
-  require_device_codec(spec, "p2p");
   if (src == dst) throw Error("p2p: src == dst");
   const std::uint64_t n = buf.size();
-  const std::uint64_t wire = wire_size_bytes(spec, n);
+  const std::uint64_t wire = message_wire(spec, buf);
   FloatBuffer out(n);
   double dur = 0.0;
   if (n) check(hccx_group_p2p_host(group_for(2), buf.data(), out.data(), n, c_of(spec), &dur), "p2p");
@@ -303,7 +335,6 @@ FloatBuffer p2p(SimClock& clock, int src, int dst, const FloatBuffer& buf, const
 std::vector<FloatBuffer> ring_reduce_scatter(SimClock& clock, const Communicator& comm,
                                              const std::vector<FloatBuffer>& inputs, const CodecSpec& spec,
                                              CommPath path) {
-  require_device_codec(spec, "reduce_scatter");
   const int p = comm.size();
   if (p < 1 || static_cast<int>(inputs.size()) != p) throw Error("reduce_scatter: one input per member");
   const std::size_t n = inputs[0].size();
@@ -319,15 +350,14 @@ std::vector<FloatBuffer> ring_reduce_scatter(SimClock& clock, const Communicator
   double dur = 0.0;
   check(hccx_group_reduce_scatter_host(group_for(p), in.data(), out.data(), n, c_of(spec), &dur), "reduce_scatter");
   const std::uint64_t rounds = p - 1;
-  commit(clock, comm, dur, rounds * p * 4 * c, rounds * p * wire_size_bytes(spec, c), p - 1, path,
-         CollectiveKind::ReduceScatter);
+  commit(clock, comm, dur, rounds * p * 4 * c, ring_wire(spec, in, n, 0, rounds * p, c), p - 1,
+         path, CollectiveKind::ReduceScatter);
   return shards;
 }
 
 std::vector<FloatBuffer> ring_allgather(SimClock& clock, const Communicator& comm,
                                         const std::vector<FloatBuffer>& shards, const CodecSpec& spec,
                                         CommPath path) {
-  require_device_codec(spec, "allgather");
   const int p = comm.size();
   if (p < 1 || static_cast<int>(shards.size()) != p) throw Error("allgather: one shard per member");
   const std::size_t c = shards[0].size();
@@ -340,14 +370,13 @@ std::vector<FloatBuffer> ring_allgather(SimClock& clock, const Communicator& com
   double dur = 0.0;
   check(hccx_group_allgather_host(group_for(p), in.data(), out.data(), c, c_of(spec), &dur), "allgather");
   const std::uint64_t rounds = p - 1;
-  commit(clock, comm, dur, rounds * p * 4 * c, rounds * p * wire_size_bytes(spec, c), p - 1, path,
-         CollectiveKind::AllGather);
+  commit(clock, comm, dur, rounds * p * 4 * c, ring_wire(spec, in, c, 1, rounds * p, c), p - 1,
+         path, CollectiveKind::AllGather);
   return outs;
 }
 
 std::vector<FloatBuffer> allreduce(SimClock& clock, const Communicator& comm, const std::vector<FloatBuffer>& inputs,
                                    const CodecSpec& spec, CommPath path, ReduceMode mode) {
-  require_device_codec(spec, "allreduce");
   const int p = comm.size();
   if (p < 1 || static_cast<int>(inputs.size()) != p) throw Error("allreduce: one input per member");
   const std::size_t n = inputs[0].size();
@@ -365,14 +394,13 @@ std::vector<FloatBuffer> allreduce(SimClock& clock, const Communicator& comm, co
                                   mode == ReduceMode::Average ? HCCX_AVERAGE : HCCX_SUM, &dur),
         "allreduce");
   const std::uint64_t rounds = p - 1;
-  commit(clock, comm, dur, 2 * rounds * p * 4 * c, 2 * rounds * p * wire_size_bytes(spec, c), 2 * (p - 1), path,
-         CollectiveKind::AllReduce);
+  commit(clock, comm, dur, 2 * rounds * p * 4 * c, ring_wire(spec, in, n, 2, 2 * rounds * p, c),
+         2 * (p - 1), path, CollectiveKind::AllReduce);
   return outs;
 }
 
 std::vector<FloatBuffer> broadcast(SimClock& clock, const Communicator& comm, int root, const FloatBuffer& buf,
                                    const CodecSpec& spec, CommPath path) {
-  require_device_codec(spec, "broadcast");
   const int p = comm.size();
   if (root < 0 || root >= p) throw Error("broadcast: root out of range");
   if (p == 1) return {buf};
@@ -382,7 +410,7 @@ std::vector<FloatBuffer> broadcast(SimClock& clock, const Communicator& comm, in
   double dur = 0.0;
   if (n) check(hccx_group_broadcast_host(group_for(p), root, buf.data(), out.data(), n, c_of(spec), &dur), "broadcast");
   const std::uint64_t rounds = p - 1;
-  commit(clock, comm, dur, rounds * 4 * n, rounds * wire_size_bytes(spec, n), p - 1, path, CollectiveKind::Broadcast);
+  commit(clock, comm, dur, rounds * 4 * n, rounds * message_wire(spec, buf), p - 1, path, CollectiveKind::Broadcast);
   return outs;
 }
 

@@ -27,7 +27,6 @@ from typing import Dict, List, Tuple
 
 from .codec import CodecKind, wire_size_bytes
 from .comm_path import CommPath
-from .errors import UnsupportedError
 from .netsim import CollectiveKind, TraceEvent
 from .parallel3d import ParallelLayout, SchemeTable
 
@@ -69,9 +68,6 @@ class HybridComm:
             from .errors import BadLayoutError
 
             raise BadLayoutError(f"layout world {layout.world()} != world size {dist.get_world_size()}")
-        for p in CommPath:
-            if scheme.at(p).kind == CodecKind.LosslessPredictor:
-                raise UnsupportedError("lossless predictor paths need the device predictor codec (not built yet)")
         self.groups: Dict[str, _Group] = {}
         for kind, groups in plan_groups(layout).items():
             for ranks in groups:
@@ -96,7 +92,47 @@ class HybridComm:
     def _record(self, path, kind, size, raw, wire, rounds, ev):
         a, b = ev
         b.synchronize()
+        if callable(wire):
+            wire = wire()
         self.trace.append(TraceEvent(self.step, path, kind, size, raw, wire, a.elapsed_time(b) / 1e3, rounds))
+
+    @staticmethod
+    def _lossless(spec) -> bool:
+        return spec.kind == CodecKind.LosslessPredictor
+
+    def _lossless_wire(self, g, x, what: str) -> int:
+        """Per-rank wire bytes (wire_total / p) under LosslessPredictor, whose
+        hop messages have data-dependent sizes (collectives.cpp:34-61,
+        :94-106).  The codec is value-transparent, so each hop's message is a
+        plain partial fold: member `me` gathers chunk `me` of every member
+        (one all-to-all), sizes the p-1 folds S_t = S_(t-1) + x[me+1+t][me]
+        that carry it round the ring (plus the folded shard's p-1 allgather
+        hops for an all-reduce) with the device size pass, and the totals are
+        summed over the group.  Accounting only: runs after the timed call."""
+        import torch
+        import torch.distributed as dist
+
+        from . import lossless
+
+        p = len(g.ranks)
+        me = g.ranks.index(self.rank)
+        torch.cuda.synchronize()  # no fused kernel in flight across an NCCL call
+        if what == "ag":
+            mine = (p - 1) * lossless.size(x)
+        else:
+            c = x.numel() // p
+            got = torch.empty(p, c, dtype=torch.float32, device=x.device)
+            dist.all_to_all_single(got, x.contiguous().view(p, c), group=g.pg)
+            part = got[(me + 1) % p].clone()
+            mine = 0
+            for t in range(p - 1):
+                mine += lossless.size(part)
+                part = part + got[(me + 2 + t) % p]
+            if what == "ar":
+                mine += (p - 1) * lossless.size(part)
+        w = torch.tensor([mine], dtype=torch.int64, device=x.device)
+        dist.all_reduce(w, group=g.pg)
+        return int(w.item()) // p
 
     # -------------------------------------------------------------- paths
     def dp_allreduce(self, grad, mode: int = 1):
@@ -115,8 +151,9 @@ class HybridComm:
             return x
         out, ev = self._timed(lambda: g.comm.allreduce(x, spec, mode))
         c = x.numel() // p
-        self._record(path, CollectiveKind.AllReduce, p, 2 * (p - 1) * 4 * c, 2 * (p - 1) * wire_size_bytes(spec, c),
-                     2 * (p - 1), ev)
+        wire = (lambda: self._lossless_wire(g, x, "ar")) if self._lossless(spec) else \
+            2 * (p - 1) * wire_size_bytes(spec, c)
+        self._record(path, CollectiveKind.AllReduce, p, 2 * (p - 1) * 4 * c, wire, 2 * (p - 1), ev)
         return out
 
     def tp_allgather(self, shard):
@@ -127,8 +164,9 @@ class HybridComm:
             return shard
         out, ev = self._timed(lambda: g.comm.allgather(shard, spec))
         c = shard.numel()
-        self._record(CommPath.TpAllGather, CollectiveKind.AllGather, p, (p - 1) * 4 * c,
-                     (p - 1) * wire_size_bytes(spec, c), p - 1, ev)
+        wire = (lambda: self._lossless_wire(g, shard, "ag")) if self._lossless(spec) else \
+            (p - 1) * wire_size_bytes(spec, c)
+        self._record(CommPath.TpAllGather, CollectiveKind.AllGather, p, (p - 1) * 4 * c, wire, p - 1, ev)
         return out
 
     def pp_send_recv(self, x, src_stage: int, dst_stage: int):
@@ -139,10 +177,26 @@ class HybridComm:
         spec = self.scheme.at(CommPath.PpP2p)
         out, ev = self._timed(lambda: g.comm.p2p(x, src_stage, dst_stage, spec))
         me = g.ranks.index(self.rank)
+        if self._lossless(spec):
+            wire = self._p2p_lossless_wire(g, x, src_stage)
+        else:
+            wire = wire_size_bytes(spec, x.numel())
         if me in (src_stage, dst_stage):
-            self._record(CommPath.PpP2p, CollectiveKind.P2P, 2, 4 * x.numel(), wire_size_bytes(spec, x.numel()), 1,
-                         ev)
+            self._record(CommPath.PpP2p, CollectiveKind.P2P, 2, 4 * x.numel(), wire, 1, ev)
         return out
+
+    def _p2p_lossless_wire(self, g, x, src_stage: int) -> int:
+        """The sender sizes its payload; the chain learns it by broadcast."""
+        import torch
+        import torch.distributed as dist
+
+        from . import lossless
+
+        torch.cuda.synchronize()
+        me = g.ranks.index(self.rank)
+        w = torch.tensor([lossless.size(x) if me == src_stage else 0], dtype=torch.int64, device=x.device)
+        dist.broadcast(w, g.ranks[src_stage], group=g.pg)
+        return int(w.item())
 
     def zero_reduce_scatter(self, grad):
         """ZeRO-1 gradient reduce-scatter over the DP group (Zero1ReduceScatter)."""
@@ -153,8 +207,9 @@ class HybridComm:
             return grad
         out, ev = self._timed(lambda: g.comm.reduce_scatter(grad, spec))
         c = grad.numel() // p
-        self._record(CommPath.Zero1ReduceScatter, CollectiveKind.ReduceScatter, p, (p - 1) * 4 * c,
-                     (p - 1) * wire_size_bytes(spec, c), p - 1, ev)
+        wire = (lambda: self._lossless_wire(g, grad, "rs")) if self._lossless(spec) else \
+            (p - 1) * wire_size_bytes(spec, c)
+        self._record(CommPath.Zero1ReduceScatter, CollectiveKind.ReduceScatter, p, (p - 1) * 4 * c, wire, p - 1, ev)
         return out
 
     def zero_allgather(self, shard):
@@ -166,8 +221,9 @@ class HybridComm:
             return shard
         out, ev = self._timed(lambda: g.comm.allgather(shard, spec))
         c = shard.numel()
-        self._record(CommPath.Zero1AllGather, CollectiveKind.AllGather, p, (p - 1) * 4 * c,
-                     (p - 1) * wire_size_bytes(spec, c), p - 1, ev)
+        wire = (lambda: self._lossless_wire(g, shard, "ag")) if self._lossless(spec) else \
+            (p - 1) * wire_size_bytes(spec, c)
+        self._record(CommPath.Zero1AllGather, CollectiveKind.AllGather, p, (p - 1) * 4 * c, wire, p - 1, ev)
         return out
 
     def status(self):

@@ -24,6 +24,9 @@ int orc_allreduce(int p, uint64_t n, const float* inputs, int kind, int rate, in
 int orc_reduce_scatter(int p, uint64_t n, const float* inputs, int kind, int rate, float* shards, uint64_t* acct);
 int orc_allgather(int p, uint64_t c, const float* shards, int kind, int rate, float* out, uint64_t* acct);
 double orc_block_bound(const float* v, uint64_t n, int rate);
+uint64_t orc_pred_size(const float* in, uint64_t n);
+uint64_t orc_pred_compress(const float* in, uint64_t n, uint8_t* out);
+int orc_p2p(uint64_t n, const float* in, int kind, int rate, float* out, uint64_t* acct);
 }
 
 using namespace hcc;
@@ -288,8 +291,66 @@ static void test_policy() {
   CHECK(clk.trace()[0].wire_bytes < clk.trace()[1].wire_bytes);
 }
 
+static void test_lossless() {
+  // test_codec.cpp:60-68 round trip of arbitrary bits
+  for (size_t n : {size_t{0}, size_t{1}, size_t{63}, size_t{4096}, size_t{4097}, size_t{10000}}) {
+    const auto x = fill(11 + n, 0, n);
+    const auto cb = compress(CodecSpec::lossless(), x);
+    CHECK(bit_equal(decompress(cb), x));
+    std::vector<uint8_t> want(orc_pred_size(x.data(), n) + 1);
+    CHECK(orc_pred_compress(x.data(), n, want.data()) == cb.payload.size());
+    CHECK(std::memcmp(want.data(), cb.payload.data(), cb.payload.size()) == 0);
+  }
+  // :70-80 constant chunk: 3077 bytes
+  const FloatBuffer ones(4096, 1.0f);
+  const auto cb1 = compress(CodecSpec::lossless(), ones);
+  CHECK(cb1.payload_bytes() == 3077u);
+  CHECK(bit_equal(decompress(cb1), ones));
+  // :95-100 sparse beats dense
+  CHECK(compress(CodecSpec::lossless(), fill(13, 3, 1 << 16, 0.9f, 0)).payload_bytes() <
+        compress(CodecSpec::lossless(), fill(13, 2, 1 << 16)).payload_bytes());
+  // :237-239 truncated payload throws CorruptPayloadError
+  auto cut = compress(CodecSpec::lossless(), fill(15, 2, 4096));
+  cut.payload.resize(cut.payload.size() / 2);
+  CHECK(throws<CorruptPayloadError>([&] { decompress(cut); }));
+  // test_collectives.cpp:35-50 identity and lossless p2p are exact
+  SimClock clk(Topology::b200_box(8));
+  const auto buf = fill(35, 2, 5000);
+  CHECK(bit_equal(p2p(clk, 1, 2, buf, CodecSpec::lossless(), CommPath::PpP2p), buf));
+  uint64_t acct[3];
+  FloatBuffer tmp(5000);
+  orc_p2p(5000, buf.data(), 1, 0, tmp.data(), acct);
+  CHECK(clk.trace().back().wire_bytes == acct[1]);
+  // :189-203 lossless transparency, accounting equal to the oracle's
+  for (int p : {2, 4}) {
+    const auto in = inputs(37 + p, p, 32 * p * 100);
+    SimClock c1(Topology::b200_box(8)), c2(Topology::b200_box(8));
+    const auto id = allreduce(c1, comm_of(p), in, CodecSpec::identity(), CommPath::DpAllReduce);
+    const auto mpc = allreduce(c2, comm_of(p), in, CodecSpec::lossless(), CommPath::DpAllReduce);
+    for (int i = 0; i < p; ++i) CHECK(bit_equal(id[i], mpc[i]));
+    CHECK(c1.trace()[0].raw_bytes == c2.trace()[0].raw_bytes);
+    const auto f = flat(in);
+    std::vector<float> out(f.size());
+    uint64_t a[3];
+    orc_allreduce(p, in[0].size(), f.data(), 1, 0, 0, out.data(), a);
+    CHECK(c2.trace()[0].wire_bytes == a[1]);
+    SimClock c3(Topology::b200_box(8));
+    ring_reduce_scatter(c3, comm_of(p), in, CodecSpec::lossless(), CommPath::Zero1ReduceScatter);
+    std::vector<float> sh(f.size() / p);
+    orc_reduce_scatter(p, in[0].size(), f.data(), 1, 0, sh.data(), a);
+    CHECK(c3.trace()[0].wire_bytes == a[1]);
+  }
+  // :275-292 deterministic replay
+  const auto in = inputs(41, 4, 128);
+  SimClock r1(Topology::b200_box(8)), r2(Topology::b200_box(8));
+  const auto o1 = allreduce(r1, comm_of(4), in, CodecSpec::lossless(), CommPath::DpAllReduce);
+  const auto o2 = allreduce(r2, comm_of(4), in, CodecSpec::lossless(), CommPath::DpAllReduce);
+  CHECK(bit_equal(o1[0], o2[0]) && r1.trace()[0].wire_bytes == r2.trace()[0].wire_bytes);
+}
+
 int main() {
   test_codec();
+  test_lossless();
   test_collectives();
   test_policy();
   std::printf("hcc shim tests: %d passed, %d failed\n", g_pass, g_fail);

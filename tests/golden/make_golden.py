@@ -30,8 +30,60 @@ CODEC_SIZES = [1, 63, 64, 65, 255, 256, 257, 1000, 2049]
 MODES = [("uniform", -1.0, 1.0), ("finite", 0, 0), ("sparse", 0.5, 0)]
 
 
+def lossless() -> None:
+    """LosslessPredictor payloads (hcc::compress) and its collective byte
+    accounting, including buffers whose chunks mix coded and raw-fallback."""
+    out = {}
+    seed = 9000
+    for n in [1, 63, 4095, 4096, 4097, 3 * 4096 + 17, 20000]:
+        for mode, lo, hi in [("bits", 0, 0), ("sparse", 0.9, 0), ("uniform", -1.0, 1.0), ("const", 0, 0),
+                             ("mixed", 0, 0)]:
+            seed += 1
+            if mode == "const":
+                x = np.full(n, 1.0, np.float32)
+            elif mode == "mixed":  # alternate chunks: sparse (coded) / random bits (raw)
+                a = O.ref_fill(seed, "sparse", n, 0.9, 0)
+                b = O.ref_fill(seed + 1, "bits", n, 0, 0)
+                idx = (np.arange(n) // 4096) % 2 == 1
+                x = np.where(idx, b, a).astype(np.float32)
+            else:
+                x = O.ref_fill(seed, mode, n, lo, hi)
+            payload, cc = O.ref_compress("lossless", 0, x)
+            key = f"n{n}_{mode}"
+            out[f"{key}_in"] = x
+            out[f"{key}_payload"] = payload
+            out[f"{key}_cc"] = np.array([cc], np.uint64)
+    for p in [2, 4]:
+        for n_per in [64, 5000]:
+            n = n_per * p
+            seed += 1
+            x = np.stack([O.ref_fill(seed * 13 + j, "sparse" if j % 2 else "uniform", n, 0.5 if j % 2 else -1.0, 1.0)
+                          for j in range(p)])
+            key = f"p{p}_n{n}"
+            out[f"{key}_in"] = x
+            for avg in (0, 1):
+                r, acct = O.ref_allreduce(x, "lossless", 0, bool(avg))
+                out[f"{key}_ar{avg}"] = r
+                out[f"{key}_ar{avg}_acct"] = np.array(acct, np.uint64)
+            r, acct = O.ref_reduce_scatter(x, "lossless", 0)
+            out[f"{key}_rs"] = r
+            out[f"{key}_rs_acct"] = np.array(acct, np.uint64)
+            shards = np.ascontiguousarray(x[:, :n_per])
+            r, acct = O.ref_allgather(shards, "lossless", 0)
+            out[f"{key}_ag"] = r
+            out[f"{key}_ag_acct"] = np.array(acct, np.uint64)
+            r, acct = O.ref_p2p(x[1], "lossless", 0)
+            out[f"{key}_p2p_acct"] = np.array(acct, np.uint64)
+    np.savez_compressed(os.path.join(HERE, "lossless.npz"), **out)
+    print("wrote", len(out), "lossless arrays")
+
+
 def main() -> None:
     assert O.ref is not None, "oracle/_ref/libhcc_ref.so is required (build with oracle/build_ref.sh)"
+    if "--only-lossless" in sys.argv:
+        lossless()
+        return
+    lossless()
     codec = {}
     seed = 1000
     for rate in CODEC_RATES:

@@ -106,6 +106,55 @@ def main():
         xs = np.stack([O.fill(1234 + j, "normal", n, 1e-3) for j in range(p)])
         got = comm.allreduce(torch.from_numpy(xs[rank]).cuda(), spec, 1)
         cmp("big ar r8", got, O.allreduce(xs, "fixed-rate", 8, True)[0][rank])
+    # mz-hybrid over the NVLink engine: lossless TP / ZeRO / PP paths (values
+    # via the transparent ring, TraceEvent bytes sized on the device) and the
+    # fixed-rate DP path, against the oracle's values and accounting
+    from paper_2409_02423_b200 import ParallelLayout, scheme_from_name
+    from paper_2409_02423_b200.hybrid import HybridComm
+
+    torch.cuda.synchronize()
+    scheme = scheme_from_name("mz-hybrid:8")
+    n = 3000 * p
+    xs = np.stack([O.fill(900 + j, "sparse" if j % 2 else "normal", n, 0.6 if j % 2 else 1e-3) for j in range(p)])
+    x = torch.from_numpy(xs[rank]).cuda()
+    for lay_name, lay in (("tp", ParallelLayout(1, 1, p)), ("dp", ParallelLayout(p, 1, 1)), ("pp", ParallelLayout(1, p, 1))):
+        hc = HybridComm(lay, scheme, n)
+        if lay_name == "tp":
+            got = hc.tp_allreduce(x)
+            want, acct = O.allreduce(xs, "lossless", 0, False)
+            cmp("mz tp ar", got, want[rank])
+            ev = hc.trace[-1]
+            if (ev.raw_bytes, ev.wire_bytes, ev.round_count) != acct:
+                fails.append(f"mz tp acct {(ev.raw_bytes, ev.wire_bytes, ev.round_count)} != {acct}")
+            sh = torch.from_numpy(np.ascontiguousarray(xs[rank, :3000])).cuda()
+            got = hc.tp_allgather(sh)
+            want, acct = O.allgather(np.ascontiguousarray(xs[:, :3000]), "lossless")
+            cmp("mz tp ag", got, want[rank])
+            ev = hc.trace[-1]
+            if (ev.raw_bytes, ev.wire_bytes, ev.round_count) != acct:
+                fails.append(f"mz tp ag acct {(ev.raw_bytes, ev.wire_bytes, ev.round_count)} != {acct}")
+        elif lay_name == "dp":
+            got = hc.dp_allreduce(x)
+            want, acct = O.allreduce(xs, "fixed-rate", 8, True)
+            cmp("mz dp ar", got, want[rank])
+            if hc.trace[-1].wire_bytes != acct[1]:
+                fails.append("mz dp acct")
+            got = hc.zero_reduce_scatter(x)
+            want, acct = O.reduce_scatter(xs, "lossless")
+            cmp("mz zero rs", got, want[rank])
+            ev = hc.trace[-1]
+            if (ev.raw_bytes, ev.wire_bytes, ev.round_count) != acct:
+                fails.append(f"mz zero rs acct {(ev.raw_bytes, ev.wire_bytes, ev.round_count)} != {acct}")
+        else:
+            got = hc.pp_send_recv(x, 0, p - 1)
+            if rank == p - 1:
+                want, acct = O.p2p(xs[0], "lossless")
+                cmp("mz pp", got, want)
+                if hc.trace[-1].wire_bytes != acct[1]:
+                    fails.append("mz pp acct")
+        hc.status()
+        torch.cuda.synchronize()
+        hc.close()
     # non-finite partial sums are reported, not hung
     bad = torch.full((4096 * p,), 3.0e38, device="cuda")
     comm.allreduce(bad, spec)

@@ -218,3 +218,27 @@ def test_collectives_match_reference(p):
         a = O.allgather(s, kind, rate)
         b = O.ref_allgather(s, kind, rate)
         assert a[0].tobytes() == b[0].tobytes() and a[1] == b[1]
+
+
+def test_lossless_oracle_matches_golden():
+    """Oracle restatement vs payloads/accounting produced by the reference
+    itself (tests/golden/lossless.npz, make_golden.py)."""
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "lossless.npz"))
+    keys = sorted(k[:-8] for k in g.files if k.endswith("_payload"))
+    assert keys
+    for k in keys:
+        x = g[k + "_in"]
+        assert O.pred_compress(x).tobytes() == g[k + "_payload"].tobytes(), k
+        assert O.pred_decompress(g[k + "_payload"], x.size).tobytes() == x.tobytes(), k
+    for k in sorted(k[:-3] for k in g.files if k.endswith("_rs") and k.startswith("p")):
+        x = g[k + "_in"]
+        p = x.shape[0]
+        for avg in (0, 1):
+            out, acct = O.allreduce(x, "lossless", 0, bool(avg))
+            assert out.tobytes() == g[f"{k}_ar{avg}"].tobytes() and acct == tuple(g[f"{k}_ar{avg}_acct"]), k
+        out, acct = O.reduce_scatter(x, "lossless")
+        assert out.tobytes() == g[k + "_rs"].tobytes() and acct == tuple(g[k + "_rs_acct"]), k
+        out, acct = O.allgather(np.ascontiguousarray(x[:, : x.shape[1] // p]), "lossless")
+        assert out.tobytes() == g[k + "_ag"].tobytes() and acct == tuple(g[k + "_ag_acct"]), k
+        _, acct = O.p2p(x[1], "lossless")
+        assert acct == tuple(g[k + "_p2p_acct"]), k
