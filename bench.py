@@ -199,39 +199,64 @@ def bench_codec(args):
     s = torch.cuda.current_stream()
     sp = s.cuda_stream
 
-    def step(i, ev=None):
+    def step(i, stream, which=3):
         k = i % nsets
-        if ev:
-            ev[0].record(s)
-        st = _lib.hccx_compress(codec, xs[k].data_ptr(), n, ps[k].data_ptr(), err.data_ptr(), sp)
-        if ev:
-            ev[1].record(s)
-        st |= _lib.hccx_decompress(codec, ps[k].data_ptr(), W, n, ys[k].data_ptr(), sp)
-        if ev:
-            ev[2].record(s)
+        st = 0
+        if which & 1:
+            st |= _lib.hccx_compress(codec, xs[k].data_ptr(), n, ps[k].data_ptr(), err.data_ptr(), stream)
+        if which & 2:
+            st |= _lib.hccx_decompress(codec, ps[k].data_ptr(), W, n, ys[k].data_ptr(), stream)
         assert st == 0
 
     for i in range(args.warmup):
-        step(i)
+        step(i, sp)
     assert _lib.hccx_flag_status(err.data_ptr(), sp) == 0
     torch.cuda.synchronize()
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
-    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+    # The K timed steps are captured once into a CUDA graph (launch-bound
+    # inner loop -> graph, no host issue gaps or per-kernel events between
+    # the kernels) and replayed inside the timed region.
+    def capture(which, count):
+        g = torch.cuda.CUDAGraph()
+        cs = torch.cuda.Stream()
+        cs.wait_stream(s)
+        with torch.cuda.stream(cs):
+            g.capture_begin()
+            for i in range(count):
+                step(i, cs.cuda_stream, which)
+            g.capture_end()
+        torch.cuda.synchronize()
+        return g
+
     launches0 = _lib.hccx_launch_count()
+    g_steps = capture(3, args.steps)
+    launches = _lib.hccx_launch_count() - launches0
+    g_steps.replay()  # upload + one untimed pass
+    torch.cuda.synchronize()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(0) as clk:
         torch.cuda.synchronize()
-        # Queue a short device-side spin first so the host gets ahead of the
-        # GPU: the timed region then measures device work, not Python issue.
-        torch.cuda._sleep(int(1e6 + 1e5 * min(args.steps, 200)))
         t0.record(s)
-        for i in range(args.steps):
-            step(i, evs[i])
+        g_steps.replay()
         t1.record(s)
         torch.cuda.synchronize()
-    launches = _lib.hccx_launch_count() - launches0
     ms = t0.elapsed_time(t1) / args.steps
-    tc = sum(e[0].elapsed_time(e[1]) for e in evs) / args.steps
-    td = sum(e[1].elapsed_time(e[2]) for e in evs) / args.steps
+
+    # Per-kernel average launch duration (roofline): K back-to-back launches
+    # of one kernel over the same rotated buffers, one event pair around the
+    # replay, on the stream the kernels run on.
+    def kernel_ms(which):
+        g = capture(which, args.steps)
+        g.replay()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(s)
+        g.replay()
+        b.record(s)
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / args.steps
+
+    tc, td = kernel_ms(1), kernel_ms(2)
     # correctness of the timed output: decompress(compress(x)) within the block bound
     k = (args.steps - 1) % nsets
     assert torch.isfinite(ys[k]).all()
@@ -281,6 +306,8 @@ def bench_codec(args):
             "n_values": n, "rate_bits": rate, "payload_bytes": W,
             "l2": f"inputs rotated over {nsets} buffer sets ({nsets * per_set >> 20} MiB > 126 MiB L2)",
             "compress_ms": round(tc, 5), "decompress_ms": round(td, 5),
+            "timing": "K steps captured in one CUDA graph, events around the replay; per-kernel ms from K "
+                      "back-to-back launches of that kernel alone",
             "compress_GBps_uncompressed": round(4 * n / (tc * 1e-3) / 1e9, 1),
             "decompress_GBps_uncompressed": round(4 * n / (td * 1e-3) / 1e9, 1),
         },

@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libhccx.so")
+# HCCX_LIB: load an alternative build (kernel-variant experiments only).
+LIB_PATH = os.environ.get("HCCX_LIB") or os.path.join(_HERE, "libhccx.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(

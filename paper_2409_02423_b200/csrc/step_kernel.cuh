@@ -276,8 +276,14 @@ __global__ void __launch_bounds__(kStepThreads) step_kernel(const __grid_constan
 // path above.
 // ---------------------------------------------------------------------------
 
-constexpr int kTmaStages = 4;
-constexpr int kTmaConsumers = 8;
+#ifndef HCCX_TMA_STAGES
+#define HCCX_TMA_STAGES 4
+#endif
+#ifndef HCCX_TMA_CONSUMERS
+#define HCCX_TMA_CONSUMERS 8
+#endif
+constexpr int kTmaStages = HCCX_TMA_STAGES;
+constexpr int kTmaConsumers = HCCX_TMA_CONSUMERS;
 constexpr int kTmaThreads = (kTmaConsumers + 1) * 32;
 constexpr int kTileGroups = kTmaConsumers;
 
