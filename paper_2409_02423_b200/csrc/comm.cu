@@ -69,6 +69,9 @@ static_assert(sizeof(HandleBlob) <= HCCX_HANDLE_BYTES, "handle blob too large");
 
 uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
 
+constexpr uint64_t kOneShotMaxChunk = 1ull << 21;         // values per chunk the one-shot slots hold
+constexpr uint64_t kOneShotDefaultBytes = 1ull << 24;     // allreduce bytes per rank routed one-shot
+
 uint64_t timeout_ns() {
   const char* e = std::getenv("HCCX_TIMEOUT_MS");
   const uint64_t ms = e ? std::strtoull(e, nullptr, 10) : 20000;
@@ -83,6 +86,8 @@ struct hccx_comm {
   uint64_t slot_bytes = 0;  // payload capacity per slot (worst codec: 257 B / 64 values)
   uint32_t max_seg = 0;
   uint64_t rs_off = 0, ag_off = 0, pp_off = 0, flag_off = 0, win_bytes = 0;
+  uint64_t os_cap = 0;  // one-shot allreduce: values per chunk
+  uint64_t os_off = 0, os_ag_off = 0, os_flag_off = 0, os_raw_bytes = 0, os_ag_bytes = 0;
   uint8_t* win = nullptr;
   uint8_t* peers[kMaxRanks] = {};
   bool connected = false;
@@ -111,13 +116,21 @@ extern "C" hccx_status_t hccx_comm_create(int rank, int nranks, int device, uint
   c->ag_off = c->rs_off + (nranks - 1) * c->slot_bytes;
   c->pp_off = c->ag_off + nranks * c->slot_bytes;
   c->flag_off = c->pp_off + nranks * c->slot_bytes;
-  c->win_bytes = c->flag_off + align_up(nslots * (c->max_seg + kAckIdx) * 4, 256);
+  // one-shot region (oneshot.cuh): p-1 raw fp32 slots + p gather slots + flags
+  c->os_cap = c->chunk_cap < kOneShotMaxChunk ? c->chunk_cap : kOneShotMaxChunk;
+  c->os_raw_bytes = align_up(4 * c->os_cap, 256);
+  c->os_ag_bytes = align_up((c->os_cap + 63) / 64 * 257, 256);
+  c->os_off = c->flag_off + align_up(nslots * (c->max_seg + kAckIdx) * 4, 256);
+  c->os_ag_off = c->os_off + (nranks - 1) * c->os_raw_bytes;
+  c->os_flag_off = c->os_ag_off + nranks * c->os_ag_bytes;
+  c->win_bytes = c->os_flag_off + align_up(2ull * nranks * kAckIdx * 4, 256);
   if (cudaMalloc(&c->win, c->win_bytes) != cudaSuccess || cudaMalloc(&c->d_err, 4) != cudaSuccess) {
     cudaFree(c->win);
     delete c;
     return HCCX_ERR_CUDA;
   }
-  if (cudaMemset(c->win + c->flag_off, 0, c->win_bytes - c->flag_off) != cudaSuccess ||
+  if (cudaMemset(c->win + c->flag_off, 0, c->os_off - c->flag_off) != cudaSuccess ||
+      cudaMemset(c->win + c->os_flag_off, 0, c->win_bytes - c->os_flag_off) != cudaSuccess ||
       cudaMemset(c->d_err, 0, 4) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) {
     cudaFree(c->win);
     cudaFree(c->d_err);
@@ -203,6 +216,17 @@ FusedParams base_params(hccx_comm* c, int op, uint64_t n_chunk, const float* in,
     return e ? std::atoi(e) : 0;
   }();
   P.debug = dbg;
+  static const uint32_t step_segs = [] {
+    const char* e = std::getenv("HCCX_STEP_SEGS");
+    const int v = e ? std::atoi(e) : 0;
+    return v > 0 ? static_cast<uint32_t>(v) : 0u;  // 0: chosen per launch (fused_launch.cuh)
+  }();
+  P.step_segs = step_segs;
+  P.os_off = c->os_off;
+  P.os_ag_off = c->os_ag_off;
+  P.os_flag_off = c->os_flag_off;
+  P.os_raw_bytes = c->os_raw_bytes;
+  P.os_ag_bytes = c->os_ag_bytes;
   P.trace = c->d_trace;
   P.trace_cap = c->trace_cap;
   // chunk offsets are multiples of n_chunk floats: aligned iff n_chunk % 8 == 0
@@ -213,6 +237,17 @@ FusedParams base_params(hccx_comm* c, int op, uint64_t n_chunk, const float* in,
 hccx_status_t check_comm(hccx_comm* c, hccx_codec_t codec) {
   if (!c || !c->connected) return HCCX_ERR_INVALID_ARGUMENT;
   return check_codec(codec);
+}
+
+// Allreduce algorithm choice: the two-round one-shot path up to
+// HCCX_ONESHOT_BYTES (bytes per rank, default below; 0 disables it), the
+// fused ring above.  Both give the reference's bits.
+bool use_oneshot(const hccx_comm* c, uint64_t n) {
+  static const uint64_t limit = [] {
+    const char* e = std::getenv("HCCX_ONESHOT_BYTES");
+    return e ? std::strtoull(e, nullptr, 10) : kOneShotDefaultBytes;
+  }();
+  return 4 * n <= limit && n / c->p <= c->os_cap;
 }
 
 hccx_status_t run(hccx_comm* c, hccx_codec_t codec, const FusedParams& P, cudaStream_t s) {
@@ -236,9 +271,13 @@ extern "C" hccx_status_t hccx_allreduce(hccx_comm_t c, const float* d_in, float*
   }
   FusedParams P = base_params(c, kFAllReduce, n / c->p, d_in, d_out);
   P.epoch = ++c->epoch;
-  P.prev_rs = c->last_rs;
-  P.prev_ag = c->last_ag;
-  c->last_rs = c->last_ag = P.epoch;
+  if (use_oneshot(c, n)) {
+    P.op = kFOneShotAllReduce;  // own slots and flags: the ring's slot epochs are untouched
+  } else {
+    P.prev_rs = c->last_rs;
+    P.prev_ag = c->last_ag;
+    c->last_rs = c->last_ag = P.epoch;
+  }
   StepParams tmp{};
   set_divisor(tmp, mode, c->p);
   P.div_mode = tmp.div_mode;

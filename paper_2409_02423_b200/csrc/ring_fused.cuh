@@ -30,13 +30,26 @@
 namespace hccx {
 
 constexpr int kMaxRanks = 16;
-constexpr int kFusedWarps = 8;
-constexpr int kFusedThreads = kFusedWarps * 32;
-constexpr int kSegGroups = kFusedWarps;  // groups per segment
+// Compute warps per CTA of the fused kernel.  One CTA per SM with 24
+// compute warps working through the same segments: with three 8-warp CTAs
+// per SM the warp scheduler's age priority starved the SM's third CTA, which
+// then finished ~30 us after the others while running alone latency-bound.
+#ifndef HCCX_FUSED_COMPUTE
+#define HCCX_FUSED_COMPUTE 24
+#endif
+constexpr int kFusedWarps = HCCX_FUSED_COMPUTE;
+constexpr int kFCtasPerSm = 24 / kFusedWarps;
+constexpr int kSegGroups = kFusedWarps;  // groups per segment (one per compute warp)
 constexpr uint32_t kSegVals = kSegGroups * kGroupVals;
-constexpr uint32_t kStepSegs = 16;  // segments per published step (one fence + flag)
 
-enum FusedOp : int { kFAllReduce = 0, kFReduceScatter = 1, kFAllGather = 2, kFBroadcast = 3, kFP2P = 4 };
+enum FusedOp : int {
+  kFAllReduce = 0,
+  kFReduceScatter = 1,
+  kFAllGather = 2,
+  kFBroadcast = 3,
+  kFP2P = 4,
+  kFOneShotAllReduce = 5  // small-message allreduce (oneshot.cuh)
+};
 
 struct FusedParams {
   uint8_t* win[kMaxRanks];  // every rank's window (own included), mapped in this process
@@ -58,12 +71,10 @@ struct FusedParams {
   uint64_t timeout_ns;
   uint64_t* trace;  // optional event log (hccx_comm_trace_enable): [0] = count, then (tag, t_ns) pairs
   uint64_t trace_cap;
+  uint64_t os_off, os_ag_off, os_flag_off;  // one-shot region: raw slots, gather slots, flags
+  uint64_t os_raw_bytes, os_ag_bytes;       // one-shot slot strides
+  uint32_t step_segs;  // segments per published step (one release + flag per destination)
   int debug;  // development knobs (HCCX_DEBUG): 16 = warp-store pushes, 32 = synchronous tile release, 64 = log launches
-};
-
-struct FusedSmem {
-  uint8_t tile[kSegGroups * 1040];  // >= 8 x largest group (1028 B), 16B multiple
-  uint8_t stage[kFusedWarps][kStageBytes];
 };
 
 // Flag classes in every window:
@@ -79,7 +90,7 @@ struct FusedSmem {
 // A sender CTA waits once per slot per call on its own index's ack of the
 // slot's previous use before overwriting it -- back-to-back collectives
 // never race a slow receiver.
-constexpr uint32_t kAckIdx = 1024;  // >= any co-resident grid of the fused kernel (148 SMs x 3 CTAs)
+constexpr uint32_t kAckIdx = 1024;  // >= any co-resident grid of the fused kernel (148 SMs x CTAs per SM)
 
 __device__ __forceinline__ uint32_t* flag_ptr(const FusedParams& P, int rank, int cls, int slot, uint32_t idx) {
   const int p = P.p;
@@ -269,18 +280,18 @@ __device__ __forceinline__ void fused_group(const FusedParams& P, const uint8_t*
 // ---------------------------------------------------------------------------
 
 constexpr int kFMaxStages = 8;                      // input ring depth cap (mbarrier pairs)
-constexpr uint32_t kFArena = 49152;                  // input ring bytes, carved per phase
+constexpr uint32_t kFArena = 6144u * kFusedWarps;    // input ring bytes, carved per phase
 constexpr int kFMaxTiles = 8;                        // output (push) ring depth cap
-constexpr uint32_t kFTileBudget = 17408;             // output ring bytes
+constexpr uint32_t kFTileBudget = 2176u * kFusedWarps;  // output ring bytes
 constexpr int kFReadsInFlight = 4;                   // bulk pushes whose smem read may be pending
 constexpr uint32_t kFPrefetch = 4;                   // L2 prefetch distance (segments)
 constexpr int kFCompute = kFusedWarps;               // compute warps
-constexpr int kFThreads2 = (kFCompute + 2) * 32;     // + producer warp + pusher warp
-constexpr uint32_t kFTileBytes = 8448;               // >= 8 x 1028 B groups, 128B multiple
+constexpr int kFThreads2 = (kFCompute + 3) * 32;     // + producer, pusher and signaller warps
 constexpr uint32_t kFGenBytes = kFCompute * kStageBytes;
 
-// Output tiles hold one encoded segment (8 groups) each; their size follows
-// the codec (2 KiB at r8), so the ring is as deep as the budget allows.
+// Output tiles hold one encoded segment (one group per compute warp) each;
+// their size follows the codec (6 KiB at r8 with 24 warps), so the ring is as
+// deep as the budget allows.
 template <class Codec>
 struct TileGeom {
   static constexpr uint32_t kBytes = (kSegGroups * Codec::kGroupBytes + 127u) / 128u * 128u;
@@ -298,7 +309,8 @@ struct FusedSmem2 {
   uint64_t tfull[kFMaxTiles];
   uint64_t tempty[kFMaxTiles];
   uint32_t direct[kFMaxStages];
-  uint32_t prog[kFCompute + 2];  // debug: per-warp progress word (phase << 20 | segment << 4 | state)
+  uint32_t prog[kFCompute + 3];  // debug: per-warp progress word (phase << 20 | segment << 4 | state)
+  uint32_t sig_events;           // pusher -> signaller: events completed (release/acquire, CTA scope)
 };
 
 enum PhaseKind : int { kPhEnc = 0, kPhDar = 1, kPhFinAr = 2, kPhFinRs = 3, kPhDec = 4 };
@@ -489,7 +501,6 @@ __device__ __forceinline__ uint32_t push_epoch(const FusedParams& P, int push_cl
   return push_cls == 2 ? P.pp_epoch[d] : P.epoch;
 }
 
-__device__ __forceinline__ void consumer_bar() { asm volatile("bar.sync 1, %0;" ::"n"(kFCompute * 32) : "memory"); }
 
 template <class Codec>
 __device__ __forceinline__ void compute_group(const FusedParams& P, const Phase& f, uint64_t g, bool direct,
@@ -550,8 +561,10 @@ __device__ __forceinline__ void compute_group(const FusedParams& P, const Phase&
   }
 }
 
+static_assert(kFusedWarps == 8 || kFusedWarps == 12 || kFusedWarps == 24, "CTAs per SM = 24 / compute warps");
+
 template <class Codec>
-__global__ void __launch_bounds__(kFThreads2, 3) ring_fused_kernel(const __grid_constant__ FusedParams P) {
+__global__ void __launch_bounds__(kFThreads2, kFCtasPerSm) ring_fused_kernel(const __grid_constant__ FusedParams P) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   FusedSmem2<Codec>& S = *reinterpret_cast<FusedSmem2<Codec>*>(smem_raw);
   constexpr int kT = TileGeom<Codec>::kTiles;
@@ -584,9 +597,16 @@ __global__ void __launch_bounds__(kFThreads2, 3) ring_fused_kernel(const __grid_
       mbar_init(&S.tfull[tt], kFCompute);
       mbar_init(&S.tempty[tt], 1);
     }
+    S.sig_events = 0;
     fence_mbar_init();
   }
   __syncthreads();
+  if (P.trace && threadIdx.x == 0 && 16384 + blockIdx.x < P.trace_cap) {
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    P.trace[8192 + 2 * blockIdx.x] = globaltimer_ns();
+    P.trace[16384 + blockIdx.x] = smid;
+  }
 
   if (warp == kFCompute) {
     // ------------------------------------------------------------ producer
@@ -599,8 +619,8 @@ __global__ void __launch_bounds__(kFThreads2, 3) ring_fused_kernel(const __grid_
         // the arena is re-carved for this phase: every earlier fill must be consumed
         for (int b = 0; b < kFMaxStages; ++b) mbar_wait_to(P, &S.empty[b], ((pu >> b) & 1u) ^ 1u, 0x100u | b, S.prog);
         int st = 0;
-        for (uint32_t k0 = 0; k0 < myseg; k0 += kStepSegs) {
-          const uint32_t k1 = min(k0 + kStepSegs, myseg);
+        for (uint32_t k0 = 0; k0 < myseg; k0 += P.step_segs) {
+          const uint32_t k1 = min(k0 + P.step_segs, myseg);
           if (f.wait_cls >= 0) {
             const uint64_t t0 = clock64();
             spin_ge(P, flag_ptr(P, j, f.wait_cls, f.wait_slot, seg_of(k0)), f.wait_ep, 0x700u | (ph << 4) | f.wait_cls);
@@ -667,7 +687,8 @@ __global__ void __launch_bounds__(kFThreads2, 3) ring_fused_kernel(const __grid_
     int tt = 0;
     uint32_t tbit = 0;
     uint32_t seq = 0, released = 0;  // segments seen / tiles handed back (ring order)
-    uint64_t c_tfull = 0, c_read = 0, c_pub = 0, c_credit = 0, c_total = clock64();
+    uint64_t c_tfull = 0, c_read = 0, c_pub = 0, c_credit = 0, c_issue = 0, c_total = clock64();
+    uint32_t events = 0;  // signaller events issued (lane 0)
     auto release_upto = [&](uint32_t upto) {
       for (; released < upto; ++released) mbar_arrive(&S.tempty[released % kT]);
     };
@@ -687,8 +708,8 @@ __global__ void __launch_bounds__(kFThreads2, 3) ring_fused_kernel(const __grid_
       }
       __syncwarp();
       c_credit += clock64() - tc;
-      for (uint32_t k0 = 0; k0 < myseg; k0 += kStepSegs) {
-        const uint32_t k1 = min(k0 + kStepSegs, myseg);
+      for (uint32_t k0 = 0; k0 < myseg; k0 += P.step_segs) {
+        const uint32_t k1 = min(k0 + P.step_segs, myseg);
         for (uint32_t k = k0; k < k1; ++k) {
           const uint32_t sg = seg_of(k);
           if (lane == 0) {
@@ -707,6 +728,7 @@ __global__ void __launch_bounds__(kFThreads2, 3) ring_fused_kernel(const __grid_
             // bit 16 selects the warp's 16-byte stores instead.
             if ((nb & 15u) == 0 && !(P.debug & 16)) {
               if (lane == 0) {
+                const uint64_t ti = clock64();
                 // the tile was written through the generic proxy; the bulk
                 // copy reads it through the async proxy
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -717,6 +739,7 @@ __global__ void __launch_bounds__(kFThreads2, 3) ring_fused_kernel(const __grid_
                   bulk_s2g(slot_ptr(P, d, f.push_cls, f.push_slot) + soff, S.tile[tt], nb);
                 }
                 bulk_commit();
+                c_issue += clock64() - ti;
               }
               bulk_issued = true;
             } else {
@@ -750,30 +773,20 @@ __global__ void __launch_bounds__(kFThreads2, 3) ring_fused_kernel(const __grid_
             tbit ^= 1u;
           }
         }
-        if (push) {  // publish the step once its stores are complete
+        if (push) {  // the step's stores are complete: hand its publication to the signaller
           const uint64_t t2 = clock64();
           if (lane == 0) {
             bulk_wait_all();
             release_upto(seq);
+            st_release_cta_shared(&S.sig_events, ++events);
           }
           c_pub += clock64() - t2;
-          __syncwarp();  // all lanes' stores precede the release below (warp barrier + release cumulativity)
-          if (lane < p - 1) {
-            const int d = (j + 1 + lane) % p;
-            const bool tgt =
-                f.push_mode == 1 || (f.push_mode == 0 && lane == 0) || (f.push_mode == 2 && d == P.dst);
-            if (tgt) signal(flag_ptr(P, d, f.push_cls, f.push_slot, seg_of(k0)), push_epoch(P, f.push_cls, d));
-          }
           __syncwarp();
         }
       }
       // every segment of the phase has been computed (tfull) -> its inbox
-      // inputs are consumed: acknowledge for this CTA's index space
-      if (f.ack_rank >= 0) {  // one fence, then relaxed stores of the ack words
-        fence_acq_rel_sys();
-        for (uint32_t kk = blockIdx.x + lane * G; kk < kAckIdx; kk += G * 32)
-          st_relaxed_sys(flag_ptr(P, f.ack_rank, f.ack_cls, f.ack_slot, 0) + kk, f.ack_ep);
-      }
+      // inputs are consumed: the signaller acknowledges them
+      if (f.ack_rank >= 0 && lane == 0) st_release_cta_shared(&S.sig_events, ++events);
       __syncwarp();
     }
     if (lane == 0) {
@@ -784,6 +797,69 @@ __global__ void __launch_bounds__(kFThreads2, 3) ring_fused_kernel(const __grid_
       trace_acc(P, 10, c_read);
       trace_acc(P, 11, c_pub);
       trace_acc(P, 12, c_credit);
+      trace_acc(P, 13, c_issue);
+      if (P.trace && 8192 + 2 * blockIdx.x + 1 < P.trace_cap) P.trace[8193 + 2 * blockIdx.x] = globaltimer_ns();
+    }
+    return;
+  }
+
+  if (warp == kFCompute + 2) {
+    // ----------------------------------------------------------- signaller
+    // Publishes the pusher's completed steps (one release store per
+    // destination flag) and the phase-end consumption acks (one fence, then
+    // relaxed stores).  System-scope releases cost microseconds under load;
+    // here they overlap the pusher's next step instead of stalling the tile
+    // ring.  Walks the same (phase, step) sequence as the pusher and waits
+    // for each event on S.sig_events: the pusher's release.cta store after
+    // its bulk writes completed, this warp's acquire, then the sys-scope
+    // release -- causality order carries the writes to the remote reader.
+    uint32_t events = 0;
+    uint64_t c_sig = 0, c_ack = 0;
+    auto wait_event = [&](uint32_t ev) {
+      if (lane == 0) {
+        const uint64_t t0 = globaltimer_ns();
+        for (uint32_t spins = 0; ld_acquire_cta_shared(&S.sig_events) < ev; ++spins) {
+          if ((spins & 255u) == 255u) {
+            if (P.err && (ldg_u32_coherent(P.err) & kErrTimeout)) break;
+            if (globaltimer_ns() - t0 > P.timeout_ns) {
+              if (P.err) atomicOr(P.err, kErrTimeout);
+              trace_timeout(P, 0xa00u, S.prog);
+              break;
+            }
+          }
+        }
+      }
+      __syncwarp();
+    };
+    for (int ph = 0; ph < nph; ++ph) {
+      const Phase f = phase_of(P, ph);
+      if (f.push_cls >= 0) {
+        for (uint32_t k0 = 0; k0 < myseg; k0 += P.step_segs) {
+          wait_event(++events);
+          const uint64_t ts = clock64();
+          if (lane < p - 1) {
+            const int d = (j + 1 + lane) % p;
+            const bool tgt =
+                f.push_mode == 1 || (f.push_mode == 0 && lane == 0) || (f.push_mode == 2 && d == P.dst);
+            if (tgt) signal(flag_ptr(P, d, f.push_cls, f.push_slot, seg_of(k0)), push_epoch(P, f.push_cls, d));
+          }
+          __syncwarp();
+          c_sig += clock64() - ts;
+        }
+      }
+      if (f.ack_rank >= 0) {  // one fence, then relaxed stores of the ack words
+        wait_event(++events);
+        const uint64_t ta = clock64();
+        fence_acq_rel_sys();
+        for (uint32_t kk = blockIdx.x + lane * G; kk < kAckIdx; kk += G * 32)
+          st_relaxed_sys(flag_ptr(P, f.ack_rank, f.ack_cls, f.ack_slot, 0) + kk, f.ack_ep);
+        c_ack += clock64() - ta;
+        __syncwarp();
+      }
+    }
+    if (lane == 0) {
+      trace_acc(P, 14, c_ack);
+      trace_acc(P, 15, c_sig);
     }
     return;
   }
