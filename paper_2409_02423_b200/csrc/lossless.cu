@@ -188,29 +188,53 @@ __global__ void __launch_bounds__(kLLWarps * 32) ll_emit_kernel(const float* __r
   }
 }
 
-// decompress (a): offsets by walking coded chunks' 5-bit fields
+// decompress (a): offsets by walking coded chunks' 5-bit length fields.
+// Serial by format (no stored offsets).  The chain per code is
+// pos += 37 - field(pos); the stream is read through a register window of
+// two aligned 64-bit words (read-only path), refilled only when the position
+// crosses a word, so the dependent chain is a funnel shift, a mask and an add.
+__device__ __forceinline__ uint64_t ll_word(const uint8_t* in, uint64_t in_bytes, uint64_t w) {
+  const uint64_t b0 = w * 8;
+  if (b0 + 8 <= in_bytes) {
+    if ((reinterpret_cast<uintptr_t>(in) & 7u) == 0) return __ldg(reinterpret_cast<const unsigned long long*>(in) + w);
+    uint64_t v = 0;
+    for (int k = 0; k < 8; ++k) v |= static_cast<uint64_t>(__ldg(in + b0 + k)) << (8 * k);
+    return v;
+  }
+  uint64_t v = 0;
+  for (uint64_t k = 0; b0 + k < in_bytes && k < 8; ++k) v |= static_cast<uint64_t>(__ldg(in + b0 + k)) << (8 * k);
+  return v;
+}
+
 __global__ void ll_walk_kernel(const uint8_t* __restrict__ in, uint64_t in_bytes, uint64_t n, uint64_t nchunks,
                                uint64_t* __restrict__ offsets, uint32_t* __restrict__ err) {
   if (threadIdx.x != 0) return;
   uint64_t pos = (nchunks + 7) / 8;
+  const uint64_t end_bit = 8 * in_bytes;
   for (uint64_t c = 0; c < nchunks; ++c) {
     offsets[c] = pos;
     const uint32_t live = static_cast<uint32_t>(n - c * kChunk < kChunk ? n - c * kChunk : kChunk);
-    if ((in[c / 8] >> (c % 8)) & 1u) {
+    if ((__ldg(in + c / 8) >> (c % 8)) & 1u) {
       pos += 4ull * live;
     } else {
       uint64_t bit = pos * 8;
-      const uint64_t end_bit = 8 * in_bytes;
-      for (uint32_t i = 0; i < live && bit <= end_bit; ++i) {
+      uint64_t wi = bit >> 6;
+      uint64_t lo = ll_word(in, in_bytes, wi), hi = ll_word(in, in_bytes, wi + 1);
+      for (uint32_t i = 0; i < live; ++i) {
         if (bit + 5 > end_bit) {
           bit = end_bit + 1;  // truncated inside a length field
           break;
         }
-        const uint64_t B = bit >> 3;
-        uint32_t w = in[B];
-        if (B + 1 < in_bytes) w |= static_cast<uint32_t>(in[B + 1]) << 8;
-        const uint32_t z = (w >> (bit & 7)) & 31u;
-        bit += 5 + (32 - z);
+        const uint64_t w = bit >> 6;
+        if (w != wi) {  // advance the window (codes are <= 37 bits: at most one word)
+          lo = hi;
+          hi = ll_word(in, in_bytes, w + 1);
+          if (w != wi + 1) lo = ll_word(in, in_bytes, w);
+          wi = w;
+        }
+        const uint32_t sh = static_cast<uint32_t>(bit & 63);
+        const uint64_t win = sh ? (lo >> sh) | (hi << (64 - sh)) : lo;
+        bit += 5 + (32 - static_cast<uint32_t>(win & 31u));
       }
       pos = bit > end_bit ? in_bytes + 1 : (bit + 7) / 8;
     }
@@ -222,54 +246,61 @@ __global__ void ll_walk_kernel(const uint8_t* __restrict__ in, uint64_t in_bytes
   offsets[nchunks] = pos;
 }
 
-// decompress (b): one warp per chunk from its offset (lane 0 decodes the
-// chain of codes; the warp stores the values)
-__global__ void __launch_bounds__(kLLWarps * 32) ll_decode_kernel(const uint8_t* __restrict__ in, uint64_t in_bytes,
-                                                                  uint64_t n, uint64_t nchunks,
-                                                                  const uint64_t* __restrict__ offsets,
-                                                                  float* __restrict__ out) {
-  extern __shared__ uint32_t llsm[];
+// decompress (b): raw chunks, one warp per chunk (coalesced copies)
+__global__ void __launch_bounds__(kLLWarps * 32) ll_raw_kernel(const uint8_t* __restrict__ in, uint64_t in_bytes,
+                                                               uint64_t n, uint64_t nchunks,
+                                                               const uint64_t* __restrict__ offsets,
+                                                               float* __restrict__ out) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint32_t* vals = llsm + warp * kChunk;
   for (uint64_t c = static_cast<uint64_t>(blockIdx.x) * kLLWarps + warp; c < nchunks;
        c += static_cast<uint64_t>(gridDim.x) * kLLWarps) {
+    if (!((__ldg(in + c / 8) >> (c % 8)) & 1u)) continue;
     const uint64_t base = c * kChunk;
     const uint32_t live = static_cast<uint32_t>(n - base < kChunk ? n - base : kChunk);
     const uint8_t* src = in + offsets[c];
-    uint32_t* o = reinterpret_cast<uint32_t*>(out) + base;
-    if ((in[c / 8] >> (c % 8)) & 1u) {
-      const uint64_t avail = in_bytes - offsets[c];
-      for (uint32_t i = lane; i < live && 4ull * i + 4 <= avail; i += 32) {
-        uint32_t v = 0;
-        memcpy(&v, src + 4 * i, 4);
-        o[i] = v;
-      }
-      continue;
-    }
     const uint64_t avail = in_bytes - offsets[c];
-    if (lane == 0) {
-      uint64_t bit = 0;
-      uint32_t prev = 0;
-      auto get = [&](uint32_t nb) -> uint32_t {
-        if (nb == 0) return 0u;
-        const uint64_t B = bit >> 3;
-        uint64_t w = 0;
-        for (int k = 0; k < 6; ++k)
-          if (B + k < avail) w |= static_cast<uint64_t>(src[B + k]) << (8 * k);
-        const uint32_t v = static_cast<uint32_t>(w >> (bit & 7)) & (nb >= 32 ? 0xffffffffu : ((1u << nb) - 1u));
-        bit += nb;
-        return v;
-      };
-      for (uint32_t i = 0; i < live; ++i) {
-        const uint32_t z = get(5);
-        const uint32_t low = get(32 - z);
-        prev ^= low;
-        vals[i] = prev;
-      }
+    uint32_t* o = reinterpret_cast<uint32_t*>(out) + base;
+    for (uint32_t i = lane; i < live && 4ull * i + 4 <= avail; i += 32) {
+      uint32_t v = 0;
+      memcpy(&v, src + 4 * i, 4);
+      o[i] = v;
     }
-    __syncwarp();
-    for (uint32_t i = lane; i < live; i += 32) o[i] = vals[i];
-    __syncwarp();
+  }
+}
+
+// decompress (c): coded chunks, one thread per chunk -- the code chain is
+// serial within a chunk, so chunks are the parallelism; the stream is read
+// through a 128-bit register window (every code is <= 37 bits).
+__global__ void __launch_bounds__(128) ll_decode_kernel(const uint8_t* __restrict__ in, uint64_t in_bytes, uint64_t n,
+                                                        uint64_t nchunks, const uint64_t* __restrict__ offsets,
+                                                        float* __restrict__ out) {
+  for (uint64_t c = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; c < nchunks;
+       c += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    if ((__ldg(in + c / 8) >> (c % 8)) & 1u) continue;
+    const uint64_t base = c * kChunk;
+    const uint32_t live = static_cast<uint32_t>(n - base < kChunk ? n - base : kChunk);
+    uint32_t* o = reinterpret_cast<uint32_t*>(out) + base;
+    uint64_t bit = offsets[c] * 8;
+    uint64_t wi = bit >> 6;
+    uint64_t lo = ll_word(in, in_bytes, wi), hi = ll_word(in, in_bytes, wi + 1);
+    uint32_t prev = 0;
+    for (uint32_t i = 0; i < live; ++i) {
+      const uint64_t w = bit >> 6;
+      if (w != wi) {
+        lo = hi;
+        hi = ll_word(in, in_bytes, w + 1);
+        if (w != wi + 1) lo = ll_word(in, in_bytes, w);
+        wi = w;
+      }
+      const uint32_t sh = static_cast<uint32_t>(bit & 63);
+      const uint64_t win = sh ? (lo >> sh) | (hi << (64 - sh)) : lo;
+      const uint32_t z = static_cast<uint32_t>(win & 31u);
+      const uint32_t nb = 32 - z;
+      const uint32_t low = static_cast<uint32_t>(win >> 5) & (nb >= 32 ? 0xffffffffu : ((1u << nb) - 1u));
+      bit += 5 + nb;
+      prev ^= low;
+      o[i] = prev;
+    }
   }
 }
 
@@ -361,8 +392,6 @@ extern "C" hccx_status_t hccx_lossless_compress(const float* d_in, uint64_t n, u
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(ll_emit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    cudaFuncSetAttribute(ll_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(sizeof(uint32_t) * kLLWarps * kChunk));
     attr = true;
   }
   ll_flags_kernel<<<grid_for((nch + 7) / 8, 256), 256, 0, st>>>(t_scratch.fallback, nch, d_out);
@@ -381,16 +410,12 @@ extern "C" hccx_status_t hccx_lossless_decompress(const uint8_t* d_in, uint64_t 
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   hccx_status_t r = t_scratch.ensure(nch);
   if (r != HCCX_OK) return r;
-  static bool attr = false;
-  const size_t smem = sizeof(uint32_t) * kLLWarps * kChunk;
-  if (!attr) {
-    cudaFuncSetAttribute(ll_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    attr = true;
-  }
   cudaMemsetAsync(t_scratch.err, 0, 4, st);
   ll_walk_kernel<<<1, 32, 0, st>>>(d_in, in_bytes, n, nch, t_scratch.offsets, t_scratch.err);
-  ll_decode_kernel<<<grid_for(nch, kLLWarps), kLLWarps * 32, smem, st>>>(d_in, in_bytes, n, nch, t_scratch.offsets,
-                                                                         d_out);
+  ll_raw_kernel<<<grid_for(nch, kLLWarps), kLLWarps * 32, 0, st>>>(d_in, in_bytes, n, nch, t_scratch.offsets, d_out);
+  ll_decode_kernel<<<static_cast<unsigned>((nch + 127) / 128), 128, 0, st>>>(d_in, in_bytes, n, nch, t_scratch.offsets,
+                                                                          d_out);
+  count_launch(1);
   count_launch(2);
   if (cudaGetLastError() != cudaSuccess) return HCCX_ERR_CUDA;
   uint32_t e = 0;
