@@ -626,6 +626,7 @@ __global__ void __launch_bounds__(kFThreads2, kFCtasPerSm) ring_fused_kernel(con
             spin_ge(P, flag_ptr(P, j, f.wait_cls, f.wait_slot, seg_of(k0)), f.wait_ep, 0x700u | (ph << 4) | f.wait_cls);
             asm volatile("fence.proxy.async.global;" ::: "memory");
             c_flag += clock64() - t0;
+            trace_ev(P, 1, ph, k0);
           }
           for (uint32_t k = k0; k < k1; ++k) {
             const uint32_t sg = seg_of(k);
@@ -740,6 +741,7 @@ __global__ void __launch_bounds__(kFThreads2, kFCtasPerSm) ring_fused_kernel(con
                 }
                 bulk_commit();
                 c_issue += clock64() - ti;
+                trace_ev(P, 3, ph, k);
               }
               bulk_issued = true;
             } else {
@@ -845,6 +847,7 @@ __global__ void __launch_bounds__(kFThreads2, kFCtasPerSm) ring_fused_kernel(con
           }
           __syncwarp();
           c_sig += clock64() - ts;
+          if (lane == 0) trace_ev(P, 5, ph, k0);
         }
       }
       if (f.ack_rank >= 0) {  // one fence, then relaxed stores of the ack words
@@ -895,6 +898,7 @@ __global__ void __launch_bounds__(kFThreads2, kFCtasPerSm) ring_fused_kernel(con
       if (g < ngroups) compute_group<Codec>(P, f, g, direct, sa, sb, S.tile[tt] + warp * GB, gen, lane, bad);
       __syncwarp();
       c_comp += clock64() - t2;
+      if (warp == 0 && lane == 0) trace_ev(P, 2, ph, k);
       if (lane == 0) S.prog[warp] = (ph << 20) | (k << 4) | 3u;
       if (lane == 0) {
         mbar_arrive(&S.empty[st]);
