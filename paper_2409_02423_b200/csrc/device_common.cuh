@@ -118,6 +118,16 @@ __device__ __forceinline__ uint32_t ld_acquire_cta_shared(const uint32_t* p) {
   return v;
 }
 
+// Programmatic dependent launch (kernels launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization): wait until the
+// preceding grid on the stream has completed and its writes are visible, then
+// let the next grid start launching (its CTAs become resident as ours exit).
+// Both are no-ops for an ordinary launch.
+__device__ __forceinline__ void pdl_wait_and_release() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 __device__ __forceinline__ void fence_acq_rel_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
 
 __device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {

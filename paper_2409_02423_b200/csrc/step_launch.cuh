@@ -8,6 +8,23 @@
 
 namespace hccx {
 
+// Launch with programmatic stream serialization, so a kernel's launch and
+// prologue overlap the previous kernel's tail (the kernels call
+// pdl_wait_and_release() before touching global memory).
+inline cudaError_t launch_pdl(const void* k, int grid, int threads, void** args, size_t smem, cudaStream_t stream) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelExC(&cfg, k, args);
+}
+
 template <class Codec, int kOp>
 cudaError_t launch_tma(const StepParams& p, cudaStream_t stream) {
   using L = TmaLayout<Codec, kOp>;
@@ -25,7 +42,7 @@ cudaError_t launch_tma(const StepParams& p, cudaStream_t stream) {
   const int grid = tma_grid(k, kTmaThreads, L::kSmem, tiles > 0 ? tiles : groups * p.njobs);
   void* args[] = {const_cast<StepParams*>(&p)};
   count_launch();
-  return cudaLaunchKernel(k, dim3(grid), dim3(kTmaThreads), args, L::kSmem, stream);
+  return launch_pdl(k, grid, kTmaThreads, args, L::kSmem, stream);
 }
 
 template <class Codec, int kOp>
@@ -39,7 +56,7 @@ cudaError_t launch_op(const StepParams& p, cudaStream_t stream) {
   const int grid = stream_grid(k, groups);
   void* args[] = {const_cast<StepParams*>(&p)};
   count_launch();
-  return cudaLaunchKernel(k, dim3(grid), dim3(kStepThreads), args, 0, stream);
+  return launch_pdl(k, grid, kStepThreads, args, 0, stream);
 }
 
 template <class Codec>
