@@ -17,6 +17,7 @@
 // registers (two 64-bit words per block, no local memory).
 #pragma once
 #include "device_common.cuh"
+#include "zfp_planes.cuh"
 
 namespace hccx {
 
@@ -48,6 +49,11 @@ struct Bits128 {
     }
     pos += nbits;
     return v & ((1ull << nbits) - 1ull);
+  }
+  __device__ __forceinline__ uint64_t peek() const {  // the next 64 bits (zeros past the end)
+    if (pos == 0) return lo;
+    if (pos < 64) return (lo >> pos) | (hi << (64 - pos));
+    return pos < 128 ? hi >> (pos - 64) : 0ull;
   }
 };
 
@@ -102,31 +108,18 @@ __device__ __forceinline__ void encode_block(const float (&v)[4], Bits128& b, ui
   uint32_t u[4];
 #pragma unroll
   for (int i = 0; i < 4; ++i) u[i] = (static_cast<uint32_t>(q[i]) + kNB) ^ kNB;
+  // embedded coding, one bit plane per step (zfp_planes.cuh)
   uint32_t bits = 4 * R - 9;
   uint32_t n = 0;
   for (int k = 31; bits && k >= 0; --k) {
-    uint32_t x = ((u[0] >> k) & 1u) | (((u[1] >> k) & 1u) << 1) | (((u[2] >> k) & 1u) << 2) |
-                 (((u[3] >> k) & 1u) << 3);
-    const uint32_t m = min(n, bits);
+    const uint32_t x = ((u[0] >> k) & 1u) | (((u[1] >> k) & 1u) << 1) | (((u[2] >> k) & 1u) << 2) |
+                       (((u[3] >> k) & 1u) << 3);
+    uint32_t code, nn;
+    const uint32_t len = zfp_planes::plane_code(n, x, &code, &nn);
+    const uint32_t m = min(len, bits);
+    b.put(code & ((1u << m) - 1u), static_cast<int>(m));
     bits -= m;
-    b.put(x & ((1u << m) - 1u), static_cast<int>(m));
-    x >>= m;
-    while (n < 4 && bits) {
-      bits--;
-      const uint32_t any = x != 0;
-      b.put(any, 1);
-      if (!any) break;
-      while (n < 3 && bits) {
-        bits--;
-        const uint32_t bit = x & 1u;
-        b.put(bit, 1);
-        if (bit) break;
-        x >>= 1;
-        n++;
-      }
-      x >>= 1;
-      n++;
-    }
+    n = nn;
   }
 }
 
@@ -142,22 +135,12 @@ __device__ __forceinline__ void decode_block(Bits128& b, float (&v)[4]) {
   uint32_t bits = 4 * R - 9;
   uint32_t n = 0;
   for (int k = 31; bits && k >= 0; --k) {
-    const uint32_t m = min(n, bits);
-    bits -= m;
-    uint32_t x = static_cast<uint32_t>(b.get(static_cast<int>(m)));
-    while (n < 4 && bits) {
-      bits--;
-      if (!b.get(1)) break;
-      while (n < 3 && bits) {
-        bits--;
-        if (b.get(1)) break;
-        n++;
-      }
-      x += 1u << n;
-      n++;
-    }
+    uint32_t used;
+    const uint32_t x = zfp_planes::plane_decode(b.peek(), bits, &n, &used);
+    b.pos += static_cast<int>(used);
+    bits -= used;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) u[i] += ((x >> i) & 1u) << k;
+    for (int i = 0; i < 4; ++i) u[i] |= ((x >> i) & 1u) << k;
   }
   int32_t q[4];
 #pragma unroll

@@ -1,0 +1,110 @@
+// test_zfp_planes.cpp -- the plane-at-a-time zfp coder (csrc/zfp_planes.cuh)
+// against the per-bit loops of the published coder (the ones in
+// oracle/hcc_oracle.c zfp_encode_block / zfp_decode_block), exhaustively
+// over (significant count n, plane bits x, remaining budget) with random
+// trailing stream bits.  CPU only.
+#include <cstdint>
+#include <cstdio>
+#include <random>
+
+#include "zfp_planes.cuh"
+
+using namespace hccx::zfp_planes;
+
+// per-bit encoder of one plane: returns emitted bits (LSB-first) and count
+static uint32_t ref_encode(uint32_t& n, uint32_t x, uint32_t& bits, uint32_t& code) {
+  uint32_t len = 0;
+  code = 0;
+  auto put = [&](uint32_t b) { code |= (b & 1u) << len; ++len; };
+  const uint32_t m = n < bits ? n : bits;
+  bits -= m;
+  for (uint32_t i = 0; i < m; ++i) { put(x); x >>= 1; }
+  while (n < 4 && bits) {
+    bits--;
+    const uint32_t any = x != 0;
+    put(any);
+    if (!any) break;
+    while (n < 3 && bits) {
+      bits--;
+      const uint32_t b = x & 1u;
+      put(b);
+      if (b) break;
+      x >>= 1;
+      n++;
+    }
+    x >>= 1;
+    n++;
+  }
+  return len;
+}
+
+static uint32_t ref_decode(uint64_t w, uint32_t& bits, uint32_t& n, uint32_t& used) {
+  used = 0;
+  auto get = [&]() { return static_cast<uint32_t>((w >> used++) & 1u); };
+  const uint32_t m = n < bits ? n : bits;
+  bits -= m;
+  uint32_t x = 0;
+  for (uint32_t i = 0; i < m; ++i) x |= get() << i;
+  while (n < 4 && bits) {
+    bits--;
+    if (!get()) break;
+    while (n < 3 && bits) {
+      bits--;
+      if (get()) break;
+      n++;
+    }
+    x += 1u << n;
+    n++;
+  }
+  return x;
+}
+
+int main() {
+  int fails = 0, checks = 0;
+  std::mt19937_64 rng(7);
+  for (uint32_t n0 = 0; n0 <= 4; ++n0)
+    for (uint32_t x = 0; x < 16; ++x) {
+      // plane values must agree with the significance state: coefficients
+      // below n0 are significant already, any bit pattern is valid
+      uint32_t code, nn;
+      const uint32_t len = plane_code(n0, x, &code, &nn);
+      for (uint32_t budget = 0; budget <= 12; ++budget) {
+        uint32_t n = n0, bits = budget, rc;
+        const uint32_t rl = ref_encode(n, x, bits, rc);
+        const uint32_t m = len < budget ? len : budget;
+        ++checks;
+        if (rl != m || (rc & ((1u << m) - 1u)) != (code & ((1u << m) - 1u)) || (len <= budget && n != nn)) {
+          if (fails++ < 10) std::printf("encode n=%u x=%u budget=%u: ref len %u code %x n %u | new len %u code %x n %u\n",
+                                        n0, x, budget, rl, rc, n, len, code, nn);
+        }
+        for (int t = 0; t < 8; ++t) {  // decode the (possibly truncated) codeword + random trailing bits
+          uint64_t w = (rng() << m) | (code & ((1u << m) - 1u));
+          uint32_t rn = n0, rb = budget, ru;
+          const uint32_t rx = ref_decode(w, rb, rn, ru);
+          uint32_t dn = n0, du;
+          const uint32_t dx = plane_decode(w, budget, &dn, &du);
+          ++checks;
+          if (rx != dx || ru != du || rn != dn) {
+            if (fails++ < 20)
+              std::printf("decode n=%u x=%u budget=%u w=%llx: ref x %u used %u n %u | new x %u used %u n %u\n", n0, x,
+                          budget, static_cast<unsigned long long>(w), rx, ru, rn, dx, du, dn);
+          }
+        }
+      }
+    }
+  // random streams (not produced by the encoder) through the decoder
+  for (int t = 0; t < 200000; ++t) {
+    const uint64_t w = rng();
+    const uint32_t n0 = rng() % 5, budget = rng() % 40;
+    uint32_t rn = n0, rb = budget, ru, dn = n0, du;
+    const uint32_t rx = ref_decode(w, rb, rn, ru);
+    const uint32_t dx = plane_decode(w, budget, &dn, &du);
+    ++checks;
+    if (rx != dx || ru != du || rn != dn) {
+      if (fails++ < 30) std::printf("random decode n=%u budget=%u w=%llx: ref %u/%u/%u new %u/%u/%u\n", n0, budget,
+                                    static_cast<unsigned long long>(w), rx, ru, rn, dx, du, dn);
+    }
+  }
+  std::printf("zfp plane coder: %d checks, %d failures\n", checks, fails);
+  return fails ? 1 : 0;
+}
