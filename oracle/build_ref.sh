@@ -26,6 +26,7 @@ if [ -d "$REF/src" ]; then
       -I "$REF/include" -I "$REF/src" -I "$REF/tests" \
       "$REF/src/codec.cpp" "$REF/src/codec_omp.cpp" "$REF/src/codec_serial.cpp" \
       "$REF/src/collectives.cpp" "$REF/src/netsim.cpp" "$REF/src/parallel3d.cpp" \
+      "$REF/src/toymodel.cpp" "$REF/src/linalg.cpp" \
       "$REF/tests/support/oracles.cpp" "$here/ref_capi.cpp" \
       -o "$here/_ref/libhcc_ref.so.tmp"
   mv "$here/_ref/libhcc_ref.so.tmp" "$here/_ref/libhcc_ref.so"

@@ -16,7 +16,9 @@
 #include "hcc/collectives.hpp"
 #include "hcc/errors.hpp"
 #include "hcc/netsim.hpp"
+#include "hcc/parallel3d.hpp"
 #include "hcc/rng.hpp"
+#include "hcc/toymodel.hpp"
 #include "support/oracles.hpp"
 
 namespace {
@@ -215,6 +217,48 @@ void ref_fill(uint64_t seed, int mode, uint64_t n, float lo, float hi, float* ou
     default: b = hcc::testing::sparse_buffer(rng, n, lo); break;
   }
   if (n) std::memcpy(out, b.data(), 4 * n);
+}
+
+// hcc::Trainer3D (src/toymodel.cpp:239-467) through run_experiment: the
+// reference's 3D-parallel toy trainer on a one-node lassen_like topology of
+// dp*pp*tp GPUs.  Outputs the step losses, the final eval loss, the
+// assembled replica-0 model and raw/wire bytes per CommPath (enum order).
+int ref_train(int num_blocks, int hidden, int width, int batch, int microbatches, int steps, uint64_t seed,
+              float lr, int dp, int pp, int tp, const char* scheme, int zero, float* step_loss,
+              int* steps_completed, float* final_eval, int* diverged, float* w1, float* w2, uint64_t* path_bytes) {
+  try {
+    hcc::ToyModelConfig cfg;
+    cfg.num_blocks = num_blocks;
+    cfg.hidden_dim = hidden;
+    cfg.input_dim = width;
+    cfg.batch_size = batch;
+    cfg.microbatches = microbatches;
+    cfg.steps = steps;
+    cfg.seed = seed;
+    cfg.learning_rate = lr;
+    hcc::Topology topo = hcc::Topology::lassen_like(1);
+    topo.gpus_per_node = dp * pp * tp;
+    const auto layout = hcc::build_layout(dp, pp, tp, topo);
+    hcc::Trainer3D trainer(cfg, layout, topo, hcc::scheme_from_name(scheme),
+                           zero == 0 ? hcc::ZeroMode::Off : (zero == 1 ? hcc::ZeroMode::Replace
+                                                                       : hcc::ZeroMode::Redundant));
+    const auto met = trainer.run();
+    for (std::size_t i = 0; i < met.step_loss.size(); ++i) step_loss[i] = met.step_loss[i];
+    *steps_completed = met.steps_completed;
+    *final_eval = met.final_eval_loss;
+    *diverged = met.diverged ? 1 : 0;
+    const auto model = trainer.assemble_replica(0);
+    std::memcpy(w1, model.w1.data(), 4 * model.w1.size());
+    std::memcpy(w2, model.w2.data(), 4 * model.w2.size());
+    for (int k = 0; k < 12; ++k) path_bytes[k] = 0;
+    for (const auto& [path, b] : met.bytes_by_path) {
+      path_bytes[2 * static_cast<int>(path)] = b.raw;
+      path_bytes[2 * static_cast<int>(path) + 1] = b.wire;
+    }
+    return 0;
+  } catch (...) {
+    return status_of(std::current_exception());
+  }
 }
 
 }  // extern "C"

@@ -78,11 +78,41 @@ def lossless() -> None:
     print("wrote", len(out), "lossless arrays")
 
 
+SMALL_CFG = {"num_blocks": 4, "hidden_dim": 16, "input_dim": 8, "batch_size": 8, "microbatches": 2, "steps": 4,
+             "seed": 3, "learning_rate": 2e-3}  # proj/tests/test_toymodel.cpp:15-26 (steps shortened)
+TRAIN_CASES = [  # (name, cfg overrides, dp, pp, tp, scheme, zero: 0 off / 1 replace / 2 redundant)
+    ("base3d_none_off", {}, 2, 2, 2, "no-compression", 0),
+    ("base3d_mpc_off", {}, 2, 2, 2, "naive-mpc", 0),
+    ("base3d_zhyb_replace", {}, 2, 2, 2, "z-hybrid:16,8", 1),
+    ("base3d_mzhyb_off", {}, 2, 2, 2, "mz-hybrid:8", 0),
+    ("dp4_none_redundant", {"batch_size": 32, "steps": 3}, 4, 1, 1, "no-compression", 2),
+    ("dp2_zfp8_replace", {"steps": 5}, 2, 1, 1, "naive-zfp8", 1),
+    ("pp2tp2_zhyb_off", {}, 1, 2, 2, "z-hybrid:16,4", 0),
+    ("diverge_zfp8", {"steps": 20, "learning_rate": 1e30}, 2, 1, 1, "naive-zfp8", 0),
+]
+
+
+def trainer() -> None:
+    """hcc::Trainer3D runs (the reference's toy 3D-parallel trainer)."""
+    out = {}
+    for name, over, dp, pp, tp, scheme, zero in TRAIN_CASES:
+        cfg = dict(SMALL_CFG, **over)
+        r = O.ref_train(cfg, dp, pp, tp, scheme, zero)
+        for k, v in r.items():
+            out[f"{name}__{k}"] = np.asarray(v)
+    np.savez_compressed(os.path.join(HERE, "trainer.npz"), **out)
+    print("wrote", len(out), "trainer arrays")
+
+
 def main() -> None:
     assert O.ref is not None, "oracle/_ref/libhcc_ref.so is required (build with oracle/build_ref.sh)"
     if "--only-lossless" in sys.argv:
         lossless()
         return
+    if "--only-trainer" in sys.argv:
+        trainer()
+        return
+    trainer()
     lossless()
     codec = {}
     seed = 1000

@@ -80,6 +80,8 @@ def _load_ref():
     lib.ref_allgather.argtypes = [i32, u64, _f, i32, i32, _f, _u64]
     lib.ref_p2p.argtypes = [u64, _f, i32, i32, _f, _u64]
     lib.ref_fill.argtypes = [u64, i32, u64, C.c_float, C.c_float, _f]
+    lib.ref_train.argtypes = [i32, i32, i32, i32, i32, i32, u64, C.c_float, i32, i32, i32, C.c_char_p, i32, _f,
+                              C.POINTER(C.c_int), C.POINTER(C.c_float), C.POINTER(C.c_int), _f, _f, _u64]
     return lib
 
 
@@ -297,3 +299,21 @@ def ref_p2p(x: np.ndarray, kind: str, rate: int = 0):
     if st:
         raise RuntimeError(f"reference status {st}")
     return out[: x.size], tuple(int(a) for a in acct)
+
+
+def ref_train(cfg: dict, dp: int, pp: int, tp: int, scheme: str, zero: int):
+    """hcc::Trainer3D::run via oracle/_ref (the reference compiled): returns a
+    dict of step losses, final eval loss, replica-0 model and path bytes."""
+    steps = cfg["steps"]
+    nb, hid, w = cfg["num_blocks"], cfg["hidden_dim"], cfg["input_dim"]
+    loss = np.zeros(max(steps, 1), np.float32)
+    w1 = np.zeros(nb * hid * w, np.float32)
+    w2 = np.zeros(nb * w * hid, np.float32)
+    pb = np.zeros(12, np.uint64)
+    done, ev, div = C.c_int(0), C.c_float(0), C.c_int(0)
+    st = ref.ref_train(nb, hid, w, cfg["batch_size"], cfg["microbatches"], steps, cfg["seed"], cfg["learning_rate"],
+                       dp, pp, tp, scheme.encode(), zero, loss, C.byref(done), C.byref(ev), C.byref(div), w1, w2, pb)
+    if st:
+        raise RuntimeError(f"reference status {st}")
+    return {"step_loss": loss[: done.value], "steps_completed": done.value, "final_eval_loss": np.float32(ev.value),
+            "diverged": bool(div.value), "w1": w1, "w2": w2, "path_bytes": pb}
