@@ -358,6 +358,37 @@ __device__ __forceinline__ int nphases(const FusedParams& P) {
   }
 }
 
+// Allgather ring hop k (1..p-1): shard i = j-k arrives from the left
+// neighbour in our ag slot i; decode it into `out` and, unless the right
+// neighbour owns it, forward the payload unchanged into the right
+// neighbour's ag slot i.  Every rank thus pushes (p-1)W bytes per allgather,
+// one W per phase, instead of (p-1)W at once from the owner (which made the
+// owner's last reduce-scatter phase NVLink-bound).  Consumption is acked to
+// the left neighbour (the writer) per slot; the credit for slot i waits on
+// the right neighbour's ack.
+__device__ __forceinline__ void ring_ag_hop(const FusedParams& P, Phase& f, int k, float* out, bool div) {
+  const int p = P.p, j = P.rank;
+  const int i = (j - k + p) % p;
+  f.kind = kPhDec;
+  f.pay = P.win[j] + P.ag_off + static_cast<uint64_t>(i) * P.slot_bytes;
+  f.out = out;
+  f.div = div;
+  f.wait_cls = 1;
+  f.wait_slot = i;
+  f.wait_ep = P.epoch;
+  f.ack_rank = (j + p - 1) % p;
+  f.ack_cls = 4;
+  f.ack_slot = i;
+  f.ack_ep = P.epoch;
+  if (k < p - 1) {
+    f.push_cls = 1;
+    f.push_slot = i;
+    f.push_mode = 0;
+    f.credit_cls = 4;
+    f.credit_ep = P.prev_ag;
+  }
+}
+
 __device__ __forceinline__ Phase phase_of(const FusedParams& P, int ph) {
   const int p = P.p, j = P.rank;
   const uint64_t c = P.n_chunk;
@@ -407,9 +438,9 @@ __device__ __forceinline__ Phase phase_of(const FusedParams& P, int ph) {
         f.kind = kPhFinAr;
         f.out = cout(j);
         f.div = true;
-        f.push_cls = 1;
+        f.push_cls = 1;  // own shard starts its allgather ring: right neighbour's ag slot j
         f.push_slot = j;
-        f.push_mode = 1;
+        f.push_mode = 0;
         f.credit_cls = 4;
         f.credit_ep = P.prev_ag;
       } else {
@@ -417,18 +448,7 @@ __device__ __forceinline__ Phase phase_of(const FusedParams& P, int ph) {
         f.out = P.out;
       }
     } else {
-      const int i = (j - (ph - p + 1) + p) % p;
-      f.kind = kPhDec;
-      f.pay = P.win[j] + P.ag_off + static_cast<uint64_t>(i) * P.slot_bytes;
-      f.out = cout(i);
-      f.div = true;
-      f.wait_cls = 1;
-      f.wait_slot = i;
-      f.wait_ep = P.epoch;
-      f.ack_rank = i;
-      f.ack_cls = 4;
-      f.ack_slot = j;
-      f.ack_ep = P.epoch;
+      ring_ag_hop(P, f, ph - p + 1, cout((j - (ph - p + 1) + p) % p), true);
     }
   } else if (P.op == kFAllGather) {
     if (ph == 0) {
@@ -437,21 +457,11 @@ __device__ __forceinline__ Phase phase_of(const FusedParams& P, int ph) {
       f.out = P.out + static_cast<uint64_t>(j) * c;
       f.push_cls = 1;
       f.push_slot = j;
-      f.push_mode = 1;
+      f.push_mode = 0;
       f.credit_cls = 4;
       f.credit_ep = P.prev_ag;
     } else {
-      const int i = (j - ph + p) % p;
-      f.kind = kPhDec;
-      f.pay = P.win[j] + P.ag_off + static_cast<uint64_t>(i) * P.slot_bytes;
-      f.out = P.out + static_cast<uint64_t>(i) * c;
-      f.wait_cls = 1;
-      f.wait_slot = i;
-      f.wait_ep = P.epoch;
-      f.ack_rank = i;
-      f.ack_cls = 4;
-      f.ack_slot = j;
-      f.ack_ep = P.epoch;
+      ring_ag_hop(P, f, ph, P.out + static_cast<uint64_t>((j - ph + p) % p) * c, false);
     }
   } else {  // broadcast / p2p
     if (j == P.root) {
@@ -541,6 +551,11 @@ __device__ __forceinline__ void compute_group(const FusedParams& P, const Phase&
   }
   // ---- outputs
   if (f.kind == kPhDec || f.kind == kPhFinRs) {
+    if (f.kind == kPhDec && f.push_cls >= 0) {  // ring allgather: forward the payload bytes unchanged
+      const uint32_t* src = reinterpret_cast<const uint32_t*>(direct ? f.pay + g * Codec::kGroupBytes : sa);
+      uint32_t* dst = reinterpret_cast<uint32_t*>(tile_g);
+      for (uint32_t w = static_cast<uint32_t>(lane); w < Codec::kGroupBytes / 4; w += 32) dst[w] = src[w];
+    }
     if (f.div) apply_div(v, P.div_mode, P.recip, P.divisor);
     store_vals(f.out, base, live, vec, lane, v);
     return;
