@@ -120,7 +120,8 @@ extern "C" hccx_status_t hccx_comm_create(int rank, int nranks, int device, uint
   c->os_cap = c->chunk_cap < kOneShotMaxChunk ? c->chunk_cap : kOneShotMaxChunk;
   c->os_raw_bytes = align_up(4 * c->os_cap, 256);
   c->os_ag_bytes = align_up((c->os_cap + 63) / 64 * 257, 256);
-  c->os_off = c->flag_off + align_up(nslots * (c->max_seg + kAckIdx) * 4, 256);
+  // data flags: 3p-1 slots x max_seg; acks: 4p-1 slots x kAckIdx (ring_fused.cuh flag classes)
+  c->os_off = c->flag_off + align_up((nslots * c->max_seg + (nslots + nranks) * kAckIdx) * 4, 256);
   c->os_ag_off = c->os_off + (nranks - 1) * c->os_raw_bytes;
   c->os_flag_off = c->os_ag_off + nranks * c->os_ag_bytes;
   c->win_bytes = c->os_flag_off + align_up(2ull * nranks * kAckIdx * 4, 256);
@@ -222,6 +223,15 @@ FusedParams base_params(hccx_comm* c, int op, uint64_t n_chunk, const float* in,
     return v > 0 ? static_cast<uint32_t>(v) : 0u;  // 0: chosen per launch (fused_launch.cuh)
   }();
   P.step_segs = step_segs;
+  // Allgather (and the allreduce's gather half) as a forwarding ring once a
+  // chunk is large: the owner pushing to all p-1 peers at once makes that
+  // phase NVLink-bound (measured p=4: ring wins at 64 MiB chunks, direct at
+  // 16 MiB); HCCX_AG_RING_BYTES sets the chunk size threshold.
+  static const uint64_t ring_from = [] {
+    const char* e = std::getenv("HCCX_AG_RING_BYTES");
+    return e ? std::strtoull(e, nullptr, 10) : (32ull << 20);
+  }();
+  P.ag_ring = 4 * n_chunk >= ring_from ? 1 : 0;
   P.os_off = c->os_off;
   P.os_ag_off = c->os_ag_off;
   P.os_flag_off = c->os_flag_off;

@@ -73,6 +73,7 @@ struct FusedParams {
   uint64_t trace_cap;
   uint64_t os_off, os_ag_off, os_flag_off;  // one-shot region: raw slots, gather slots, flags
   uint64_t os_raw_bytes, os_ag_bytes;       // one-shot slot strides
+  int ag_ring;         // allgather as a forwarding ring (1) or direct owner pushes (0)
   uint32_t step_segs;  // segments per published step (one release + flag per destination)
   int debug;  // development knobs (HCCX_DEBUG): 16 = warp-store pushes, 32 = synchronous tile release, 64 = log launches
 };
@@ -84,6 +85,11 @@ struct FusedParams {
 //   3 ack_rs[t]  rs[t] of the RIGHT neighbour consumed           (p-1 x kAckIdx)
 //   4 ack_ag[r]  receiver r consumed our shard in its ag slot   (p x kAckIdx)
 //   5 ack_pp[r]  receiver r consumed our pp message              (p x kAckIdx)
+//   6 ack_agl[i] RIGHT neighbour consumed its ag slot i          (p x kAckIdx)
+// A receiver acks every consumed ag slot both ways (to the shard's owner in
+// class 4, to its left neighbour in class 6), so the direct allgather (owner
+// pushes to everyone) and the ring allgather (left neighbour forwards) can
+// alternate between calls: each checks the credit its own writer needs.
 // Acks are per CTA index, not per segment: after a receiver CTA b (grid G)
 // has consumed all of its segments of a slot it acks every index b, b+G, ...
 // below kAckIdx, so each call acks the whole index space whatever its grid.
@@ -99,7 +105,7 @@ __device__ __forceinline__ uint32_t* flag_ptr(const FusedParams& P, int rank, in
     const int base[3] = {0, p - 1, 2 * p - 1};
     return f + static_cast<uint64_t>(base[cls] + slot) * P.max_seg + idx;
   }
-  const int base[3] = {0, p - 1, 2 * p - 1};
+  const int base[4] = {0, p - 1, 2 * p - 1, 3 * p - 1};
   return f + static_cast<uint64_t>(3 * p - 1) * P.max_seg + static_cast<uint64_t>(base[cls - 3] + slot) * kAckIdx +
          idx;
 }
@@ -328,6 +334,7 @@ struct Phase {
   int credit_cls;           // ack class to wait on before pushing (-1: none)
   uint32_t credit_ep;       // (pp: per destination, see credit_for)
   int ack_rank, ack_cls, ack_slot;  // consumption ack at phase end (-1: none)
+  int ack2_rank, ack2_cls, ack2_slot;  // second ack (ag slots: owner and left neighbour)
   uint32_t ack_ep;
 };
 
@@ -358,10 +365,10 @@ __device__ __forceinline__ int nphases(const FusedParams& P) {
   }
 }
 
-// Allgather ring hop k (1..p-1): shard i = j-k arrives from the left
-// neighbour in our ag slot i; decode it into `out` and, unless the right
-// neighbour owns it, forward the payload unchanged into the right
-// neighbour's ag slot i.  Every rank thus pushes (p-1)W bytes per allgather,
+// Allgather receive k (1..p-1): shard i = j-k is in our ag slot i; decode it
+// into `out`.  Ring mode (P.ag_ring): it came from the left neighbour and,
+// unless the right neighbour owns it, is forwarded unchanged into the right
+// neighbour's ag slot i.  Direct mode: its owner wrote it.  Every rank thus pushes (p-1)W bytes per allgather,
 // one W per phase, instead of (p-1)W at once from the owner (which made the
 // owner's last reduce-scatter phase NVLink-bound).  Consumption is acked to
 // the left neighbour (the writer) per slot; the credit for slot i waits on
@@ -376,15 +383,18 @@ __device__ __forceinline__ void ring_ag_hop(const FusedParams& P, Phase& f, int 
   f.wait_cls = 1;
   f.wait_slot = i;
   f.wait_ep = P.epoch;
-  f.ack_rank = (j + p - 1) % p;
+  f.ack_rank = i;  // both acks, whatever the mode (see flag classes)
   f.ack_cls = 4;
-  f.ack_slot = i;
+  f.ack_slot = j;
   f.ack_ep = P.epoch;
-  if (k < p - 1) {
+  f.ack2_rank = (j + p - 1) % p;
+  f.ack2_cls = 6;
+  f.ack2_slot = i;
+  if (P.ag_ring && k < p - 1) {
     f.push_cls = 1;
     f.push_slot = i;
     f.push_mode = 0;
-    f.credit_cls = 4;
+    f.credit_cls = 6;
     f.credit_ep = P.prev_ag;
   }
 }
@@ -412,6 +422,9 @@ __device__ __forceinline__ Phase phase_of(const FusedParams& P, int ph) {
   f.ack_cls = 0;
   f.ack_slot = 0;
   f.ack_ep = 0;
+  f.ack2_rank = -1;
+  f.ack2_cls = 0;
+  f.ack2_slot = 0;
   const int left = (j + p - 1) % p;
   if (P.op == kFAllReduce || P.op == kFReduceScatter) {
     if (ph < p) {
@@ -438,10 +451,10 @@ __device__ __forceinline__ Phase phase_of(const FusedParams& P, int ph) {
         f.kind = kPhFinAr;
         f.out = cout(j);
         f.div = true;
-        f.push_cls = 1;  // own shard starts its allgather ring: right neighbour's ag slot j
+        f.push_cls = 1;  // own shard into ag slot j: the right neighbour (ring) or everyone (direct)
         f.push_slot = j;
-        f.push_mode = 0;
-        f.credit_cls = 4;
+        f.push_mode = P.ag_ring ? 0 : 1;
+        f.credit_cls = P.ag_ring ? 6 : 4;
         f.credit_ep = P.prev_ag;
       } else {
         f.kind = kPhFinRs;
@@ -457,8 +470,8 @@ __device__ __forceinline__ Phase phase_of(const FusedParams& P, int ph) {
       f.out = P.out + static_cast<uint64_t>(j) * c;
       f.push_cls = 1;
       f.push_slot = j;
-      f.push_mode = 0;
-      f.credit_cls = 4;
+      f.push_mode = P.ag_ring ? 0 : 1;
+      f.credit_cls = P.ag_ring ? 6 : 4;
       f.credit_ep = P.prev_ag;
     } else {
       ring_ag_hop(P, f, ph, P.out + static_cast<uint64_t>((j - ph + p) % p) * c, false);
@@ -869,8 +882,10 @@ __global__ void __launch_bounds__(kFThreads2, kFCtasPerSm) ring_fused_kernel(con
         wait_event(++events);
         const uint64_t ta = clock64();
         fence_acq_rel_sys();
-        for (uint32_t kk = blockIdx.x + lane * G; kk < kAckIdx; kk += G * 32)
+        for (uint32_t kk = blockIdx.x + lane * G; kk < kAckIdx; kk += G * 32) {
           st_relaxed_sys(flag_ptr(P, f.ack_rank, f.ack_cls, f.ack_slot, 0) + kk, f.ack_ep);
+          if (f.ack2_rank >= 0) st_relaxed_sys(flag_ptr(P, f.ack2_rank, f.ack2_cls, f.ack2_slot, 0) + kk, f.ack_ep);
+        }
         c_ack += clock64() - ta;
         __syncwarp();
       }
