@@ -223,6 +223,12 @@ FusedParams base_params(hccx_comm* c, int op, uint64_t n_chunk, const float* in,
     return v > 0 ? static_cast<uint32_t>(v) : 0u;  // 0: chosen per launch (fused_launch.cuh)
   }();
   P.step_segs = step_segs;
+  static const uint32_t first_segs = [] {
+    const char* e = std::getenv("HCCX_FIRST_SEGS");
+    const int v = e ? std::atoi(e) : 0;
+    return v > 0 ? static_cast<uint32_t>(v) : 0u;  // 0: same as the step size
+  }();
+  P.first_segs = first_segs;
   // Allgather (and the allreduce's gather half) as a forwarding ring once a
   // chunk is large: the owner pushing to all p-1 peers at once makes that
   // phase NVLink-bound (measured p=4: ring wins at 64 MiB chunks, direct at

@@ -56,6 +56,7 @@ cudaError_t launch_fused_codec(const FusedParams& p, cudaStream_t stream) {
     const uint64_t s = (myseg + 2) / 3;
     q.step_segs = static_cast<uint32_t>(s < 2 ? 2 : (s > 16 ? 16 : s));
   }
+  if (q.first_segs == 0) q.first_segs = q.step_segs;
   void* args[] = {&q};
   count_launch();
   if (p.debug & 64) {

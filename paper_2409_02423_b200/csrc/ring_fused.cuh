@@ -74,6 +74,7 @@ struct FusedParams {
   uint64_t os_off, os_ag_off, os_flag_off;  // one-shot region: raw slots, gather slots, flags
   uint64_t os_raw_bytes, os_ag_bytes;       // one-shot slot strides
   int ag_ring;         // allgather as a forwarding ring (1) or direct owner pushes (0)
+  uint32_t first_segs;  // segments in the first step of every phase
   uint32_t step_segs;  // segments per published step (one release + flag per destination)
   int debug;  // development knobs (HCCX_DEBUG): 16 = warp-store pushes, 32 = synchronous tile release, 64 = log launches
 };
@@ -615,6 +616,9 @@ __global__ void __launch_bounds__(kFThreads2, kFCtasPerSm) ring_fused_kernel(con
   const bool tma_ok = Codec::kFastPath && P.vec_ok;
   auto seg_of = [&](uint32_t k) { return blockIdx.x + k * G; };
   auto seg_full = [&](uint32_t sg) { return (static_cast<uint64_t>(sg) + 1) * kSegVals <= c; };
+  // Step boundaries within a phase: a short first step (P.first_segs) so the
+  // neighbour's next phase can start early, then P.step_segs per step.
+  auto step_end = [&](uint32_t k0) { return min(k0 == 0 ? P.first_segs : k0 + P.step_segs, myseg); };
 
   if (threadIdx.x == 0) {
     for (int st = 0; st < kFMaxStages; ++st) {
@@ -647,8 +651,8 @@ __global__ void __launch_bounds__(kFThreads2, kFCtasPerSm) ring_fused_kernel(con
         // the arena is re-carved for this phase: every earlier fill must be consumed
         for (int b = 0; b < kFMaxStages; ++b) mbar_wait_to(P, &S.empty[b], ((pu >> b) & 1u) ^ 1u, 0x100u | b, S.prog);
         int st = 0;
-        for (uint32_t k0 = 0; k0 < myseg; k0 += P.step_segs) {
-          const uint32_t k1 = min(k0 + P.step_segs, myseg);
+        for (uint32_t k0 = 0, k1; k0 < myseg; k0 = k1) {
+          k1 = step_end(k0);
           if (f.wait_cls >= 0) {
             const uint64_t t0 = clock64();
             spin_ge(P, flag_ptr(P, j, f.wait_cls, f.wait_slot, seg_of(k0)), f.wait_ep, 0x700u | (ph << 4) | f.wait_cls);
@@ -737,8 +741,8 @@ __global__ void __launch_bounds__(kFThreads2, kFCtasPerSm) ring_fused_kernel(con
       }
       __syncwarp();
       c_credit += clock64() - tc;
-      for (uint32_t k0 = 0; k0 < myseg; k0 += P.step_segs) {
-        const uint32_t k1 = min(k0 + P.step_segs, myseg);
+      for (uint32_t k0 = 0, k1; k0 < myseg; k0 = k1) {
+        k1 = step_end(k0);
         for (uint32_t k = k0; k < k1; ++k) {
           const uint32_t sg = seg_of(k);
           if (lane == 0) {
@@ -864,7 +868,7 @@ __global__ void __launch_bounds__(kFThreads2, kFCtasPerSm) ring_fused_kernel(con
     for (int ph = 0; ph < nph; ++ph) {
       const Phase f = phase_of(P, ph);
       if (f.push_cls >= 0) {
-        for (uint32_t k0 = 0; k0 < myseg; k0 += P.step_segs) {
+        for (uint32_t k0 = 0; k0 < myseg; k0 = step_end(k0)) {
           wait_event(++events);
           const uint64_t ts = clock64();
           if (lane < p - 1) {
