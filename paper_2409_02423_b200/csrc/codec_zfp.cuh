@@ -25,37 +25,7 @@ namespace zfp_detail {
 
 constexpr uint32_t kNB = 0xaaaaaaaau;
 
-struct Bits128 {
-  uint64_t lo = 0, hi = 0;
-  int pos = 0;
-  __device__ __forceinline__ void put(uint64_t val, int nbits) {  // nbits <= 32, val < 2^nbits
-    if (nbits == 0) return;
-    if (pos < 64) {
-      lo |= val << pos;
-      if (pos + nbits > 64) hi |= val >> (64 - pos);
-    } else {
-      hi |= val << (pos - 64);
-    }
-    pos += nbits;
-  }
-  __device__ __forceinline__ uint64_t get(int nbits) {  // nbits <= 32
-    if (nbits == 0) return 0;
-    uint64_t v;
-    if (pos < 64) {
-      v = lo >> pos;
-      if (pos + nbits > 64) v |= hi << (64 - pos);
-    } else {
-      v = hi >> (pos - 64);
-    }
-    pos += nbits;
-    return v & ((1ull << nbits) - 1ull);
-  }
-  __device__ __forceinline__ uint64_t peek() const {  // the next 64 bits (zeros past the end)
-    if (pos == 0) return lo;
-    if (pos < 64) return (lo >> pos) | (hi << (64 - pos));
-    return pos < 128 ? hi >> (pos - 64) : 0ull;
-  }
-};
+using Bits128 = zfp_planes::Bits;
 
 __device__ __forceinline__ int32_t wadd(int32_t a, int32_t b) {
   return static_cast<int32_t>(static_cast<uint32_t>(a) + static_cast<uint32_t>(b));
@@ -108,19 +78,8 @@ __device__ __forceinline__ void encode_block(const float (&v)[4], Bits128& b, ui
   uint32_t u[4];
 #pragma unroll
   for (int i = 0; i < 4; ++i) u[i] = (static_cast<uint32_t>(q[i]) + kNB) ^ kNB;
-  // embedded coding, one bit plane per step (zfp_planes.cuh)
-  uint32_t bits = 4 * R - 9;
-  uint32_t n = 0;
-  for (int k = 31; bits && k >= 0; --k) {
-    const uint32_t x = ((u[0] >> k) & 1u) | (((u[1] >> k) & 1u) << 1) | (((u[2] >> k) & 1u) << 2) |
-                       (((u[3] >> k) & 1u) << 3);
-    uint32_t code, nn;
-    const uint32_t len = zfp_planes::plane_code(n, x, &code, &nn);
-    const uint32_t m = min(len, bits);
-    b.put(code & ((1u << m) - 1u), static_cast<int>(m));
-    bits -= m;
-    n = nn;
-  }
+  // embedded bit-plane coding (zfp_planes.cuh)
+  zfp_planes::encode_planes(u, 4 * R - 9, b);
 }
 
 template <int R>
@@ -131,17 +90,8 @@ __device__ __forceinline__ void decode_block(Bits128& b, float (&v)[4]) {
     return;
   }
   const int emax = static_cast<int>(b.get(8)) - 127;
-  uint32_t u[4] = {0, 0, 0, 0};
-  uint32_t bits = 4 * R - 9;
-  uint32_t n = 0;
-  for (int k = 31; bits && k >= 0; --k) {
-    uint32_t used;
-    const uint32_t x = zfp_planes::plane_decode(b.peek(), bits, &n, &used);
-    b.pos += static_cast<int>(used);
-    bits -= used;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) u[i] |= ((x >> i) & 1u) << k;
-  }
+  uint32_t u[4];
+  zfp_planes::decode_planes(b, 4 * R - 9, u);
   int32_t q[4];
 #pragma unroll
   for (int i = 0; i < 4; ++i) q[i] = static_cast<int32_t>((u[i] ^ kNB) - kNB);

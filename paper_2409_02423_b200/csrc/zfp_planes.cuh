@@ -17,6 +17,11 @@
 #pragma once
 #include <cstdint>
 
+#if !defined(__CUDACC__)
+#include <algorithm>
+using std::max;
+#endif
+
 #if defined(__CUDACC__)
 #define HCCX_HD __host__ __device__ __forceinline__
 #else
@@ -109,6 +114,117 @@ HCCX_HD uint32_t plane_decode(uint64_t w, uint32_t budget, uint32_t* n_io, uint3
   *used = c;
   *n_io = pos > n ? pos : n;
   return x;
+}
+
+
+// 128-bit LSB-first bit accumulator / reader (host + device).
+struct Bits {
+  uint64_t lo = 0, hi = 0;
+  int pos = 0;
+  HCCX_HD void put(uint64_t val, int nbits) {  // nbits <= 64, val < 2^nbits
+    if (nbits == 0) return;
+    if (pos < 64) {
+      lo |= val << pos;
+      if (pos + nbits > 64) hi |= val >> (64 - pos);
+    } else {
+      hi |= val << (pos - 64);
+    }
+    pos += nbits;
+  }
+  HCCX_HD uint64_t peek() const {  // the next 64 bits (zeros past the end)
+    if (pos == 0) return lo;
+    if (pos < 64) return (lo >> pos) | (hi << (64 - pos));
+    return pos < 128 ? hi >> (pos - 64) : 0ull;
+  }
+  HCCX_HD uint64_t get(int nbits) {  // nbits <= 32
+    const uint64_t v = nbits ? peek() & ((1ull << nbits) - 1ull) : 0ull;
+    pos += nbits;
+    return v;
+  }
+};
+
+HCCX_HD int top_bit(uint32_t v) {  // index of the highest set bit, -1 for 0
+#if defined(__CUDA_ARCH__)
+  return 31 - __clz(static_cast<int>(v));
+#else
+  return v ? 31 - __builtin_clz(v) : -1;
+#endif
+}
+
+HCCX_HD uint32_t plane_bits(const uint32_t (&u)[4], int k) {
+  return ((u[0] >> k) & 1u) | (((u[1] >> k) & 1u) << 1) | (((u[2] >> k) & 1u) << 2) | (((u[3] >> k) & 1u) << 3);
+}
+
+// Embedded coding of one block's negabinary coefficients with `budget` bits
+// (4R-9 after the header), same bits as the per-bit coder.  Three regimes:
+// planes above the highest set bit each cost one '0' group test (emitted as
+// a run); planes while fewer than four coefficients are significant use
+// plane_code; once all four are, every plane is its 4 bits verbatim.
+HCCX_HD void encode_planes(const uint32_t (&u)[4], uint32_t budget, Bits& b) {
+  const int G = max(max(top_bit(u[0]), top_bit(u[1])), max(top_bit(u[2]), top_bit(u[3])));
+  const uint32_t lead = static_cast<uint32_t>(31 - G);  // all-zero planes (32 when the block is zero)
+  const uint32_t e = lead < budget ? lead : budget;
+  b.pos += static_cast<int>(e);  // '0' group tests: zeros already in place
+  budget -= e;
+  int k = G;
+  uint32_t n = 0;
+  while (budget && k >= 0 && n < 4) {
+    uint32_t code, nn;
+    const uint32_t len = plane_code(n, plane_bits(u, k), &code, &nn);
+    const uint32_t m = len < budget ? len : budget;
+    b.put(code & ((1u << m) - 1u), static_cast<int>(m));
+    budget -= m;
+    n = nn;
+    --k;
+  }
+  while (budget && k >= 0) {  // verbatim planes
+    const uint32_t m = budget < 4 ? budget : 4u;
+    b.put(plane_bits(u, k) & ((1u << m) - 1u), static_cast<int>(m));
+    budget -= m;
+    --k;
+  }
+}
+
+HCCX_HD void decode_planes(Bits& b, uint32_t budget, uint32_t (&u)[4]) {
+  u[0] = u[1] = u[2] = u[3] = 0;
+  // leading all-zero planes: a run of '0' group tests
+  const uint64_t w = b.peek();
+  uint32_t lead = w ? static_cast<uint32_t>(
+#if defined(__CUDA_ARCH__)
+                          __ffsll(static_cast<long long>(w)) - 1
+#else
+                          __builtin_ctzll(w)
+#endif
+                          )
+                    : 64u;
+  if (lead > 32) lead = 32;
+  if (lead > budget) lead = budget;
+  b.pos += static_cast<int>(lead);
+  budget -= lead;
+  int k = 31 - static_cast<int>(lead);
+  uint32_t n = 0;
+  while (budget && k >= 0 && n < 4) {
+    uint32_t used;
+    const uint32_t x = plane_decode(b.peek(), budget, &n, &used);
+    b.pos += static_cast<int>(used);
+    budget -= used;
+    u[0] |= (x & 1u) << k;
+    u[1] |= ((x >> 1) & 1u) << k;
+    u[2] |= ((x >> 2) & 1u) << k;
+    u[3] |= ((x >> 3) & 1u) << k;
+    --k;
+  }
+  while (budget && k >= 0) {  // verbatim planes
+    const uint32_t m = budget < 4 ? budget : 4u;
+    const uint32_t x = static_cast<uint32_t>(b.peek()) & ((1u << m) - 1u);
+    b.pos += static_cast<int>(m);
+    budget -= m;
+    u[0] |= (x & 1u) << k;
+    u[1] |= ((x >> 1) & 1u) << k;
+    u[2] |= ((x >> 2) & 1u) << k;
+    u[3] |= ((x >> 3) & 1u) << k;
+    --k;
+  }
 }
 
 }  // namespace zfp_planes

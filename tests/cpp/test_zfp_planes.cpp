@@ -59,6 +59,28 @@ static uint32_t ref_decode(uint64_t w, uint32_t& bits, uint32_t& n, uint32_t& us
   return x;
 }
 
+// per-bit block coder (the loops of oracle/hcc_oracle.c zfp_encode_block /
+// zfp_decode_block after the header) on a Bits accumulator
+static void ref_block_encode(const uint32_t (&u)[4], uint32_t bits, Bits& b) {
+  uint32_t n = 0;
+  for (int k = 31; bits && k >= 0; --k) {
+    uint32_t x = plane_bits(u, k), code;
+    const uint32_t len = ref_encode(n, x, bits, code);
+    b.put(code, static_cast<int>(len));
+  }
+}
+
+static void ref_block_decode(Bits& b, uint32_t bits, uint32_t (&u)[4]) {
+  u[0] = u[1] = u[2] = u[3] = 0;
+  uint32_t n = 0;
+  for (int k = 31; bits && k >= 0; --k) {
+    uint32_t used;
+    const uint32_t x = ref_decode(b.peek(), bits, n, used);
+    b.pos += static_cast<int>(used);
+    for (int i = 0; i < 4; ++i) u[i] |= ((x >> i) & 1u) << k;
+  }
+}
+
 int main() {
   int fails = 0, checks = 0;
   std::mt19937_64 rng(7);
@@ -103,6 +125,35 @@ int main() {
     if (rx != dx || ru != du || rn != dn) {
       if (fails++ < 30) std::printf("random decode n=%u budget=%u w=%llx: ref %u/%u/%u new %u/%u/%u\n", n0, budget,
                                     static_cast<unsigned long long>(w), rx, ru, rn, dx, du, dn);
+    }
+  }
+  // whole blocks: random negabinary coefficients of mixed magnitudes, every budget
+  for (int t = 0; t < 60000; ++t) {
+    uint32_t u[4];
+    for (int i = 0; i < 4; ++i) {
+      const int sh = static_cast<int>(rng() % 33);
+      u[i] = sh == 32 ? 0u : static_cast<uint32_t>(rng()) >> sh;
+    }
+    const uint32_t budget = 3 + rng() % 117;  // 4R-9 for R in [3, 32]
+    Bits a, b;
+    ref_block_encode(u, budget, a);
+    encode_planes(u, budget, b);
+    ++checks;
+    if (a.lo != b.lo || a.hi != b.hi) {
+      if (fails++ < 40) std::printf("block encode u=%x,%x,%x,%x budget %u\n", u[0], u[1], u[2], u[3], budget);
+      continue;
+    }
+    // decode the stream plus random trailing garbage past the budget
+    Bits s1, s2;
+    s1.lo = s2.lo = a.lo;
+    s1.hi = s2.hi = a.hi;
+    uint32_t r[4], d[4];
+    ref_block_decode(s1, budget, r);
+    decode_planes(s2, budget, d);
+    ++checks;
+    if (r[0] != d[0] || r[1] != d[1] || r[2] != d[2] || r[3] != d[3] || s1.pos != s2.pos) {
+      if (fails++ < 40) std::printf("block decode u=%x,%x,%x,%x budget %u: ref pos %d new pos %d\n", u[0], u[1], u[2], u[3],
+                                    budget, s1.pos, s2.pos);
     }
   }
   std::printf("zfp plane coder: %d checks, %d failures\n", checks, fails);
