@@ -19,7 +19,9 @@
 //           starts (fallback chunks cost O(1)); then one warp per chunk
 //           decodes in parallel from the recovered offsets.
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
+#include <vector>
 
 #include "device_common.cuh"
 #include "hccx.h"
@@ -246,6 +248,72 @@ __global__ void ll_walk_kernel(const uint8_t* __restrict__ in, uint64_t in_bytes
   offsets[nchunks] = pos;
 }
 
+// decompress (a'): the same offsets by pointer doubling.  J0[x] = the bit
+// position after the code starting at bit x (S+1 when it would run past the
+// S-bit stream; S+1 is absorbing).  Twelve rounds of J <- J o J give
+// J12[x] = the position after 4096 codes, so a coded chunk starting at byte
+// B ends at byte ceil(J12[8B] / 8): the serial walk shrinks to one lookup
+// per chunk.  Every position of the stream is a candidate start because the
+// chunk starts are unknown; 8 bytes of table per stream bit.
+__global__ void ll_jump0_kernel(const uint8_t* __restrict__ in, uint64_t in_bytes, uint32_t S,
+                                uint32_t* __restrict__ J) {
+  const uint64_t total = static_cast<uint64_t>(S) + 2;
+  for (uint64_t x = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; x < total;
+       x += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    uint32_t nx = S + 1;
+    if (x + 5 <= S) {
+      const uint64_t B = x >> 3;
+      uint32_t w = __ldg(in + B);
+      if (B + 1 < in_bytes) w |= static_cast<uint32_t>(__ldg(in + B + 1)) << 8;
+      const uint64_t e = x + 37 - ((w >> (x & 7)) & 31u);
+      if (e <= S) nx = static_cast<uint32_t>(e);
+    }
+    J[x] = nx;
+  }
+}
+
+__global__ void ll_jump_kernel(const uint32_t* __restrict__ Jin, uint32_t* __restrict__ Jout, uint64_t total) {
+  for (uint64_t x = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; x < total;
+       x += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    Jout[x] = Jin[Jin[x]];
+}
+
+__global__ void ll_walk_jump_kernel(const uint8_t* __restrict__ in, uint64_t in_bytes, uint64_t n, uint64_t nchunks,
+                                    const uint32_t* __restrict__ J12, uint32_t S, uint64_t* __restrict__ offsets,
+                                    uint32_t* __restrict__ err) {
+  if (threadIdx.x != 0) return;
+  uint64_t pos = (nchunks + 7) / 8;
+  const uint64_t end_bit = 8 * in_bytes;
+  for (uint64_t c = 0; c < nchunks; ++c) {
+    offsets[c] = pos;
+    const uint32_t live = static_cast<uint32_t>(n - c * kChunk < kChunk ? n - c * kChunk : kChunk);
+    if ((__ldg(in + c / 8) >> (c % 8)) & 1u) {
+      pos += 4ull * live;
+    } else if (live == kChunk) {
+      const uint32_t b = J12[8 * pos <= S ? 8 * pos : static_cast<uint64_t>(S) + 1];
+      pos = b > S ? in_bytes + 1 : (static_cast<uint64_t>(b) + 7) / 8;
+    } else {  // the short last chunk: walk it
+      uint64_t bit = pos * 8;
+      for (uint32_t i = 0; i < live && bit <= end_bit; ++i) {
+        if (bit + 5 > end_bit) {
+          bit = end_bit + 1;
+          break;
+        }
+        const uint64_t B = bit >> 3;
+        uint32_t w = __ldg(in + B);
+        if (B + 1 < in_bytes) w |= static_cast<uint32_t>(__ldg(in + B + 1)) << 8;
+        bit += 5 + (32 - ((w >> (bit & 7)) & 31u));
+      }
+      pos = bit > end_bit ? in_bytes + 1 : (bit + 7) / 8;
+    }
+    if (pos > in_bytes) {
+      atomicOr(err, 8u);
+      pos = in_bytes;
+    }
+  }
+  offsets[nchunks] = pos;
+}
+
 // decompress (b): raw chunks, one warp per chunk (coalesced copies)
 __global__ void __launch_bounds__(kLLWarps * 32) ll_raw_kernel(const uint8_t* __restrict__ in, uint64_t in_bytes,
                                                                uint64_t n, uint64_t nchunks,
@@ -323,7 +391,11 @@ struct Scratch {
   uint64_t* offsets = nullptr;
   uint32_t* err = nullptr;
   uint64_t cap = 0;
+  uint32_t* jump[2] = {nullptr, nullptr};  // pointer-doubling tables
+  uint64_t jump_cap = 0;
   ~Scratch() {
+    cudaFree(jump[0]);
+    cudaFree(jump[1]);
     cudaFree(sizes);
     cudaFree(fallback);
     cudaFree(offsets);
@@ -341,6 +413,22 @@ struct Scratch {
       return HCCX_ERR_CUDA;
     cap = c;
     return HCCX_OK;
+  }
+  bool ensure_jump(uint64_t entries) {
+    if (entries <= jump_cap) return true;
+    cudaFree(jump[0]);
+    cudaFree(jump[1]);
+    jump[0] = jump[1] = nullptr;
+    jump_cap = 0;
+    if (cudaMalloc(&jump[0], 4 * entries) != cudaSuccess || cudaMalloc(&jump[1], 4 * entries) != cudaSuccess) {
+      cudaFree(jump[0]);
+      cudaFree(jump[1]);
+      jump[0] = jump[1] = nullptr;
+      cudaGetLastError();  // clear the allocation failure: fall back to the serial walk
+      return false;
+    }
+    jump_cap = entries;
+    return true;
   }
 };
 
@@ -411,7 +499,32 @@ extern "C" hccx_status_t hccx_lossless_decompress(const uint8_t* d_in, uint64_t 
   hccx_status_t r = t_scratch.ensure(nch);
   if (r != HCCX_OK) return r;
   cudaMemsetAsync(t_scratch.err, 0, 4, st);
-  ll_walk_kernel<<<1, 32, 0, st>>>(d_in, in_bytes, n, nch, t_scratch.offsets, t_scratch.err);
+  // Offsets: pointer doubling over the whole stream when there are many
+  // full chunks and the tables fit (8 bytes per stream bit), else the
+  // serial walk (cheap for all-raw payloads: O(1) per raw chunk).
+  const uint64_t S = 8 * in_bytes;
+  bool jump = nch >= 64 && S + 2 < (1ull << 32) && std::getenv("HCCX_LL_SERIAL") == nullptr;
+  if (jump) {  // worth it only with many coded chunks: count them from the flag bytes
+    std::vector<uint8_t> flags((nch + 7) / 8);
+    if (cudaMemcpyAsync(flags.data(), d_in, flags.size(), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess)
+      return HCCX_ERR_CUDA;
+    uint64_t raw = 0;
+    for (uint64_t c = 0; c < nch; ++c) raw += (flags[c / 8] >> (c % 8)) & 1u;
+    jump = nch - raw >= 64 && t_scratch.ensure_jump(S + 2);
+  }
+  if (jump) {
+    const int g = 148 * 8;
+    ll_jump0_kernel<<<g, 256, 0, st>>>(d_in, in_bytes, static_cast<uint32_t>(S), t_scratch.jump[0]);
+    int cur = 0;
+    for (int r = 0; r < 12; ++r, cur ^= 1)
+      ll_jump_kernel<<<g, 256, 0, st>>>(t_scratch.jump[cur], t_scratch.jump[cur ^ 1], S + 2);
+    ll_walk_jump_kernel<<<1, 32, 0, st>>>(d_in, in_bytes, n, nch, t_scratch.jump[cur], static_cast<uint32_t>(S),
+                                          t_scratch.offsets, t_scratch.err);
+    count_launch(13);
+  } else {
+    ll_walk_kernel<<<1, 32, 0, st>>>(d_in, in_bytes, n, nch, t_scratch.offsets, t_scratch.err);
+  }
   ll_raw_kernel<<<grid_for(nch, kLLWarps), kLLWarps * 32, 0, st>>>(d_in, in_bytes, n, nch, t_scratch.offsets, d_out);
   ll_decode_kernel<<<static_cast<unsigned>((nch + 127) / 128), 128, 0, st>>>(d_in, in_bytes, n, nch, t_scratch.offsets,
                                                                           d_out);
