@@ -70,7 +70,7 @@ static_assert(sizeof(HandleBlob) <= HCCX_HANDLE_BYTES, "handle blob too large");
 uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
 
 constexpr uint64_t kOneShotMaxChunk = 1ull << 21;         // values per chunk the one-shot slots hold
-constexpr uint64_t kOneShotDefaultBytes = 1ull << 24;     // allreduce bytes per rank routed one-shot
+constexpr uint64_t kOneShotBytesPerRank = 4ull << 20;    // one-shot allreduce up to p x this many bytes
 
 uint64_t timeout_ns() {
   const char* e = std::getenv("HCCX_TIMEOUT_MS");
@@ -259,11 +259,15 @@ hccx_status_t check_comm(hccx_comm* c, hccx_codec_t codec) {
 // HCCX_ONESHOT_BYTES (bytes per rank, default below; 0 disables it), the
 // fused ring above.  Both give the reference's bits.
 bool use_oneshot(const hccx_comm* c, uint64_t n) {
-  static const uint64_t limit = [] {
+  // default: 4 MiB per rank per peer count (16 MiB at p = 4, measured
+  // crossover; the ring's 2(p-1) dependent rounds grow with p while the
+  // one-shot path keeps two)
+  static const int64_t limit = [] {
     const char* e = std::getenv("HCCX_ONESHOT_BYTES");
-    return e ? std::strtoull(e, nullptr, 10) : kOneShotDefaultBytes;
+    return e ? static_cast<int64_t>(std::strtoull(e, nullptr, 10)) : int64_t{-1};
   }();
-  return 4 * n <= limit && n / c->p <= c->os_cap;
+  const uint64_t lim = limit >= 0 ? static_cast<uint64_t>(limit) : kOneShotBytesPerRank * c->p;
+  return 4 * n <= lim && n / c->p <= c->os_cap;
 }
 
 hccx_status_t run(hccx_comm* c, hccx_codec_t codec, const FusedParams& P, cudaStream_t s) {
