@@ -290,8 +290,14 @@ constexpr int kFMaxStages = 8;                      // input ring depth cap (mba
 constexpr uint32_t kFArena = 6144u * kFusedWarps;    // input ring bytes, carved per phase
 constexpr int kFMaxTiles = 8;                        // output (push) ring depth cap
 constexpr uint32_t kFTileBudget = 2176u * kFusedWarps;  // output ring bytes
-constexpr int kFReadsInFlight = 4;                   // bulk pushes whose smem read may be pending
-constexpr uint32_t kFPrefetch = 4;                   // L2 prefetch distance (segments)
+#ifndef HCCX_READS_IN_FLIGHT
+#define HCCX_READS_IN_FLIGHT 4
+#endif
+#ifndef HCCX_PREFETCH_SEGS
+#define HCCX_PREFETCH_SEGS 4
+#endif
+constexpr int kFReadsInFlight = HCCX_READS_IN_FLIGHT;  // bulk pushes whose smem read may be pending
+constexpr uint32_t kFPrefetch = HCCX_PREFETCH_SEGS;  // L2 prefetch distance (segments)
 constexpr int kFCompute = kFusedWarps;               // compute warps
 constexpr int kFThreads2 = (kFCompute + 3) * 32;     // + producer, pusher and signaller warps
 constexpr uint32_t kFGenBytes = kFCompute * kStageBytes;
