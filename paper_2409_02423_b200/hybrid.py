@@ -177,26 +177,21 @@ class HybridComm:
         spec = self.scheme.at(CommPath.PpP2p)
         out, ev = self._timed(lambda: g.comm.p2p(x, src_stage, dst_stage, spec))
         me = g.ranks.index(self.rank)
-        if self._lossless(spec):
-            wire = self._p2p_lossless_wire(g, x, src_stage)
-        else:
-            wire = wire_size_bytes(spec, x.numel())
         if me in (src_stage, dst_stage):
+            if self._lossless(spec):
+                wire = self._p2p_lossless_wire(g, x, out, src_stage)
+            else:
+                wire = wire_size_bytes(spec, x.numel())
             self._record(CommPath.PpP2p, CollectiveKind.P2P, 2, 4 * x.numel(), wire, 1, ev)
         return out
 
-    def _p2p_lossless_wire(self, g, x, src_stage: int) -> int:
-        """The sender sizes its payload; the chain learns it by broadcast."""
-        import torch
-        import torch.distributed as dist
-
+    def _p2p_lossless_wire(self, g, x, out, src_stage: int) -> int:
+        """The payload size of dec(comp(x)) == x (the codec is transparent):
+        the source sizes its input, the destination what it received."""
         from . import lossless
 
-        torch.cuda.synchronize()
         me = g.ranks.index(self.rank)
-        w = torch.tensor([lossless.size(x) if me == src_stage else 0], dtype=torch.int64, device=x.device)
-        dist.broadcast(w, g.ranks[src_stage], group=g.pg)
-        return int(w.item())
+        return lossless.size(x if me == src_stage else out)
 
     def zero_reduce_scatter(self, grad):
         """ZeRO-1 gradient reduce-scatter over the DP group (Zero1ReduceScatter)."""

@@ -89,6 +89,9 @@ TRAIN_CASES = [  # (name, cfg overrides, dp, pp, tp, scheme, zero: 0 off / 1 rep
     ("dp2_zfp8_replace", {"steps": 5}, 2, 1, 1, "naive-zfp8", 1),
     ("pp2tp2_zhyb_off", {}, 1, 2, 2, "z-hybrid:16,4", 0),
     ("diverge_zfp8", {"steps": 20, "learning_rate": 1e30}, 2, 1, 1, "naive-zfp8", 0),
+    ("dp2pp2_mzhyb_off", {}, 2, 2, 1, "mz-hybrid:8", 0),
+    ("tp2_zhyb_off", {}, 1, 1, 2, "z-hybrid:16,8", 0),
+    ("dp2tp2_mpc_replace", {}, 2, 1, 2, "naive-mpc", 1),
 ]
 
 
