@@ -41,3 +41,15 @@ def test_trainer_across_processes_matches_reference():
                        timeout=900)
     print(r.stdout[-4000:], r.stderr[-4000:])
     assert r.returncode == 0 and "TRAINER DIST PARITY OK" in r.stdout
+
+
+@pytest.mark.skipif(_ngpus() < 2, reason="needs >= 2 GPUs")
+def test_nvlink_randomized_soak():
+    """Random ops / sizes / codecs back to back (tests/nvlink_soak.py)."""
+    n = min(_ngpus(), 8)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes", "1", "--nproc-per-node", str(n),
+           "--master-addr", "127.0.0.1", "--master-port", "29619", os.path.join(ROOT, "tests", "nvlink_soak.py")]
+    r = subprocess.run(cmd, cwd=ROOT, env=dict(os.environ, SOAK_ITERS="80", HCCX_TIMEOUT_MS="20000"),
+                       capture_output=True, text=True, timeout=900)
+    print(r.stdout[-4000:], r.stderr[-4000:])
+    assert r.returncode == 0 and "NVLINK SOAK OK" in r.stdout
