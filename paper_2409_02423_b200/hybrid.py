@@ -75,7 +75,8 @@ class HybridComm:
                 if self.rank in ranks:
                     comm = NvlinkComm(max_n, group=pg) if len(ranks) > 1 else None
                     self.groups[kind] = _Group(ranks, pg, comm)
-        self.trace: List[TraceEvent] = []
+        self._trace: List[TraceEvent] = []
+        self._pending: list = []
         self.step = 0
 
     # ---------------------------------------------------------------- utils
@@ -90,11 +91,32 @@ class HybridComm:
         return out, (a, b)
 
     def _record(self, path, kind, size, raw, wire, rounds, ev):
-        a, b = ev
-        b.synchronize()
+        """Queue the event; its device time is read when ``trace`` is next
+        accessed, so back-to-back calls are not serialised by the host.
+        Data-dependent (lossless) byte counts are taken now."""
         if callable(wire):
+            ev[1].synchronize()
             wire = wire()
-        self.trace.append(TraceEvent(self.step, path, kind, size, raw, wire, a.elapsed_time(b) / 1e3, rounds))
+        self._pending.append((self.step, path, kind, size, raw, wire, rounds, ev))
+
+    def last_bytes(self):
+        """(path, raw_bytes, wire_bytes) of the most recent event, without
+        waiting for its device time."""
+        if self._pending:
+            e = self._pending[-1]
+            return e[1], e[4], e[5]
+        if self._trace:
+            e = self._trace[-1]
+            return e.path, e.raw_bytes, e.wire_bytes
+        return None
+
+    @property
+    def trace(self) -> List[TraceEvent]:
+        for step, path, kind, size, raw, wire, rounds, (a, b) in self._pending:
+            b.synchronize()
+            self._trace.append(TraceEvent(step, path, kind, size, raw, wire, a.elapsed_time(b) / 1e3, rounds))
+        self._pending = []
+        return self._trace
 
     @staticmethod
     def _lossless(spec) -> bool:

@@ -80,10 +80,11 @@ class DistTrainer3D:
     def _tally(self, leader: bool) -> None:
         """Count a collective once (the reference records one event per
         call): the group's first rank, or the p2p source."""
-        if leader and self.hc.trace:
-            e = self.hc.trace[-1]
-            self.bytes[e.path][0] += e.raw_bytes
-            self.bytes[e.path][1] += e.wire_bytes
+        last = self.hc.last_bytes() if leader else None
+        if last:
+            path, raw, wire = last
+            self.bytes[path][0] += raw
+            self.bytes[path][1] += wire
 
     def _tp_allreduce(self, y: np.ndarray) -> np.ndarray:
         out = self.hc.tp_allreduce(self._dev(y))
