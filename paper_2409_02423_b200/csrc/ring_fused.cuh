@@ -272,16 +272,19 @@ __device__ __forceinline__ void fused_group(const FusedParams& P, const uint8_t*
 // ---------------------------------------------------------------------------
 // Warp-specialised fused kernel.
 //
-// CTA = 8 compute warps + 1 producer warp.  The collective is a list of
-// *phases* (ring rounds, allgather receives, ...; see phase_of) that both
-// roles walk in the same order.  The producer's elected lane waits for each
-// step's inbound-data flag, then streams every segment's inputs (inbox
-// payload and/or local fp32) into a per-phase carved (up to kFMaxStages deep) shared-memory ring with
-// cp.async.bulk (completing on the stage's "full" mbarrier).  Compute warps
-// decode / add / encode one group each per segment straight from shared
-// memory, release the stage ("empty" mbarrier), stage the encoded segment in
-// `tile` and push it to the peer window(s) with 16-byte stores.  HBM latency
-// is therefore hidden behind several segments of prefetch per CTA.
+// One CTA per SM: kFCompute (24) compute warps + a producer, a pusher and a
+// signaller warp.  The collective is a list of *phases* (ring rounds,
+// allgather receives, ...; see phase_of) that every role walks in the same
+// order.  The producer's elected lane waits for each step's inbound-data
+// flag, then streams every segment's inputs (inbox payload and/or local
+// fp32) into a per-phase carved (up to kFMaxStages deep) shared-memory ring
+// with cp.async.bulk (completing on the stage's "full" mbarrier).  Compute
+// warps decode / add / encode one group each per segment straight from
+// shared memory, release the stage ("empty" mbarrier) and stage the encoded
+// segment in a tile; the pusher hands tiles to the TMA engine (bulk stores
+// into the peer's window); the signaller publishes completed steps and
+// consumption acks with system-scope releases.  HBM latency is hidden
+// behind several segments of prefetch per CTA.
 // Partial segments (and unaligned buffers / non-word codecs) are read
 // directly from global memory instead ("direct" stages).
 // ---------------------------------------------------------------------------
