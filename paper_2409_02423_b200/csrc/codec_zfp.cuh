@@ -53,16 +53,18 @@ __device__ __forceinline__ void inv_lift(int32_t& x, int32_t& y, int32_t& z, int
   w = wadd(w, x); x = wshl1(x); x = wsub(x, w);
 }
 
-// One 4-value block -> exactly 4R bits (LSB-first) in b.
+// Block prologue: header (zero flag, biased emax) into b, the negabinary
+// coefficients into u; returns the bit-plane budget (0 for a zero block).
 template <int R>
-__device__ __forceinline__ void encode_block(const float (&v)[4], Bits128& b, uint32_t& bad) {
+__device__ __forceinline__ uint32_t encode_head(const float (&v)[4], Bits128& b, uint32_t& bad, uint32_t (&u)[4]) {
   uint32_t fmax = 0;
 #pragma unroll
   for (int i = 0; i < 4; ++i) fmax = max(fmax, __float_as_uint(v[i]) & 0x7fffffffu);
   bad |= static_cast<uint32_t>(fmax >= 0x7f800000u);
   if (fmax == 0) {
     b.put(0, 1);
-    return;
+    u[0] = u[1] = u[2] = u[3] = 0;
+    return 0;
   }
   const int f = static_cast<int>(fmax >> 23);
   const int emax = max(f - 126, -126);  // frexp exponent of the block max, clamped
@@ -75,23 +77,34 @@ __device__ __forceinline__ void encode_block(const float (&v)[4], Bits128& b, ui
 #pragma unroll
   for (int i = 0; i < 4; ++i) q[i] = __float2int_rz(__fmul_rn(__fmul_rn(v[i], s1), s2));
   fwd_lift(q[0], q[1], q[2], q[3]);
-  uint32_t u[4];
 #pragma unroll
   for (int i = 0; i < 4; ++i) u[i] = (static_cast<uint32_t>(q[i]) + kNB) ^ kNB;
-  // embedded bit-plane coding (zfp_planes.cuh)
-  zfp_planes::encode_planes(u, 4 * R - 9, b);
+  return 4 * R - 9;
 }
 
+// Two blocks -> 4R bits each: prologues, then both embedded codings in one
+// loop (zfp_planes.cuh steppers).
 template <int R>
-__device__ __forceinline__ void decode_block(Bits128& b, float (&v)[4]) {
-  if (!b.get(1)) {
+__device__ __forceinline__ void encode_pair(const float (&a)[4], const float (&c)[4], Bits128& b0, Bits128& b1,
+                                            uint32_t& bad) {
+  uint32_t ua[4], uc[4];
+  const uint32_t ba = encode_head<R>(a, b0, bad, ua);
+  const uint32_t bc = encode_head<R>(c, b1, bad, uc);
+  zfp_planes::PlaneEnc e0, e1;
+  e0.init(ua, ba, b0);
+  e1.init(uc, bc, b1);
+  while (e0.active() || e1.active()) {
+    if (e0.active()) e0.step(b0);
+    if (e1.active()) e1.step(b1);
+  }
+}
+
+__device__ __forceinline__ void finish_block(const uint32_t (&u)[4], int emax, bool zero, float (&v)[4]) {
+  if (zero) {
 #pragma unroll
     for (int i = 0; i < 4; ++i) v[i] = 0.0f;
     return;
   }
-  const int emax = static_cast<int>(b.get(8)) - 127;
-  uint32_t u[4];
-  zfp_planes::decode_planes(b, 4 * R - 9, u);
   int32_t q[4];
 #pragma unroll
   for (int i = 0; i < 4; ++i) q[i] = static_cast<int32_t>((u[i] ^ kNB) - kNB);
@@ -101,6 +114,23 @@ __device__ __forceinline__ void decode_block(Bits128& b, float (&v)[4]) {
   for (int i = 0; i < 4; ++i) v[i] = __double2float_rn(__dmul_rn(static_cast<double>(q[i]), s));
 }
 
+// Decode two blocks: headers, both embedded codings in one loop, then the
+// inverse transform of each.
+template <int R>
+__device__ __forceinline__ void decode_pair(Bits128& b0, Bits128& b1, float (&a)[4], float (&c)[4]) {
+  const bool z0 = !b0.get(1), z1 = !b1.get(1);
+  const int e0 = z0 ? 0 : static_cast<int>(b0.get(8)) - 127;
+  const int e1 = z1 ? 0 : static_cast<int>(b1.get(8)) - 127;
+  zfp_planes::PlaneDec d0, d1;
+  d0.init(b0, z0 ? 0u : 4u * R - 9u);
+  d1.init(b1, z1 ? 0u : 4u * R - 9u);
+  while (d0.active() || d1.active()) {
+    if (d0.active()) d0.step(b0);
+    if (d1.active()) d1.step(b1);
+  }
+  finish_block(d0.u, e0, z0, a);
+  finish_block(d1.u, e1, z1, c);
+}
 }  // namespace zfp_detail
 
 template <int R>
@@ -138,8 +168,7 @@ struct ZfpRateCodec {
     }
     pad(a, min(lane_live, 4u));
     pad(c, lane_live > 4 ? lane_live - 4 : 0u);
-    zfp_detail::encode_block<R>(a, b0, bad);
-    zfp_detail::encode_block<R>(c, b1, bad);
+    zfp_detail::encode_pair<R>(a, c, b0, b1, bad);
     // chunk = b0 (4R bits) | b1 << 4R
     constexpr int S = 4 * R;
     uint64_t c0 = b0.lo, c1 = b0.hi, c2 = 0, c3 = 0;
@@ -187,8 +216,7 @@ struct ZfpRateCodec {
     }
     // mask block 0 to its 4R bits (decoder never reads past them, but keep it clean)
     float a[4], c[4];
-    zfp_detail::decode_block<R>(b0, a);
-    zfp_detail::decode_block<R>(b1, c);
+    zfp_detail::decode_pair<R>(b0, b1, a, c);
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       v[i] = a[i];

@@ -227,5 +227,78 @@ HCCX_HD void decode_planes(Bits& b, uint32_t budget, uint32_t (&u)[4]) {
   }
 }
 
+
+// Steppers for coding two blocks in one loop (a lane owns two blocks: the
+// joint loop runs max(planes) iterations instead of their sum and gives the
+// two independent dependency chains to the scheduler side by side).  Same
+// bits as encode_planes / decode_planes.
+struct PlaneEnc {
+  uint32_t u[4];
+  uint32_t budget, n;
+  int k;
+  HCCX_HD void init(const uint32_t (&uu)[4], uint32_t bud, Bits& b) {
+    u[0] = uu[0], u[1] = uu[1], u[2] = uu[2], u[3] = uu[3];
+    const int G = max(max(top_bit(u[0]), top_bit(u[1])), max(top_bit(u[2]), top_bit(u[3])));
+    const uint32_t lead = static_cast<uint32_t>(31 - G);
+    const uint32_t e = lead < bud ? lead : bud;
+    b.pos += static_cast<int>(e);
+    budget = bud - e;
+    k = G;
+    n = 0;
+  }
+  HCCX_HD bool active() const { return budget != 0 && k >= 0; }
+  HCCX_HD void step(Bits& b) {
+    const uint32_t x = plane_bits(u, k);
+    uint32_t code = x, nn = 4, len = 4;  // all significant: verbatim plane
+    if (n < 4) len = plane_code(n, x, &code, &nn);
+    const uint32_t m = len < budget ? len : budget;
+    b.put(code & ((1u << m) - 1u), static_cast<int>(m));
+    budget -= m;
+    n = nn;
+    --k;
+  }
+};
+
+struct PlaneDec {
+  uint32_t u[4];
+  uint32_t budget, n;
+  int k;
+  HCCX_HD void init(Bits& b, uint32_t bud) {
+    u[0] = u[1] = u[2] = u[3] = 0;
+    const uint64_t w = b.peek();
+    uint32_t lead = w ? static_cast<uint32_t>(
+#if defined(__CUDA_ARCH__)
+                            __ffsll(static_cast<long long>(w)) - 1
+#else
+                            __builtin_ctzll(w)
+#endif
+                            )
+                      : 64u;
+    if (lead > 32) lead = 32;
+    if (lead > bud) lead = bud;
+    b.pos += static_cast<int>(lead);
+    budget = bud - lead;
+    k = 31 - static_cast<int>(lead);
+    n = 0;
+  }
+  HCCX_HD bool active() const { return budget != 0 && k >= 0; }
+  HCCX_HD void step(Bits& b) {
+    uint32_t used, x;
+    if (n == 4) {
+      used = budget < 4 ? budget : 4u;
+      x = static_cast<uint32_t>(b.peek()) & ((1u << used) - 1u);
+    } else {
+      x = plane_decode(b.peek(), budget, &n, &used);
+    }
+    b.pos += static_cast<int>(used);
+    budget -= used;
+    u[0] |= (x & 1u) << k;
+    u[1] |= ((x >> 1) & 1u) << k;
+    u[2] |= ((x >> 2) & 1u) << k;
+    u[3] |= ((x >> 3) & 1u) << k;
+    --k;
+  }
+};
+
 }  // namespace zfp_planes
 }  // namespace hccx
