@@ -165,16 +165,22 @@ def bench_allreduce_main(args, metric, ClockSampler, peaks, traffic_for, cpu_all
     s = torch.cuda.current_stream()
 
     def timed(fn, steps):
+        import gc
+
         t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()  # no fused kernel may be in flight across an NCCL call
         dist.barrier()
         torch.cuda.synchronize()
-        torch.cuda._sleep(int(1e6))
-        t0.record(s)
-        for _ in range(steps):
-            fn()
-        t1.record(s)
-        torch.cuda.synchronize()
+        gc.disable()  # a collection pause on one rank's host would stall every peer
+        try:
+            torch.cuda._sleep(int(1e6))
+            t0.record(s)
+            for _ in range(steps):
+                fn()
+            t1.record(s)
+            torch.cuda.synchronize()
+        finally:
+            gc.enable()
         ms = torch.tensor([t0.elapsed_time(t1) / steps], device="cuda")
         dist.all_reduce(ms, op=dist.ReduceOp.MAX)
         return float(ms.item())
