@@ -243,9 +243,62 @@ HCCX_API hccx_status_t hccx_comm_status(hccx_comm_t c, void* stream);
 
 /* Timeline of CTA 0 of the fused kernel (development / performance
  * analysis: ncu cannot replay a multi-rank kernel).  capacity in 64-bit
- * words (0 disables).  Read returns [count, (tag, t_ns) x count]. */
+ * words: 0 disables, otherwise at least 17408 (the fixed slots: wait-chain
+ * log at 4000, role accumulators at 4096, per-CTA times at 8192/16384), else
+ * HCCX_ERR_INVALID_ARGUMENT.  Read returns [count, (tag, t_ns) x count]. */
 HCCX_API hccx_status_t hccx_comm_trace_enable(hccx_comm_t c, uint64_t capacity);
 HCCX_API hccx_status_t hccx_comm_trace_read(hccx_comm_t c, uint64_t* host, uint64_t max_words, uint64_t* words);
+
+/* -------------------------------------- single-process communicator -- */
+/* All p members of a communicator in ONE process: the shape of the
+ * reference's all-members-in-one-call collectives (collectives.hpp:23-25;
+ * SURVEY.md §8(b) "hccx_comm_create(ndev, devices)").  devices[j] is member
+ * j's GPU (ring order = member order).  Members on distinct GPUs exchange
+ * compressed segments over NVLink through peer access, with the same fused
+ * kernel as the multi-process communicator; members sharing a GPU run as
+ * virtual ranks of one cooperative launch (bit-identical, used for 1-GPU
+ * testing of the NVLink kernel).  Device pointers d_*[j] live on devices[j];
+ * streams[j] (nullable array) is member j's stream -- members sharing a GPU
+ * run on the stream of the first such member.  p in [1,16].  Semantics and
+ * errors as the group calls above. */
+
+typedef struct hccx_mcomm* hccx_mcomm_t;
+
+HCCX_API hccx_status_t hccx_mcomm_create(int nmembers, const int* devices, uint64_t max_n, hccx_mcomm_t* out);
+HCCX_API hccx_status_t hccx_mcomm_destroy(hccx_mcomm_t m);
+HCCX_API int hccx_mcomm_size(hccx_mcomm_t m);
+/* Replaces hcc::allreduce (collectives.hpp:61-64, src/collectives.cpp:202-248). */
+HCCX_API hccx_status_t hccx_mcomm_allreduce(hccx_mcomm_t m, const float* const* d_in, float* const* d_out,
+                                            uint64_t n, hccx_codec_t codec, int mode, void* const* streams);
+/* Replaces hcc::ring_reduce_scatter (collectives.hpp:51-55, src/collectives.cpp:154-181). */
+HCCX_API hccx_status_t hccx_mcomm_reduce_scatter(hccx_mcomm_t m, const float* const* d_in, float* const* d_shard,
+                                                 uint64_t n, hccx_codec_t codec, void* const* streams);
+/* Replaces hcc::ring_allgather (collectives.hpp:57-59, src/collectives.cpp:183-200). */
+HCCX_API hccx_status_t hccx_mcomm_allgather(hccx_mcomm_t m, const float* const* d_shard, float* const* d_out,
+                                            uint64_t shard_n, hccx_codec_t codec, void* const* streams);
+/* Broadcast (NOT in the reference); d_in on devices[root]. */
+HCCX_API hccx_status_t hccx_mcomm_broadcast(hccx_mcomm_t m, int root, const float* d_in, float* const* d_out,
+                                            uint64_t n, hccx_codec_t codec, void* const* streams);
+/* Replaces hcc::p2p (collectives.hpp:45-48, src/collectives.cpp:130-152):
+ * d_in on devices[src], d_out on devices[dst] = dec(comp(d_in)). */
+HCCX_API hccx_status_t hccx_mcomm_p2p(hccx_mcomm_t m, int src, int dst, const float* d_in, float* d_out,
+                                      uint64_t n, hccx_codec_t codec, void* const* streams);
+/* Synchronise every member's stream and report the first error flag. */
+HCCX_API hccx_status_t hccx_mcomm_status(hccx_mcomm_t m, void* const* streams);
+/* Host-buffer variants (the reference's value semantics): device buffers are
+ * cached in the communicator; *device_seconds (nullable) = device time of
+ * the collective. */
+HCCX_API hccx_status_t hccx_mcomm_allreduce_host(hccx_mcomm_t m, const float* const* h_in, float* const* h_out,
+                                                 uint64_t n, hccx_codec_t codec, int mode, double* device_seconds);
+HCCX_API hccx_status_t hccx_mcomm_reduce_scatter_host(hccx_mcomm_t m, const float* const* h_in,
+                                                      float* const* h_shard, uint64_t n, hccx_codec_t codec,
+                                                      double* device_seconds);
+HCCX_API hccx_status_t hccx_mcomm_allgather_host(hccx_mcomm_t m, const float* const* h_shard, float* const* h_out,
+                                                 uint64_t shard_n, hccx_codec_t codec, double* device_seconds);
+HCCX_API hccx_status_t hccx_mcomm_broadcast_host(hccx_mcomm_t m, int root, const float* h_in, float* const* h_out,
+                                                 uint64_t n, hccx_codec_t codec, double* device_seconds);
+HCCX_API hccx_status_t hccx_mcomm_p2p_host(hccx_mcomm_t m, int src, int dst, const float* h_in, float* h_out,
+                                           uint64_t n, hccx_codec_t codec, double* device_seconds);
 
 /* Kernel launches issued by this library since it was loaded. */
 HCCX_API uint64_t hccx_launch_count(void);

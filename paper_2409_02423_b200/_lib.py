@@ -87,6 +87,21 @@ hccx_p2p = _sig("hccx_p2p", _st, _p, C.c_int, C.c_int, _p, _p, _u64, Codec, _p)
 hccx_comm_status = _sig("hccx_comm_status", _st, _p, _p)
 hccx_comm_trace_enable = _sig("hccx_comm_trace_enable", _st, _p, _u64)
 hccx_comm_trace_read = _sig("hccx_comm_trace_read", _st, _p, C.POINTER(_u64), _u64, C.POINTER(_u64))
+_ip = C.POINTER(C.c_int)
+hccx_mcomm_create = _sig("hccx_mcomm_create", _st, C.c_int, _ip, _u64, C.POINTER(_p))
+hccx_mcomm_destroy = _sig("hccx_mcomm_destroy", _st, _p)
+hccx_mcomm_size = _sig("hccx_mcomm_size", C.c_int, _p)
+hccx_mcomm_allreduce = _sig("hccx_mcomm_allreduce", _st, _p, _pp, _pp, _u64, Codec, C.c_int, _pp)
+hccx_mcomm_reduce_scatter = _sig("hccx_mcomm_reduce_scatter", _st, _p, _pp, _pp, _u64, Codec, _pp)
+hccx_mcomm_allgather = _sig("hccx_mcomm_allgather", _st, _p, _pp, _pp, _u64, Codec, _pp)
+hccx_mcomm_broadcast = _sig("hccx_mcomm_broadcast", _st, _p, C.c_int, _p, _pp, _u64, Codec, _pp)
+hccx_mcomm_p2p = _sig("hccx_mcomm_p2p", _st, _p, C.c_int, C.c_int, _p, _p, _u64, Codec, _pp)
+hccx_mcomm_status = _sig("hccx_mcomm_status", _st, _p, _pp)
+hccx_mcomm_allreduce_host = _sig("hccx_mcomm_allreduce_host", _st, _p, _pp, _pp, _u64, Codec, C.c_int, _dp)
+hccx_mcomm_reduce_scatter_host = _sig("hccx_mcomm_reduce_scatter_host", _st, _p, _pp, _pp, _u64, Codec, _dp)
+hccx_mcomm_allgather_host = _sig("hccx_mcomm_allgather_host", _st, _p, _pp, _pp, _u64, Codec, _dp)
+hccx_mcomm_broadcast_host = _sig("hccx_mcomm_broadcast_host", _st, _p, C.c_int, _p, _pp, _u64, Codec, _dp)
+hccx_mcomm_p2p_host = _sig("hccx_mcomm_p2p_host", _st, _p, C.c_int, C.c_int, _p, _p, _u64, Codec, _dp)
 hccx_launch_count = _sig("hccx_launch_count", _u64)
 
 #: every symbol include/hccx.h declares (checked by tests/test_abi.py)

@@ -4,24 +4,24 @@
 
 namespace hccx {
 
-cudaError_t launch_fused_fr_hi(int rate, const FusedParams& p, cudaStream_t s) {
+cudaError_t launch_fused_fr_hi(int rate, const FusedParams* p, int nv, cudaStream_t s) {
   switch (rate) {
-    case 17: return launch_fused_codec<FixedRateCodec<17>>(p, s);
-    case 18: return launch_fused_codec<FixedRateCodec<18>>(p, s);
-    case 19: return launch_fused_codec<FixedRateCodec<19>>(p, s);
-    case 20: return launch_fused_codec<FixedRateCodec<20>>(p, s);
-    case 21: return launch_fused_codec<FixedRateCodec<21>>(p, s);
-    case 22: return launch_fused_codec<FixedRateCodec<22>>(p, s);
-    case 23: return launch_fused_codec<FixedRateCodec<23>>(p, s);
-    case 24: return launch_fused_codec<FixedRateCodec<24>>(p, s);
-    case 25: return launch_fused_codec<FixedRateCodec<25>>(p, s);
-    case 26: return launch_fused_codec<FixedRateCodec<26>>(p, s);
-    case 27: return launch_fused_codec<FixedRateCodec<27>>(p, s);
-    case 28: return launch_fused_codec<FixedRateCodec<28>>(p, s);
-    case 29: return launch_fused_codec<FixedRateCodec<29>>(p, s);
-    case 30: return launch_fused_codec<FixedRateCodec<30>>(p, s);
-    case 31: return launch_fused_codec<FixedRateCodec<31>>(p, s);
-    case 32: return launch_fused_codec<FixedRateCodec<32>>(p, s);
+    case 17: return launch_fused_codec<FixedRateCodec<17>>(p, nv, s);
+    case 18: return launch_fused_codec<FixedRateCodec<18>>(p, nv, s);
+    case 19: return launch_fused_codec<FixedRateCodec<19>>(p, nv, s);
+    case 20: return launch_fused_codec<FixedRateCodec<20>>(p, nv, s);
+    case 21: return launch_fused_codec<FixedRateCodec<21>>(p, nv, s);
+    case 22: return launch_fused_codec<FixedRateCodec<22>>(p, nv, s);
+    case 23: return launch_fused_codec<FixedRateCodec<23>>(p, nv, s);
+    case 24: return launch_fused_codec<FixedRateCodec<24>>(p, nv, s);
+    case 25: return launch_fused_codec<FixedRateCodec<25>>(p, nv, s);
+    case 26: return launch_fused_codec<FixedRateCodec<26>>(p, nv, s);
+    case 27: return launch_fused_codec<FixedRateCodec<27>>(p, nv, s);
+    case 28: return launch_fused_codec<FixedRateCodec<28>>(p, nv, s);
+    case 29: return launch_fused_codec<FixedRateCodec<29>>(p, nv, s);
+    case 30: return launch_fused_codec<FixedRateCodec<30>>(p, nv, s);
+    case 31: return launch_fused_codec<FixedRateCodec<31>>(p, nv, s);
+    case 32: return launch_fused_codec<FixedRateCodec<32>>(p, nv, s);
     default: return cudaErrorInvalidValue;
   }
 }

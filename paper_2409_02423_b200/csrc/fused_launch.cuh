@@ -1,5 +1,6 @@
-// fused_launch.cuh -- cooperative launch of ring_fused_kernel<Codec>; included
-// by the per-rate-range translation units.
+// fused_launch.cuh -- cooperative launch of the NVLink-engine kernels
+// (ring_fused_kernel / oneshot_allreduce_kernel and their virtual-rank
+// twins); included by the per-rate-range translation units.
 #pragma once
 #include <atomic>
 #include <cstdio>
@@ -14,59 +15,92 @@ namespace hccx {
 // Co-resident CTAs of the fused kernel on this device (cooperative-launch cap).
 int fused_capacity(const void* kernel, int threads, uint32_t smem);
 
-template <class Codec>
-cudaError_t launch_oneshot_codec(const FusedParams& p, cudaStream_t stream) {
-  const void* k = reinterpret_cast<const void*>(&oneshot_allreduce_kernel<Codec>);
-  const uint64_t groups = (p.n_chunk + kGroupVals - 1) / kGroupVals;
-  if (groups == 0) return cudaSuccess;
-  // co-resident (cooperative) so no CTA waits on a peer while another CTA of
-  // this launch is still queued; ~8 groups per CTA, at most one CTA per SM
-  const uint64_t cap = static_cast<uint64_t>(fused_capacity(k, kOsWarps * 32, 0));
-  uint64_t grid = (groups + 7) / 8;
-  const uint64_t lim = cap < 148 ? cap : 148;
-  grid = grid < lim ? grid : lim;
-  grid = grid < kAckIdx ? grid : kAckIdx;
-  void* args[] = {const_cast<FusedParams*>(&p)};
+// CTAs per rank: every rank of a communicator must use the same grid (CTA b
+// of a rank only talks to CTA b of its peers), so the cap shared by all
+// ranks (P.max_grid, set for single-process communicators) wins over this
+// device's own capacity split over its nv virtual ranks.
+inline uint64_t rank_grid_cap(const FusedParams& p, uint64_t cap, int nv) {
+  uint64_t g = cap / static_cast<uint64_t>(nv);
+  if (p.max_grid && p.max_grid < g) g = p.max_grid;
+  if (g > kAckIdx) g = kAckIdx;
+  return g < 1 ? 1 : g;
+}
+
+inline cudaError_t launch_ranks(const void* kernel_1, const void* kernel_v, const FusedParams* P, int nv, uint32_t G, int threads,
+                         uint32_t smem, cudaStream_t stream) {
   count_launch();
-  return cudaLaunchCooperativeKernel(k, dim3(static_cast<unsigned>(grid)), dim3(kOsWarps * 32), args, 0, stream);
+  if (nv == 1) {
+    void* args[] = {const_cast<FusedParams*>(P)};
+    return cudaLaunchCooperativeKernel(kernel_1, dim3(G), dim3(threads), args, smem,
+                                       stream);
+  }
+  static thread_local VParams V;  // copied into the launch's parameter buffer at the call
+  for (int v = 0; v < nv; ++v) V.r[v] = P[v];
+  V.G = G;
+  void* args[] = {&V};
+  return cudaLaunchCooperativeKernel(kernel_v, dim3(G * static_cast<uint32_t>(nv)),
+                                     dim3(threads), args, smem, stream);
 }
 
 template <class Codec>
-cudaError_t launch_fused_codec(const FusedParams& p, cudaStream_t stream) {
-  if (p.op == kFOneShotAllReduce) return launch_oneshot_codec<Codec>(p, stream);
-  const void* k = reinterpret_cast<const void*>(&ring_fused_kernel<Codec>);
-  const uint64_t groups = (p.n_chunk + kGroupVals - 1) / kGroupVals;
+cudaError_t launch_oneshot_codec(const FusedParams* P, int nv, cudaStream_t stream) {
+  const uint64_t groups = (P[0].n_chunk + kGroupVals - 1) / kGroupVals;
+  if (groups == 0) return cudaSuccess;
+  const void* kv = reinterpret_cast<const void*>(&oneshot_allreduce_vkernel<Codec>);
+  // co-resident (cooperative) so no CTA waits on a peer while another CTA of
+  // this launch is still queued; ~8 groups per CTA, at most one CTA per SM
+  uint64_t cap = static_cast<uint64_t>(fused_capacity(kv, kOsWarps * 32, 0));
+  cap = cap < 148 ? cap : 148;
+  uint64_t grid = (groups + 7) / 8;
+  const uint64_t lim = rank_grid_cap(P[0], cap, nv);
+  grid = grid < lim ? grid : lim;
+  return launch_ranks(reinterpret_cast<const void*>(&oneshot_allreduce_kernel<Codec>), kv, P, nv,
+                      static_cast<uint32_t>(grid), kOsWarps * 32, 0, stream);
+}
+
+// Launch one collective (or one pass of it) for the nv ranks P[0..nv) that
+// live on the current device: one cooperative kernel either way.
+template <class Codec>
+cudaError_t launch_fused_codec(const FusedParams* P, int nv, cudaStream_t stream) {
+  if (nv < 1 || nv > kMaxRanks) return cudaErrorInvalidValue;
+  if (P[0].op == kFOneShotAllReduce) return launch_oneshot_codec<Codec>(P, nv, stream);
+  const uint64_t groups = (P[0].n_chunk + kGroupVals - 1) / kGroupVals;
   const uint64_t nseg = (groups + kSegGroups - 1) / kSegGroups;
   if (nseg == 0) return cudaSuccess;
   constexpr uint32_t smem = sizeof(FusedSmem2<Codec>);
   static_assert(smem <= 232448, "fused kernel shared memory exceeds the 227 KiB per-CTA limit");
+  const void* k1 = reinterpret_cast<const void*>(&ring_fused_kernel<Codec>);
+  const void* kv = reinterpret_cast<const void*>(&ring_fused_vkernel<Codec>);
   static std::atomic<uint64_t> configured{0};  // one bit per device
   int dev = 0;
   cudaGetDevice(&dev);
   if (!(configured.load() & (1ull << (dev & 63)))) {
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    cudaFuncSetAttribute(kv, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     configured.fetch_or(1ull << (dev & 63));
   }
-  const uint64_t cap = static_cast<uint64_t>(fused_capacity(k, kFThreads2, smem));
-  const uint64_t cap_ack = cap < kAckIdx ? cap : kAckIdx;
-  const int grid = static_cast<int>(nseg < cap_ack ? nseg : cap_ack);
-  FusedParams q = p;
-  if (q.step_segs == 0) {  // auto: about three published steps per phase per CTA, 2..16 segments each
-    const uint64_t myseg = (nseg + grid - 1) / grid;
-    const uint64_t s = (myseg + 2) / 3;
-    q.step_segs = static_cast<uint32_t>(s < 2 ? 2 : (s > 16 ? 16 : s));
+  const uint64_t cap = static_cast<uint64_t>(fused_capacity(nv == 1 ? k1 : kv, kFThreads2, smem));
+  const uint64_t gcap = rank_grid_cap(P[0], cap, nv);
+  const uint32_t grid = static_cast<uint32_t>(nseg < gcap ? nseg : gcap);
+  FusedParams q[kMaxRanks];
+  for (int v = 0; v < nv; ++v) {
+    q[v] = P[v];
+    q[v].ack_span = static_cast<uint32_t>(gcap);
+    if (q[v].step_segs == 0) {  // auto: about three published steps per phase per CTA, 2..16 segments each
+      const uint64_t myseg = (nseg + grid - 1) / grid;
+      const uint64_t s = (myseg + 2) / 3;
+      q[v].step_segs = static_cast<uint32_t>(s < 2 ? 2 : (s > 16 ? 16 : s));
+    }
+    if (q[v].first_segs == 0) q[v].first_segs = q[v].step_segs;
   }
-  if (q.first_segs == 0) q.first_segs = q.step_segs;
-  void* args[] = {&q};
-  count_launch();
-  if (p.debug & 64) {
+  if (P[0].debug & 64) {
     int b = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k, kFThreads2, smem);
-    std::fprintf(stderr, "hccx fused launch rank %d: op %d n_chunk %llu nseg %llu cap %llu grid %d smem %u occ %d\n",
-                 p.rank, p.op, static_cast<unsigned long long>(p.n_chunk), static_cast<unsigned long long>(nseg),
-                 static_cast<unsigned long long>(cap), grid, smem, b);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, nv == 1 ? k1 : kv, kFThreads2, smem);
+    std::fprintf(stderr, "hccx fused launch rank %d (+%d virtual): op %d n_chunk %llu nseg %llu cap %llu grid %u smem %u occ %d\n",
+                 P[0].rank, nv - 1, P[0].op, static_cast<unsigned long long>(P[0].n_chunk),
+                 static_cast<unsigned long long>(nseg), static_cast<unsigned long long>(cap), grid, smem, b);
   }
-  return cudaLaunchCooperativeKernel(k, dim3(grid), dim3(kFThreads2), args, smem, stream);
+  return launch_ranks(k1, kv, q, nv, grid, kFThreads2, smem, stream);
 }
 
 }  // namespace hccx

@@ -4,22 +4,22 @@
 
 namespace hccx {
 
-cudaError_t launch_fused_zfp_a(int rate, const FusedParams& p, cudaStream_t s) {
+cudaError_t launch_fused_zfp_a(int rate, const FusedParams* p, int nv, cudaStream_t s) {
   switch (rate) {
-    case 3: return launch_fused_codec<ZfpRateCodec<3>>(p, s);
-    case 4: return launch_fused_codec<ZfpRateCodec<4>>(p, s);
-    case 5: return launch_fused_codec<ZfpRateCodec<5>>(p, s);
-    case 6: return launch_fused_codec<ZfpRateCodec<6>>(p, s);
-    case 7: return launch_fused_codec<ZfpRateCodec<7>>(p, s);
-    case 8: return launch_fused_codec<ZfpRateCodec<8>>(p, s);
-    case 9: return launch_fused_codec<ZfpRateCodec<9>>(p, s);
-    case 10: return launch_fused_codec<ZfpRateCodec<10>>(p, s);
-    case 11: return launch_fused_codec<ZfpRateCodec<11>>(p, s);
-    case 12: return launch_fused_codec<ZfpRateCodec<12>>(p, s);
-    case 13: return launch_fused_codec<ZfpRateCodec<13>>(p, s);
-    case 14: return launch_fused_codec<ZfpRateCodec<14>>(p, s);
-    case 15: return launch_fused_codec<ZfpRateCodec<15>>(p, s);
-    case 16: return launch_fused_codec<ZfpRateCodec<16>>(p, s);
+    case 3: return launch_fused_codec<ZfpRateCodec<3>>(p, nv, s);
+    case 4: return launch_fused_codec<ZfpRateCodec<4>>(p, nv, s);
+    case 5: return launch_fused_codec<ZfpRateCodec<5>>(p, nv, s);
+    case 6: return launch_fused_codec<ZfpRateCodec<6>>(p, nv, s);
+    case 7: return launch_fused_codec<ZfpRateCodec<7>>(p, nv, s);
+    case 8: return launch_fused_codec<ZfpRateCodec<8>>(p, nv, s);
+    case 9: return launch_fused_codec<ZfpRateCodec<9>>(p, nv, s);
+    case 10: return launch_fused_codec<ZfpRateCodec<10>>(p, nv, s);
+    case 11: return launch_fused_codec<ZfpRateCodec<11>>(p, nv, s);
+    case 12: return launch_fused_codec<ZfpRateCodec<12>>(p, nv, s);
+    case 13: return launch_fused_codec<ZfpRateCodec<13>>(p, nv, s);
+    case 14: return launch_fused_codec<ZfpRateCodec<14>>(p, nv, s);
+    case 15: return launch_fused_codec<ZfpRateCodec<15>>(p, nv, s);
+    case 16: return launch_fused_codec<ZfpRateCodec<16>>(p, nv, s);
     default: return cudaErrorInvalidValue;
   }
 }

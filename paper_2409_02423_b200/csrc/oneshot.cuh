@@ -38,7 +38,7 @@ __device__ __forceinline__ uint32_t* os_flag(const FusedParams& P, int rank, int
 }
 
 template <class Codec>
-__global__ void __launch_bounds__(kOsWarps * 32) oneshot_allreduce_kernel(const __grid_constant__ FusedParams P) {
+__device__ __forceinline__ void oneshot_body(const FusedParams& P, const uint32_t cta, const uint32_t G) {
   __shared__ __align__(16) uint8_t stage[kOsWarps][kStageBytes];
   const int lane = static_cast<int>(lane_id()), warp = static_cast<int>(threadIdx.x >> 5);
   const int p = P.p, j = P.rank;
@@ -46,8 +46,8 @@ __global__ void __launch_bounds__(kOsWarps * 32) oneshot_allreduce_kernel(const 
   const uint64_t GB = Codec::kGroupBytes;
   const uint64_t wire = Codec::wire_bytes(c);
   const uint64_t gc = (c + kGroupVals - 1) / kGroupVals;
-  const uint64_t gpc = (gc + gridDim.x - 1) / gridDim.x;
-  const uint64_t g0 = blockIdx.x * gpc, g1 = min(g0 + gpc, gc);
+  const uint64_t gpc = (gc + G - 1) / G;
+  const uint64_t g0 = min(cta * gpc, gc), g1 = min(g0 + gpc, gc);
   const uint64_t v0 = min(g0 * kGroupVals, c), v1 = min(g1 * kGroupVals, c);
   const bool vec = P.vec_ok != 0;
   uint8_t* sm = stage[warp];
@@ -76,11 +76,11 @@ __global__ void __launch_bounds__(kOsWarps * 32) oneshot_allreduce_kernel(const 
   __syncthreads();  // every thread's stores precede the releases below (bar.sync + release cumulativity)
   if (threadIdx.x < static_cast<unsigned>(p - 1)) {
     const int d = (j + 1 + static_cast<int>(threadIdx.x)) % p;
-    signal(os_flag(P, d, 0, (j - d - 1 + 2 * p) % p, blockIdx.x), P.epoch);
+    signal(os_flag(P, d, 0, (j - d - 1 + 2 * p) % p, cta), P.epoch);
   }
 
   // ---- B: replay the ring chain of chunk j for this CTA's groups
-  if (threadIdx.x < static_cast<unsigned>(p - 1)) spin_ge(P, os_flag(P, j, 0, threadIdx.x, blockIdx.x), P.epoch, 0xb00u);
+  if (threadIdx.x < static_cast<unsigned>(p - 1)) spin_ge(P, os_flag(P, j, 0, threadIdx.x, cta), P.epoch, 0xb00u);
   __syncthreads();
   for (uint64_t g = g0 + warp; g < g1; g += kOsWarps) {
     const uint64_t base = g * kGroupVals;
@@ -117,13 +117,13 @@ __global__ void __launch_bounds__(kOsWarps * 32) oneshot_allreduce_kernel(const 
   __syncthreads();
   if (threadIdx.x < static_cast<unsigned>(p - 1)) {
     const int d = (j + 1 + static_cast<int>(threadIdx.x)) % p;
-    signal(os_flag(P, d, 1, j, blockIdx.x), P.epoch);
+    signal(os_flag(P, d, 1, j, cta), P.epoch);
   }
 
   // ---- C: decode every peer's shard (this CTA's groups of it)
   if (threadIdx.x < static_cast<unsigned>(p - 1)) {
     const int src = (j + 1 + static_cast<int>(threadIdx.x)) % p;
-    spin_ge(P, os_flag(P, j, 1, src, blockIdx.x), P.epoch, 0xc00u);
+    spin_ge(P, os_flag(P, j, 1, src, cta), P.epoch, 0xc00u);
   }
   __syncthreads();
   for (int q = 1; q < p; ++q) {
@@ -143,6 +143,18 @@ __global__ void __launch_bounds__(kOsWarps * 32) oneshot_allreduce_kernel(const 
   if constexpr (Codec::kCheckFinite) {
     if (__any_sync(kFull, bad) && lane == 0 && P.err) atomicOr(P.err, kErrNonFinite);
   }
+}
+
+template <class Codec>
+__global__ void __launch_bounds__(kOsWarps * 32) oneshot_allreduce_kernel(const __grid_constant__ FusedParams P) {
+  oneshot_body<Codec>(P, blockIdx.x, gridDim.x);
+}
+
+// Virtual ranks (see ring_fused_vkernel): rank v = blockIdx.x / G.
+template <class Codec>
+__global__ void __launch_bounds__(kOsWarps * 32) oneshot_allreduce_vkernel(const __grid_constant__ VParams V) {
+  const uint32_t v = blockIdx.x / V.G;
+  oneshot_body<Codec>(V.r[v], blockIdx.x - v * V.G, V.G);
 }
 
 }  // namespace hccx

@@ -76,7 +76,16 @@ struct FusedParams {
   int ag_ring;         // allgather as a forwarding ring (1) or direct owner pushes (0)
   uint32_t first_segs;  // segments in the first step of every phase
   uint32_t step_segs;  // segments per published step (one release + flag per destination)
+  uint32_t credit_all;  // bit c: slot class c (0 rs, 1 ag, 2 pp) changed geometry since its last use
+  uint32_t ack_span;    // consumption-ack indices covering every CTA of any grid this communicator launches
+  uint32_t max_grid;    // CTAs per rank cap shared by all ranks (0: the device's co-resident capacity)
   int debug;  // development knobs (HCCX_DEBUG): 16 = warp-store pushes, 32 = synchronous tile release, 64 = log launches
+};
+
+// Parameters of the virtual-rank kernels: nv ranks, G CTAs each.
+struct VParams {
+  FusedParams r[kMaxRanks];
+  uint32_t G;
 };
 
 // Flag classes in every window:
@@ -97,6 +106,7 @@ struct FusedParams {
 // A sender CTA waits once per slot per call on its own index's ack of the
 // slot's previous use before overwriting it -- back-to-back collectives
 // never race a slow receiver.
+constexpr uint64_t kTraceMinWords = 16384 + 1024;  // fixed trace slots (timeouts 4000.., accumulators 4096..)
 constexpr uint32_t kAckIdx = 1024;  // >= any co-resident grid of the fused kernel (148 SMs x CTAs per SM)
 
 __device__ __forceinline__ uint32_t* flag_ptr(const FusedParams& P, int rank, int cls, int slot, uint32_t idx) {
@@ -120,7 +130,7 @@ __device__ __forceinline__ uint8_t* slot_ptr(const FusedParams& P, int rank, int
 // Expired waits are logged (trace words 4000..4090: cta << 32 | who) so the
 // wait chain of a stalled collective can be read back.
 __device__ __forceinline__ void trace_timeout(const FusedParams& P, uint32_t who, const uint32_t* prog = nullptr) {
-  if (!P.trace) return;
+  if (!P.trace || P.trace_cap < kTraceMinWords) return;  // hccx_comm_trace_enable enforces the minimum
   unsigned long long* t = reinterpret_cast<unsigned long long*>(P.trace);
   const unsigned long long i = atomicAdd(t + 4000, 1ull);
   if (i < 90) t[4001 + i] = (static_cast<unsigned long long>(blockIdx.x) << 32) | who;
@@ -180,94 +190,11 @@ __device__ __forceinline__ void mbar_wait_to(const FusedParams& P, uint64_t* bar
   }
 }
 
-// The CTA barrier publishes thread 0's acquire to every warp.
-__device__ __forceinline__ void seg_wait(const FusedParams& P, const uint32_t* flag, uint32_t epoch) {
-  if (threadIdx.x == 0) spin_ge(P, flag, epoch);
-  __syncthreads();
-}
-
-// Push `nbytes` of the staged tile to `dst` (peer memory) with 16-byte stores.
-__device__ __forceinline__ void push_tile(const uint8_t* tile, uint8_t* dst, uint32_t nbytes) {
-  const uint32_t n16 = nbytes >> 4;
-  if ((reinterpret_cast<uintptr_t>(dst) & 15u) == 0) {
-    for (uint32_t i = threadIdx.x; i < n16; i += blockDim.x)
-      reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(tile)[i];
-    for (uint32_t b = (n16 << 4) + threadIdx.x; b < nbytes; b += blockDim.x) dst[b] = tile[b];
-  } else {
-    for (uint32_t b = threadIdx.x; b < nbytes; b += blockDim.x) dst[b] = tile[b];
-  }
-}
-
-__device__ __forceinline__ void push_tile_n(const uint8_t* tile, uint8_t* dst, uint32_t nbytes, uint32_t nthreads) {
-  const uint32_t n16 = nbytes >> 4;
-  if ((reinterpret_cast<uintptr_t>(dst) & 15u) == 0) {
-    for (uint32_t i = threadIdx.x; i < n16; i += nthreads)
-      reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(tile)[i];
-    for (uint32_t b = (n16 << 4) + threadIdx.x; b < nbytes; b += nthreads) dst[b] = tile[b];
-  } else {
-    for (uint32_t b = threadIdx.x; b < nbytes; b += nthreads) dst[b] = tile[b];
-  }
-}
-
 // Publish a step.  The pushes of every thread precede this thread's
 // release store through the CTA barrier (cumulativity of st.release at
 // system scope), so no separate sc fence is needed; the remote reader
 // pairs it with ld.acquire.sys.
 __device__ __forceinline__ void signal(uint32_t* flag, uint32_t epoch) { st_release_sys(flag, epoch); }
-
-// Consumption ack for this CTA's indices (see kAckIdx).  Call after a CTA
-// barrier that follows the last read of the slot.
-__device__ __forceinline__ void ack_all(uint32_t* flags, uint32_t epoch) {
-  for (uint32_t k = blockIdx.x + threadIdx.x * gridDim.x; k < kAckIdx; k += gridDim.x * blockDim.x)
-    st_release_sys(flags + k, epoch);
-}
-
-// One warp's group of a segment.
-//   kEnc  : values (src_vals [+ local]) -> encoded group written into the
-//           shared tile at `tile_g`; optional decoded copy -> out_vals
-//   !kEnc : payload (src_pay, local memory) decoded [+ local] -> out_vals
-template <class Codec, bool kEnc, bool kAdd>
-__device__ __forceinline__ void fused_group(const FusedParams& P, const uint8_t* src_pay, const float* src_vals,
-                                            const float* local, float* out_vals, bool out_is_sum,
-                                            uint8_t* tile_g, uint64_t g, uint8_t* sm, int lane, uint32_t& bad) {
-  const uint64_t base = g * kGroupVals;
-  const uint32_t live = static_cast<uint32_t>(P.n_chunk - base < kGroupVals ? P.n_chunk - base : kGroupVals);
-  const bool full = live == kGroupVals;
-  const bool vec = P.vec_ok != 0;
-  typename Codec::Lane s;
-  float v[8];
-  if (src_pay) {
-    group_load<Codec, false>(s, src_pay + g * Codec::kGroupBytes, live, true, sm, lane);
-    Codec::decode(s, v);
-  } else {
-    load_vals<false>(src_vals, base, live, vec, lane, v);
-  }
-  if constexpr (kAdd) {
-    float loc[8];
-    load_vals<false>(local, base, live, vec, lane, loc);
-#pragma unroll
-    for (int i = 0; i < 8; ++i) v[i] = __fadd_rn(v[i], loc[i]);
-  }
-  if constexpr (kEnc) {
-    Codec::encode(v, s, bad, lane_live(live, lane));
-    bool done = false;
-    if constexpr (Codec::kFastPath) {
-      if (full && (reinterpret_cast<uintptr_t>(tile_g) & (Codec::kKind == 0 ? 31u : 3u)) == 0) {
-        Codec::store_fast_generic(s, reinterpret_cast<uint32_t*>(tile_g), lane);
-        done = true;
-      }
-    }
-    if (!done) Codec::to_stage(s, tile_g, lane);
-    if (out_vals) {
-      Codec::decode(s, v);
-      apply_div(v, P.div_mode, P.recip, P.divisor);
-      store_vals(out_vals, base, live, vec, lane, v);
-    }
-  } else {
-    if (!out_is_sum) apply_div(v, P.div_mode, P.recip, P.divisor);
-    store_vals(out_vals, base, live, vec, lane, v);
-  }
-}
 
 // ---------------------------------------------------------------------------
 // Warp-specialised fused kernel.
@@ -514,8 +441,8 @@ __device__ __forceinline__ Phase phase_of(const FusedParams& P, int ph) {
 
 // Event log for CTA 0 (timeline of one CTA; ncu cannot replay a multi-rank
 // kernel).  tag = (event << 32) | (phase << 16) | segment.
-__device__ __forceinline__ void trace_ev(const FusedParams& P, uint32_t ev, uint32_t ph, uint32_t seg) {
-  if (P.trace == nullptr || blockIdx.x != 0) return;
+__device__ __forceinline__ void trace_ev(const FusedParams& P, uint32_t cta, uint32_t ev, uint32_t ph, uint32_t seg) {
+  if (P.trace == nullptr || cta != 0) return;
   const unsigned long long i = atomicAdd(reinterpret_cast<unsigned long long*>(P.trace), 1ull);
   if (2 * i + 2 < 4000 && 2 * i + 2 < P.trace_cap) {
     P.trace[1 + 2 * i] = (static_cast<uint64_t>(ev) << 32) | (static_cast<uint64_t>(ph) << 16) | seg;
@@ -525,8 +452,8 @@ __device__ __forceinline__ void trace_ev(const FusedParams& P, uint32_t ev, uint
 
 // Cycle accumulators for CTA 0 (written once at the end, slots 1..): a
 // breakdown of where each role's time goes without per-event round trips.
-__device__ __forceinline__ void trace_acc(const FusedParams& P, uint32_t slot, uint64_t cycles) {
-  if (P.trace == nullptr || blockIdx.x != 0) return;
+__device__ __forceinline__ void trace_acc(const FusedParams& P, uint32_t cta, uint32_t slot, uint64_t cycles) {
+  if (P.trace == nullptr || cta != 0 || 4096 + slot >= P.trace_cap) return;
   atomicAdd(reinterpret_cast<unsigned long long*>(P.trace) + 4096 + slot, static_cast<unsigned long long>(cycles));
 }
 
@@ -601,8 +528,12 @@ __device__ __forceinline__ void compute_group(const FusedParams& P, const Phase&
 
 static_assert(kFusedWarps == 8 || kFusedWarps == 12 || kFusedWarps == 24, "CTAs per SM = 24 / compute warps");
 
+// The kernel body for one rank's CTA `cta` of `G`: the real kernel runs one
+// rank per launch (cta = blockIdx.x); the virtual-rank kernel below splits
+// one cooperative grid into several ranks on the same device (single-process
+// communicators and the 1-GPU tests of this exact code).
 template <class Codec>
-__global__ void __launch_bounds__(kFThreads2, kFCtasPerSm) ring_fused_kernel(const __grid_constant__ FusedParams P) {
+__device__ __forceinline__ void ring_fused_body(const FusedParams& P, const uint32_t cta, const uint32_t G) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   FusedSmem2<Codec>& S = *reinterpret_cast<FusedSmem2<Codec>*>(smem_raw);
   constexpr int kT = TileGeom<Codec>::kTiles;
@@ -616,14 +547,13 @@ __global__ void __launch_bounds__(kFThreads2, kFCtasPerSm) ring_fused_kernel(con
   const uint32_t nseg = static_cast<uint32_t>((ngroups + kSegGroups - 1) / kSegGroups);
   const uint64_t GB = Codec::kGroupBytes;
   const uint64_t wire = Codec::wire_bytes(c);
-  const uint32_t G = gridDim.x;
-  const uint32_t myseg = nseg > blockIdx.x ? (nseg - blockIdx.x + G - 1) / G : 0;
+  const uint32_t myseg = nseg > cta ? (nseg - cta + G - 1) / G : 0;
   const int nph = nphases(P);
   // TMA needs whole 16B-multiple segments at 16B-aligned addresses: word
   // codecs with 32B-aligned fp32 chunks (payload segments are 8*GB bytes,
   // a multiple of 16, at 256B-aligned slot offsets).
   const bool tma_ok = Codec::kFastPath && P.vec_ok;
-  auto seg_of = [&](uint32_t k) { return blockIdx.x + k * G; };
+  auto seg_of = [&](uint32_t k) { return cta + k * G; };
   auto seg_full = [&](uint32_t sg) { return (static_cast<uint64_t>(sg) + 1) * kSegVals <= c; };
   // Step boundaries within a phase: a short first step (P.first_segs) so the
   // neighbour's next phase can start early, then P.step_segs per step.
@@ -642,11 +572,11 @@ __global__ void __launch_bounds__(kFThreads2, kFCtasPerSm) ring_fused_kernel(con
     fence_mbar_init();
   }
   __syncthreads();
-  if (P.trace && threadIdx.x == 0 && 16384 + blockIdx.x < P.trace_cap) {
+  if (P.trace && threadIdx.x == 0 && 16384 + cta < P.trace_cap) {
     uint32_t smid;
     asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-    P.trace[8192 + 2 * blockIdx.x] = globaltimer_ns();
-    P.trace[16384 + blockIdx.x] = smid;
+    P.trace[8192 + 2 * cta] = globaltimer_ns();
+    P.trace[16384 + cta] = smid;
   }
 
   if (warp == kFCompute) {
@@ -667,7 +597,7 @@ __global__ void __launch_bounds__(kFThreads2, kFCtasPerSm) ring_fused_kernel(con
             spin_ge(P, flag_ptr(P, j, f.wait_cls, f.wait_slot, seg_of(k0)), f.wait_ep, 0x700u | (ph << 4) | f.wait_cls);
             asm volatile("fence.proxy.async.global;" ::: "memory");
             c_flag += clock64() - t0;
-            trace_ev(P, 1, ph, k0);
+            trace_ev(P, cta, 1, ph, k0);
           }
           for (uint32_t k = k0; k < k1; ++k) {
             const uint32_t sg = seg_of(k);
@@ -708,9 +638,9 @@ __global__ void __launch_bounds__(kFThreads2, kFCtasPerSm) ring_fused_kernel(con
           }
         }
       }
-      trace_acc(P, 0, clock64() - c_total);
-      trace_acc(P, 1, c_empty);
-      trace_acc(P, 2, c_flag);
+      trace_acc(P, cta, 0, clock64() - c_total);
+      trace_acc(P, cta, 1, c_empty);
+      trace_acc(P, cta, 2, c_flag);
     }
     return;
   }
@@ -738,14 +668,26 @@ __global__ void __launch_bounds__(kFThreads2, kFCtasPerSm) ring_fused_kernel(con
       const Phase f = phase_of(P, ph);
       const bool push = f.push_cls >= 0;
       const uint64_t tc = clock64();
-      if (push && lane == 0) {  // credit: previous use of the destination slot(s) consumed
+      if (push) {  // credit: previous use of the destination slot(s) consumed
+        // Same slot geometry as the previous use (codec, chunk size, hence
+        // grid and segment bytes): this CTA's segments were read by the
+        // receiver CTA with our index, whose ack we wait for.  Geometry
+        // changed (P.credit_all): the byte ranges we are about to overwrite
+        // were read by arbitrary receiver CTAs, so wait for all of them --
+        // receiver CTA r of a grid G' acked indices r, r+G', ..., so indices
+        // [0, ack_span) cover every CTA of any grid <= ack_span.
+        const bool all = ((P.credit_all >> f.push_cls) & 1u) != 0;
         for (int q = 1; q < p; ++q) {
           const int d = (j + q) % p;
           if (f.push_mode == 0 && d != (j + 1) % p) continue;
           if (f.push_mode == 2 && d != P.dst) continue;
           const uint32_t need = f.push_cls == 2 ? P.pp_epoch[d] - 1u : f.credit_ep;
-          spin_ge(P, flag_ptr(P, j, f.credit_cls, f.push_mode == 0 ? f.push_slot : d, blockIdx.x), need,
-                  0x800u | (ph << 4) | f.credit_cls);
+          const uint32_t* fl = flag_ptr(P, j, f.credit_cls, f.push_mode == 0 ? f.push_slot : d, 0);
+          if (all) {
+            for (uint32_t k = lane; k < P.ack_span; k += 32) spin_ge(P, fl + k, need, 0x900u | (ph << 4) | f.credit_cls);
+          } else if (lane == 0) {
+            spin_ge(P, fl + cta, need, 0x800u | (ph << 4) | f.credit_cls);
+          }
         }
       }
       __syncwarp();
@@ -782,7 +724,7 @@ __global__ void __launch_bounds__(kFThreads2, kFCtasPerSm) ring_fused_kernel(con
                 }
                 bulk_commit();
                 c_issue += clock64() - ti;
-                trace_ev(P, 3, ph, k);
+                trace_ev(P, cta, 3, ph, k);
               }
               bulk_issued = true;
             } else {
@@ -835,13 +777,13 @@ __global__ void __launch_bounds__(kFThreads2, kFCtasPerSm) ring_fused_kernel(con
     if (lane == 0) {
       bulk_wait_all();
       release_upto(seq);
-      trace_acc(P, 8, clock64() - c_total);
-      trace_acc(P, 9, c_tfull);
-      trace_acc(P, 10, c_read);
-      trace_acc(P, 11, c_pub);
-      trace_acc(P, 12, c_credit);
-      trace_acc(P, 13, c_issue);
-      if (P.trace && 8192 + 2 * blockIdx.x + 1 < P.trace_cap) P.trace[8193 + 2 * blockIdx.x] = globaltimer_ns();
+      trace_acc(P, cta, 8, clock64() - c_total);
+      trace_acc(P, cta, 9, c_tfull);
+      trace_acc(P, cta, 10, c_read);
+      trace_acc(P, cta, 11, c_pub);
+      trace_acc(P, cta, 12, c_credit);
+      trace_acc(P, cta, 13, c_issue);
+      if (P.trace && 8192 + 2 * cta + 1 < P.trace_cap) P.trace[8193 + 2 * cta] = globaltimer_ns();
     }
     return;
   }
@@ -888,14 +830,14 @@ __global__ void __launch_bounds__(kFThreads2, kFCtasPerSm) ring_fused_kernel(con
           }
           __syncwarp();
           c_sig += clock64() - ts;
-          if (lane == 0) trace_ev(P, 5, ph, k0);
+          if (lane == 0) trace_ev(P, cta, 5, ph, k0);
         }
       }
       if (f.ack_rank >= 0) {  // one fence, then relaxed stores of the ack words
         wait_event(++events);
         const uint64_t ta = clock64();
         fence_acq_rel_sys();
-        for (uint32_t kk = blockIdx.x + lane * G; kk < kAckIdx; kk += G * 32) {
+        for (uint32_t kk = cta + lane * G; kk < kAckIdx; kk += G * 32) {
           st_relaxed_sys(flag_ptr(P, f.ack_rank, f.ack_cls, f.ack_slot, 0) + kk, f.ack_ep);
           if (f.ack2_rank >= 0) st_relaxed_sys(flag_ptr(P, f.ack2_rank, f.ack2_cls, f.ack2_slot, 0) + kk, f.ack_ep);
         }
@@ -904,8 +846,8 @@ __global__ void __launch_bounds__(kFThreads2, kFCtasPerSm) ring_fused_kernel(con
       }
     }
     if (lane == 0) {
-      trace_acc(P, 14, c_ack);
-      trace_acc(P, 15, c_sig);
+      trace_acc(P, cta, 14, c_ack);
+      trace_acc(P, cta, 15, c_sig);
     }
     return;
   }
@@ -941,7 +883,7 @@ __global__ void __launch_bounds__(kFThreads2, kFCtasPerSm) ring_fused_kernel(con
       if (g < ngroups) compute_group<Codec>(P, f, g, direct, sa, sb, S.tile[tt] + warp * GB, gen, lane, bad);
       __syncwarp();
       c_comp += clock64() - t2;
-      if (warp == 0 && lane == 0) trace_ev(P, 2, ph, k);
+      if (warp == 0 && lane == 0) trace_ev(P, cta, 2, ph, k);
       if (lane == 0) S.prog[warp] = (ph << 20) | (k << 4) | 3u;
       if (lane == 0) {
         mbar_arrive(&S.empty[st]);
@@ -955,14 +897,29 @@ __global__ void __launch_bounds__(kFThreads2, kFCtasPerSm) ring_fused_kernel(con
     }
   }
   if (lane == 0 && warp == 0) {
-    trace_acc(P, 16, clock64() - c_total);
-    trace_acc(P, 17, c_full);
-    trace_acc(P, 18, c_tile);
-    trace_acc(P, 19, c_comp);
+    trace_acc(P, cta, 16, clock64() - c_total);
+    trace_acc(P, cta, 17, c_full);
+    trace_acc(P, cta, 18, c_tile);
+    trace_acc(P, cta, 19, c_comp);
   }
   if constexpr (Codec::kCheckFinite) {
     if (__any_sync(kFull, bad) && lane == 0 && P.err) atomicOr(P.err, kErrNonFinite);
   }
+}
+
+template <class Codec>
+__global__ void __launch_bounds__(kFThreads2, kFCtasPerSm) ring_fused_kernel(const __grid_constant__ FusedParams P) {
+  ring_fused_body<Codec>(P, blockIdx.x, gridDim.x);
+}
+
+// Virtual ranks: several ranks of one communicator on this device share one
+// cooperative grid of nv x G CTAs (all co-resident, so every flag wait can
+// be satisfied); rank v's parameters are V.r[v] (a large kernel parameter,
+// up to 16 x sizeof(FusedParams), passed by value: graph-capturable).
+template <class Codec>
+__global__ void __launch_bounds__(kFThreads2, kFCtasPerSm) ring_fused_vkernel(const __grid_constant__ VParams V) {
+  const uint32_t v = blockIdx.x / V.G;
+  ring_fused_body<Codec>(V.r[v], blockIdx.x - v * V.G, V.G);
 }
 
 }  // namespace hccx

@@ -15,6 +15,7 @@
 #include <utility>
 
 #include "hcc/hcc_b200.hpp"
+#include "hcc/rng.hpp"
 #include "hccx.h"
 
 namespace hcc {
@@ -497,3 +498,17 @@ SchemeTable scheme_from_name(const std::string& name) {
 }
 
 }  // namespace hcc
+
+// Synthetic inputs for the bench / tools: the reference's hcc::Rng streams
+// (include/hcc/rng.hpp), so the GPU and the CPU reference see the same
+// buffers for a seed.  mode 0: lo * normal() (the gradient-like bench input,
+// lo = 1e-3); mode 1: uniform(lo, hi).
+extern "C" __attribute__((visibility("default"))) void hcc_b200_fill(std::uint64_t seed, int mode, std::uint64_t n,
+                                                                    float lo, float hi, float* out) {
+  hcc::Rng rng(seed);
+  if (mode == 1) {
+    for (std::uint64_t i = 0; i < n; ++i) out[i] = rng.uniform(lo, hi);
+  } else {
+    for (std::uint64_t i = 0; i < n; ++i) out[i] = lo * rng.normal();
+  }
+}

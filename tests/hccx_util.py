@@ -23,10 +23,10 @@ def wire(kind: str, rate: int, n: int) -> int:
     return out.value
 
 
-def dev(x: np.ndarray, offset: int = 0, dtype=torch.float32):
-    """Copy to cuda:0, optionally at an element offset inside a larger buffer
-    (to exercise unaligned pointers)."""
-    t = torch.zeros(x.size + offset + 8, dtype=dtype, device="cuda:0")
+def dev(x: np.ndarray, offset: int = 0, dtype=torch.float32, device: int = 0):
+    """Copy to cuda:<device>, optionally at an element offset inside a larger
+    buffer (to exercise unaligned pointers)."""
+    t = torch.zeros(x.size + offset + 8, dtype=dtype, device=f"cuda:{device}")
     v = t[offset:offset + x.size]
     if x.size:
         v.copy_(torch.from_numpy(np.ascontiguousarray(x)))
@@ -117,4 +117,69 @@ class Group:
         src = dev(x)
         out = torch.full((x.size,), float("nan"), device="cuda:0")
         st = self._run(_lib.hccx_group_p2p, src.data_ptr(), out.data_ptr(), x.size, codec(kind, rate), stream())
+        return out.cpu().numpy(), st
+
+
+class MComm(Group):
+    """Single-process communicator (hccx_mcomm_*): member j on devices[j].
+    With every member on cuda:0 the members are virtual ranks of ONE
+    cooperative launch of the NVLink engine's kernels (ring_fused_kernel /
+    oneshot_allreduce_kernel device code), so a 1-GPU box runs the exact
+    multi-GPU data path; with distinct devices the same kernels talk over
+    NVLink (peer access)."""
+
+    def __init__(self, p: int, max_n: int, devices=None):
+        h = C.c_void_p()
+        self.devices = list(devices or [0] * p)
+        devs = (C.c_int * p)(*self.devices)
+        check(_lib.hccx_mcomm_create(p, devs, max_n, C.byref(h)))
+        self.h = h.value
+        self.p = p
+
+    def __del__(self):
+        try:
+            _lib.hccx_mcomm_destroy(self.h)
+        except Exception:
+            pass
+
+    def _run(self, fn, *args):
+        st = fn(self.h, *args)
+        if st == 0:
+            st = _lib.hccx_mcomm_status(self.h, None)
+        return st
+
+    def _nan(self, n, j):
+        return torch.full((n,), float("nan"), device=f"cuda:{self.devices[j]}")
+
+    def allreduce(self, x, kind, rate=0, average=False, inplace=False):
+        return self._coll(_lib.hccx_mcomm_allreduce, x, x.shape[1], x.shape[1], inplace,
+                          (codec(kind, rate), int(average)))
+
+    def reduce_scatter(self, x, kind, rate=0):
+        return self._coll(_lib.hccx_mcomm_reduce_scatter, x, x.shape[1] // self.p, x.shape[1], False,
+                          (codec(kind, rate),))
+
+    def allgather(self, s, kind, rate=0):
+        return self._coll(_lib.hccx_mcomm_allgather, s, s.shape[1] * self.p, s.shape[1], False,
+                          (codec(kind, rate),))
+
+    def _coll(self, fn, x, out_n, n_arg, inplace, tail):
+        ins = [dev(x[j], device=self.devices[j]) for j in range(self.p)]
+        outs = ins if inplace else [self._nan(out_n, j) for j in range(self.p)]
+        a, _ka = _lib.ptr_array([t.data_ptr() for t in ins])
+        b, _kb = _lib.ptr_array([t.data_ptr() for t in outs])
+        st = self._run(fn, a, b, n_arg, *tail, None)
+        return np.stack([t.cpu().numpy() for t in outs]), st
+
+    def broadcast(self, x, root, kind, rate=0):
+        src = dev(x, device=self.devices[root])
+        outs = [self._nan(x.size, j) for j in range(self.p)]
+        b, _kb = _lib.ptr_array([t.data_ptr() for t in outs])
+        st = self._run(_lib.hccx_mcomm_broadcast, root, src.data_ptr(), b, x.size, codec(kind, rate), None)
+        return np.stack([t.cpu().numpy() for t in outs]), st
+
+    def p2p(self, x, kind, rate=0, src=0, dst=1):
+        s = dev(x, device=self.devices[src])
+        out = self._nan(x.size, dst)
+        st = self._run(_lib.hccx_mcomm_p2p, src, dst, s.data_ptr(), out.data_ptr(), x.size, codec(kind, rate), None)
         return out.cpu().numpy(), st
