@@ -399,28 +399,6 @@ def bench_codec(args):
 
 # ----------------------------------------------------- N > 1: allreduce ----
 
-def _nccl_debug_setup():
-    """NCCL's own INIT/TUNING log (algorithm / protocol chosen for the
-    uncompressed baseline), one file per process, summarised into the line."""
-    path = os.path.join("/tmp", f"hccx_bench_nccl.{os.getpid()}.log")
-    os.environ.setdefault("NCCL_DEBUG", "INFO")
-    os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT,TUNING")
-    os.environ.setdefault("NCCL_DEBUG_FILE", path)
-    return path
-
-
-def _nccl_summary(path: str, nbytes: int):
-    try:
-        with open(path, errors="replace") as f:
-            lines = f.read().splitlines()
-    except Exception:
-        return None
-    keep = [ln.split("NCCL INFO", 1)[-1].strip() for ln in lines if "NCCL INFO" in ln]
-    init = [ln for ln in keep if any(k in ln for k in ("NCCL version", "NVLS", "Channel 00", "comm 0x"))][:8]
-    tuning = [ln for ln in keep if "AllReduce" in ln and str(nbytes) in ln][:3]
-    return {"init": init, "allreduce_tuning": tuning}
-
-
 def bench_allreduce(args):
     import numpy as np
     import torch
@@ -430,7 +408,11 @@ def bench_allreduce(args):
     from paper_2409_02423_b200.codec import CodecSpec, wire_size_bytes
     from paper_2409_02423_b200.dist import NvlinkComm
 
-    nccl_log = _nccl_debug_setup()
+    # the image exports NCCL_DEBUG=VERSION, which prints NCCL's version line
+    # on stdout: keep stdout to the one JSON line (NCCL's own log of the
+    # baseline is tools/nccl_info.py)
+    if os.environ.get("NCCL_DEBUG", "VERSION").upper() == "VERSION":
+        os.environ["NCCL_DEBUG"] = "WARN"
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
@@ -567,7 +549,6 @@ def bench_allreduce(args):
     nvl_ach = wire_bytes / t / 1e9
     bound = "hbm" if hbm_bytes / (hbm * 1e9) >= wire_bytes / (NVLINK_PEAK * 1e9) else "nvlink"
     t_roof = max(hbm_bytes / (hbm * 1e9), wire_bytes / (NVLINK_PEAK * 1e9))
-    nccl = _nccl_summary(nccl_log, 4 * n) if rank == 0 else None
     if rank == 0:
         line = {
             "metric": METRIC, "value": round(4 * n / t / 1e9, 2), "unit": "GB/s", "n_gpus": world,
@@ -584,7 +565,7 @@ def bench_allreduce(args):
                        "soak_ms_per_call": round(soak_ms, 5),
                        "nccl_allreduce_GBps": round(4 * n / (nccl_ms * 1e-3) / 1e9, 2) if nccl_ms else None,
                        "nccl_ms": round(nccl_ms, 5) if nccl_ms else None,
-                       "nccl_log": nccl},
+                       "nccl_log": "profiles/r02_nccl_info_p*.txt (tools/nccl_info.py, NCCL_DEBUG=INFO)"},
             "parity": dict(parity, ranks_agree=agree),
             "roofline": {"bound": bound, "kernel": "ring_fused_kernel",
                          "achieved": round(hbm_ach if bound == "hbm" else nvl_ach, 1),

@@ -12,8 +12,10 @@
 // bit-identical (fixed-rate / identity).  Differences, all additive:
 //   * CodecKind::ZfpRate ("zfp-rate:N") -- ZFP-style transform codec;
 //   * broadcast() collective and CollectiveKind::Broadcast;
-//   * TraceEvent::duration_s is the measured device time (no alpha-beta
-//     model); Topology keeps the shape (world size, rank -> node) only.
+//   * TraceEvent::device_s: the measured device time of each collective
+//     (duration_s keeps the reference's alpha-beta model, netsim.cpp:53-75);
+//   * collectives run on the NVLink engine (hccx_mcomm_*): members on
+//     distinct GPUs talk over NVLink, members sharing a GPU are virtual ranks;
 //   * LosslessPredictor runs on the device (csrc/lossless.cu); collectives
 //     move its values through the identity ring (the codec is transparent)
 //     and size every hop's message with the device size pass.
@@ -133,18 +135,35 @@ CommPath comm_path_from_string(const std::string& s);
 
 // ------------------------------------------------------- clock and trace --
 
+// proj/include/hcc/netsim.hpp:17-41.  The clock keeps the reference's
+// alpha-beta cost model (simulated time: durations are identical to the
+// reference's for the same topology and messages); the B200 engine's
+// measured device time of each collective is TraceEvent::device_s.
 struct Topology {
   int num_nodes = 1;
   int gpus_per_node = 1;
-  double intra_bw = 0, inter_bw = 0, intra_lat = 0, inter_lat = 0, codec_bw = 0, compute_flops = 0;
+  double intra_bw = 0;       // bytes/s within a node
+  double inter_bw = 0;       // bytes/s across nodes
+  double intra_lat = 0;      // s
+  double inter_lat = 0;      // s
+  double codec_bw = 0;       // bytes/s, charged per compress and per decompress
+  double compute_flops = 0;  // flop/s per rank
 
   int world_size() const { return num_nodes * gpus_per_node; }
   int node_of(int rank) const { return rank / gpus_per_node; }
+  void validate() const;  // ConfigError on a nonpositive count or rate (src/netsim.cpp:9-18)
   static Topology lassen_like(int num_nodes = 2);
   static Topology desk_2x2(int num_nodes = 2);
+  // Addition: one B200 box; codec_bw is the measured fixed-rate codec
+  // throughput (bench.py N=1), intra_bw NVLink 5 per direction.
   static Topology b200_box(int num_gpus = 8);
   static Topology preset(const std::string& name, int num_nodes);
 };
+
+enum class LinkClass { SelfLoop, IntraNode, InterNode };
+LinkClass link_class(const Topology& topo, int a, int b);
+double transfer_time(const Topology& topo, std::uint64_t bytes, LinkClass link);
+double codec_time(const Topology& topo, std::uint64_t raw_bytes, const CodecSpec& spec);
 
 enum class CollectiveKind { AllReduce, AllGather, ReduceScatter, P2P, Broadcast };
 const char* to_string(CollectiveKind c);
@@ -156,8 +175,9 @@ struct TraceEvent {
   int comm_size = 0;
   std::uint64_t raw_bytes = 0;   // per-rank sent bytes
   std::uint64_t wire_bytes = 0;
-  double duration_s = 0;         // measured device time of the collective
+  double duration_s = 0;         // the reference's cost model (simulated seconds)
   int round_count = 0;
+  double device_s = 0;           // addition: measured device time of the collective on the B200s
 };
 
 class SimClock {
@@ -233,8 +253,13 @@ SchemeTable scheme_mz_hybrid(int dp_rate);
 SchemeTable scheme_z_hybrid(int mp_rate, int dp_rate);
 SchemeTable scheme_from_name(const std::string& name);
 
-// Device the shim runs on (default: the current CUDA device / 0).
+// Where the shim runs.  Codec calls use one device (default 0).  Collective
+// member rank r runs on GPU devices[r % devices.size()] (default: every
+// visible GPU; env HCC_B200_DEVICES="0,1,..." overrides): members on distinct
+// GPUs exchange compressed segments over NVLink, members sharing a GPU are
+// virtual ranks of one launch.  set_device(d) pins everything to GPU d.
 void set_device(int device);
+void set_devices(const std::vector<int>& devices);
 
 }  // namespace hcc
 

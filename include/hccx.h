@@ -156,6 +156,16 @@ HCCX_API hccx_status_t hccx_lossless_ring_wire(const float* const* d_in, int p, 
                                                uint64_t* wire, void* stream);
 HCCX_API hccx_status_t hccx_lossless_ring_wire_host(const float* const* h_in, int p, uint64_t n, int collective,
                                                     uint64_t* wire, int device);
+/* Per-message payload bytes of the same ring (the reference's cost model
+ * charges each hop by its own message, collectives.cpp:53-62, :97-104):
+ * collective 0: hop[t*p + j] = bytes member j sends in round t (t < p-1);
+ * 1: hop[j] = bytes of shard j (compressed once, forwarded p-1 times);
+ * 2: the RS layout, then hop[(p-1)*p + k] = bytes of member k's reduced
+ * shard.  hop holds up to p*p entries.  Synchronises. */
+HCCX_API hccx_status_t hccx_lossless_ring_hops(const float* const* d_in, int p, uint64_t n, int collective,
+                                               uint64_t* hop, void* stream);
+HCCX_API hccx_status_t hccx_lossless_ring_hops_host(const float* const* h_in, int p, uint64_t n, int collective,
+                                                    uint64_t* hop, int device);
 
 /* ------------------------------------------- single-device ring (group) -- */
 /* All p members' buffers live on one device ("virtual ranks"): the value
@@ -299,6 +309,9 @@ HCCX_API hccx_status_t hccx_mcomm_broadcast_host(hccx_mcomm_t m, int root, const
                                                  uint64_t n, hccx_codec_t codec, double* device_seconds);
 HCCX_API hccx_status_t hccx_mcomm_p2p_host(hccx_mcomm_t m, int src, int dst, const float* h_in, float* h_out,
                                            uint64_t n, hccx_codec_t codec, double* device_seconds);
+
+/* CUDA devices visible to this process (0 when none). */
+HCCX_API int hccx_device_count(void);
 
 /* Kernel launches issued by this library since it was loaded. */
 HCCX_API uint64_t hccx_launch_count(void);

@@ -61,6 +61,9 @@ hccx_lossless_decompress_host = _sig("hccx_lossless_decompress_host", _st, _p, _
 hccx_lossless_ring_wire = _sig("hccx_lossless_ring_wire", _st, _pp, C.c_int, _u64, C.c_int, C.POINTER(_u64), _p)
 hccx_lossless_ring_wire_host = _sig("hccx_lossless_ring_wire_host", _st, _pp, C.c_int, _u64, C.c_int,
                                     C.POINTER(_u64), C.c_int)
+hccx_lossless_ring_hops = _sig("hccx_lossless_ring_hops", _st, _pp, C.c_int, _u64, C.c_int, C.POINTER(_u64), _p)
+hccx_lossless_ring_hops_host = _sig("hccx_lossless_ring_hops_host", _st, _pp, C.c_int, _u64, C.c_int,
+                                    C.POINTER(_u64), C.c_int)
 hccx_group_create = _sig("hccx_group_create", _st, C.c_int, C.c_int, C.POINTER(_p))
 hccx_group_destroy = _sig("hccx_group_destroy", _st, _p)
 hccx_group_allreduce = _sig("hccx_group_allreduce", _st, _p, _pp, _pp, _u64, Codec, C.c_int, _p)
@@ -103,6 +106,7 @@ hccx_mcomm_allgather_host = _sig("hccx_mcomm_allgather_host", _st, _p, _pp, _pp,
 hccx_mcomm_broadcast_host = _sig("hccx_mcomm_broadcast_host", _st, _p, C.c_int, _p, _pp, _u64, Codec, _dp)
 hccx_mcomm_p2p_host = _sig("hccx_mcomm_p2p_host", _st, _p, C.c_int, C.c_int, _p, _p, _u64, Codec, _dp)
 hccx_launch_count = _sig("hccx_launch_count", _u64)
+hccx_device_count = _sig("hccx_device_count", C.c_int)
 
 #: every symbol include/hccx.h declares (checked by tests/test_abi.py)
 EXPORTED = [n for n in dir() if n.startswith("hccx_")]

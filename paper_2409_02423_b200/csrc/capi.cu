@@ -156,6 +156,11 @@ extern "C" hccx_status_t hccx_chunk_count(hccx_codec_t codec, uint64_t n, uint64
 
 extern "C" uint64_t hccx_launch_count(void) { return launch_count(); }
 
+extern "C" int hccx_device_count(void) {
+  int n = 0;
+  return cudaGetDeviceCount(&n) == cudaSuccess ? n : 0;
+}
+
 // -------------------------------------------------------------- codec ----
 
 extern "C" hccx_status_t hccx_compress(hccx_codec_t codec, const float* d_in, uint64_t n,

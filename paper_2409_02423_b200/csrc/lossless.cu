@@ -589,45 +589,65 @@ extern "C" hccx_status_t hccx_lossless_decompress_host(const uint8_t* h_in, uint
 }
 
 // Ring wire bytes under LosslessPredictor (see hccx.h).
-extern "C" hccx_status_t hccx_lossless_ring_wire(const float* const* d_in, int p, uint64_t n, int collective,
-                                                 uint64_t* wire, void* stream) {
-  if (!wire || !d_in || p < 1 || p > 16 || collective < 0 || collective > 2) return HCCX_ERR_INVALID_ARGUMENT;
-  *wire = 0;
-  if (p == 1 || n == 0) return HCCX_OK;
+extern "C" hccx_status_t hccx_lossless_ring_hops(const float* const* d_in, int p, uint64_t n, int collective,
+                                                 uint64_t* hop, void* stream) {
+  if (!hop || !d_in || p < 1 || p > 16 || collective < 0 || collective > 2) return HCCX_ERR_INVALID_ARGUMENT;
+  if (p == 1) return HCCX_OK;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   uint64_t sz = 0;
   hccx_status_t r = HCCX_OK;
-  if (collective == 1) {  // allgather: shard j's payload crosses p-1 hops (collectives.cpp:94-106)
+  if (collective == 1) {  // allgather: shard j is compressed once (collectives.cpp:77-84)
     for (int j = 0; j < p && r == HCCX_OK; ++j) {
-      r = hccx_lossless_size(d_in[j], n, &sz, stream);
-      *wire += static_cast<uint64_t>(p - 1) * sz;
+      r = n ? hccx_lossless_size(d_in[j], n, &sz, stream) : HCCX_OK;
+      hop[j] = n ? sz : 0;
     }
     return r;
   }
   if (n % p) return HCCX_ERR_BAD_CHUNKING;
   const uint64_t c = n / p;
+  const uint64_t nrs = static_cast<uint64_t>(p - 1) * p;
+  if (c == 0) {
+    for (uint64_t i = 0; i < nrs + (collective == 2 ? p : 0); ++i) hop[i] = 0;
+    return HCCX_OK;
+  }
   float* part = nullptr;
   if (cudaMalloc(&part, 4 * c) != cudaSuccess) return HCCX_ERR_CUDA;
   for (int k = 0; k < p && r == HCCX_OK; ++k) {
-    // chunk k: round-0 message is member k+1's chunk; each hop folds the next member in
+    // chunk k: the round-t message is sent by member (k+1+t) mod p and holds
+    // the fold of members k+1 .. k+1+t (collectives.cpp:34-61)
     if (cudaMemcpyAsync(part, d_in[(k + 1) % p] + k * c, 4 * c, cudaMemcpyDeviceToDevice, st) != cudaSuccess) {
       r = HCCX_ERR_CUDA;
       break;
     }
     for (int t = 0; t < p - 1 && r == HCCX_OK; ++t) {
       r = hccx_lossless_size(part, c, &sz, stream);
-      *wire += sz;
+      hop[static_cast<uint64_t>(t) * p + (k + 1 + t) % p] = sz;
       ll_fold_kernel<<<grid_for(c, 256 * 4), 256, 0, st>>>(part, d_in[(k + 2 + t) % p] + k * c, c);
       count_launch();
     }
-    if (r == HCCX_OK && collective == 2) {  // allreduce: the folded shard crosses p-1 allgather hops
+    if (r == HCCX_OK && collective == 2) {  // allreduce: member k's reduced shard, compressed once
       r = hccx_lossless_size(part, c, &sz, stream);
-      *wire += static_cast<uint64_t>(p - 1) * sz;
+      hop[nrs + k] = sz;
     }
   }
   cudaStreamSynchronize(st);
   cudaFree(part);
   return r;
+}
+
+extern "C" hccx_status_t hccx_lossless_ring_wire(const float* const* d_in, int p, uint64_t n, int collective,
+                                                 uint64_t* wire, void* stream) {
+  if (!wire || !d_in || p < 1 || p > 16 || collective < 0 || collective > 2) return HCCX_ERR_INVALID_ARGUMENT;
+  *wire = 0;
+  if (p == 1 || n == 0) return HCCX_OK;
+  uint64_t hop[16 * 16 + 16] = {};
+  const hccx_status_t r = hccx_lossless_ring_hops(d_in, p, n, collective, hop, stream);
+  if (r != HCCX_OK) return r;
+  const uint64_t nrs = collective == 1 ? 0 : static_cast<uint64_t>(p - 1) * p;
+  for (uint64_t i = 0; i < nrs; ++i) *wire += hop[i];
+  if (collective != 0)  // each compressed shard crosses p-1 allgather hops (collectives.cpp:94-106)
+    for (int k = 0; k < p; ++k) *wire += static_cast<uint64_t>(p - 1) * hop[nrs + k];
+  return HCCX_OK;
 }
 
 extern "C" hccx_status_t hccx_lossless_ring_wire_host(const float* const* h_in, int p, uint64_t n, int collective,
@@ -642,6 +662,22 @@ extern "C" hccx_status_t hccx_lossless_ring_wire_host(const float* const* h_in, 
       r = HCCX_ERR_CUDA;
   }
   if (r == HCCX_OK) r = hccx_lossless_ring_wire(d, p, n, collective, wire, nullptr);
+  for (int j = 0; j < p; ++j) cudaFree(d[j]);
+  return r;
+}
+
+extern "C" hccx_status_t hccx_lossless_ring_hops_host(const float* const* h_in, int p, uint64_t n, int collective,
+                                                      uint64_t* hop, int device) {
+  if (!hop || !h_in || p < 1 || p > 16) return HCCX_ERR_INVALID_ARGUMENT;
+  DeviceGuard g(device);
+  float* d[16] = {};
+  hccx_status_t r = HCCX_OK;
+  for (int j = 0; j < p && r == HCCX_OK; ++j) {
+    if (cudaMalloc(&d[j], 4 * (n ? n : 1)) != cudaSuccess ||
+        (n && cudaMemcpy(d[j], h_in[j], 4 * n, cudaMemcpyHostToDevice) != cudaSuccess))
+      r = HCCX_ERR_CUDA;
+  }
+  if (r == HCCX_OK) r = hccx_lossless_ring_hops(d, p, n, collective, hop, nullptr);
   for (int j = 0; j < p; ++j) cudaFree(d[j]);
   return r;
 }

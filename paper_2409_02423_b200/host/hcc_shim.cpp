@@ -24,6 +24,31 @@ namespace {
 
 int g_device = 0;
 
+// Collective members run on the NVLink engine's single-process communicator
+// (include/hccx.h hccx_mcomm_*), one per member->GPU map, grown on demand.
+std::vector<int>& device_list() {
+  static std::vector<int> devs = [] {
+    std::vector<int> d;
+    if (const char* e = std::getenv("HCC_B200_DEVICES")) {
+      std::string s(e);
+      for (size_t pos = 0; pos < s.size();) {
+        const size_t comma = s.find(',', pos);
+        const std::string tok = s.substr(pos, comma == std::string::npos ? std::string::npos : comma - pos);
+        if (!tok.empty()) d.push_back(std::stoi(tok));
+        if (comma == std::string::npos) break;
+        pos = comma + 1;
+      }
+    }
+    if (d.empty()) {
+      const int n = hccx_device_count();
+      for (int i = 0; i < (n > 0 ? n : 1); ++i) d.push_back(i);
+    }
+    return d;
+  }();
+  return devs;
+}
+
+
 [[noreturn]] void raise(hccx_status_t st, const std::string& what) {
   const std::string msg = what + ": " + hccx_status_string(st);
   switch (st) {
@@ -46,37 +71,12 @@ hccx_codec_t c_of(const CodecSpec& s) { return hccx_codec_t{static_cast<int32_t>
 
 bool lossless(const CodecSpec& s) { return s.kind == CodecKind::LosslessPredictor; }
 
-// Wire bytes of a ring collective: the size law, or under LosslessPredictor
-// the device-sized hop messages (hccx_lossless_ring_wire).
-std::uint64_t ring_wire(const CodecSpec& spec, const std::vector<const float*>& in, std::uint64_t n, int collective,
-                        std::uint64_t law_msgs, std::uint64_t law_n) {
-  if (!lossless(spec)) return law_msgs * wire_size_bytes(spec, law_n);
-  std::uint64_t w = 0;
-  check(hccx_lossless_ring_wire_host(in.data(), static_cast<int>(in.size()), n, collective, &w, g_device),
-        "lossless wire accounting");
-  return w;
-}
-
 std::uint64_t message_wire(const CodecSpec& spec, const FloatBuffer& buf) {
   if (!lossless(spec)) return wire_size_bytes(spec, buf.size());
   const float* two[2] = {buf.data(), buf.data()};
   std::uint64_t w = 0;  // allgather over 2 members = one hop of this buffer
   check(hccx_lossless_ring_wire_host(two, 2, buf.size(), 1, &w, g_device), "lossless wire accounting");
   return w / 2;
-}
-
-// one device group per communicator size, created on first use
-hccx_group_t group_for(int p) {
-  static std::mutex mu;
-  static std::map<std::pair<int, int>, hccx_group_t> groups;
-  std::lock_guard<std::mutex> lock(mu);
-  auto key = std::make_pair(p, g_device);
-  auto it = groups.find(key);
-  if (it != groups.end()) return it->second;
-  hccx_group_t g = nullptr;
-  check(hccx_group_create(p, g_device, &g), "group_create");
-  groups.emplace(key, g);
-  return g;
 }
 
 std::vector<const float*> cptrs(const std::vector<FloatBuffer>& v) {
@@ -91,23 +91,6 @@ std::vector<float*> mptrs(std::vector<FloatBuffer>& v) {
   return out;
 }
 
-// src/collectives.cpp:113-126
-void commit(SimClock& clock, const Communicator& comm, double dur, std::uint64_t raw_total,
-            std::uint64_t wire_total, int rounds, CommPath path, CollectiveKind kind) {
-  clock.sync_to_max(comm.ranks);
-  for (int r : comm.ranks) clock.advance(r, dur);
-  const auto p = static_cast<std::uint64_t>(comm.size());
-  TraceEvent e;
-  e.path = path;
-  e.collective = kind;
-  e.comm_size = comm.size();
-  e.raw_bytes = raw_total / p;
-  e.wire_bytes = wire_total / p;
-  e.duration_s = dur;
-  e.round_count = rounds;
-  clock.record(e);
-}
-
 // std::stoi with the reference's error mapping (src/codec.cpp:31-45)
 int parse_rate(const std::string& s, const std::string& field, const std::string& whole) {
   try {
@@ -119,7 +102,15 @@ int parse_rate(const std::string& s, const std::string& field, const std::string
 
 }  // namespace
 
-void set_device(int device) { g_device = device; }
+void set_device(int device) {
+  g_device = device;
+  device_list() = {device};
+}
+void set_devices(const std::vector<int>& devices) {
+  if (devices.empty()) throw Error("set_devices: empty device list");
+  g_device = devices[0];
+  device_list() = devices;
+}
 
 // ------------------------------------------------------------------ codec --
 
@@ -270,14 +261,47 @@ const char* to_string(CollectiveKind c) {
 
 // ------------------------------------------------------------ topology --
 
+void Topology::validate() const {
+  auto need = [](bool ok, const char* field, const char* what) {
+    if (!ok) throw ConfigError(field, what);
+  };
+  need(num_nodes >= 1, "topology.num_nodes", "must be >= 1");
+  need(gpus_per_node >= 1, "topology.gpus_per_node", "must be >= 1");
+  need(intra_bw > 0, "topology.intra_bw", "must be > 0");
+  need(inter_bw > 0, "topology.inter_bw", "must be > 0");
+  need(intra_lat > 0, "topology.intra_lat", "must be > 0");
+  need(inter_lat > 0, "topology.inter_lat", "must be > 0");
+  need(codec_bw > 0, "topology.codec_bw", "must be > 0");
+  need(compute_flops > 0, "topology.compute_flops", "must be > 0");
+}
+
 Topology Topology::lassen_like(int n) { return Topology{n, 4, 75.0e9, 12.5e9, 2.0e-6, 5.0e-6, 400.0e9, 7.0e12}; }
 Topology Topology::desk_2x2(int n) { return Topology{n, 2, 16.0e9, 1.25e9, 5.0e-6, 20.0e-6, 50.0e9, 1.0e12}; }
-Topology Topology::b200_box(int g) { return Topology{1, g, 900.0e9, 900.0e9, 2.0e-6, 2.0e-6, 0.0, 0.0}; }
+// codec_bw: fixed-rate r8 compress on one B200, 4.05e12 uncompressed B/s
+// (bench.py N=1, profiles/r02_bench_n1.json); compute_flops: fp32 CUDA-core
+// peak, 148 SMs x 128 lanes x 2 x 1.965 GHz (the toy trainer's matmuls are
+// fp32); intra: NVLink 5, 900 GB/s per direction, ~2 us flag latency.
+Topology Topology::b200_box(int g) { return Topology{1, g, 900.0e9, 900.0e9, 2.0e-6, 2.0e-6, 4.05e12, 74.4e12}; }
 Topology Topology::preset(const std::string& name, int n) {
   if (name == "lassen-like") return lassen_like(n);
   if (name == "desk-2x2") return desk_2x2(n);
   if (name == "b200-box") return b200_box(8 * n);
-  throw ConfigError("topology.preset", "unknown preset '" + name + "'");
+  throw ConfigError("topology.preset", "unknown preset '" + name + "' (expected lassen-like | desk-2x2 | b200-box)");
+}
+
+LinkClass link_class(const Topology& topo, int a, int b) {
+  if (a == b) return LinkClass::SelfLoop;
+  return topo.node_of(a) == topo.node_of(b) ? LinkClass::IntraNode : LinkClass::InterNode;
+}
+
+double transfer_time(const Topology& topo, std::uint64_t bytes, LinkClass link) {
+  if (link == LinkClass::SelfLoop) return 0.0;
+  const bool intra = link == LinkClass::IntraNode;
+  return (intra ? topo.intra_lat : topo.inter_lat) + static_cast<double>(bytes) / (intra ? topo.intra_bw : topo.inter_bw);
+}
+
+double codec_time(const Topology& topo, std::uint64_t raw_bytes, const CodecSpec& spec) {
+  return spec.kind == CodecKind::Identity ? 0.0 : static_cast<double>(raw_bytes) / topo.codec_bw;
 }
 
 double SimClock::max_time() const { return clock_.empty() ? 0.0 : *std::max_element(clock_.begin(), clock_.end()); }
@@ -310,13 +334,139 @@ void write_trace_csv(std::ostream& os, const std::vector<TraceEvent>& trace) {
 
 // ------------------------------------------------------------ collectives --
 
+namespace {
+
+std::vector<int> member_devices(const std::vector<int>& ranks) {
+  const auto& devs = device_list();
+  std::vector<int> out;
+  for (int r : ranks) out.push_back(devs[static_cast<size_t>(r) % devs.size()]);
+  return out;
+}
+
+hccx_mcomm_t mcomm_for(const std::vector<int>& devices, std::uint64_t max_n) {
+  static std::mutex mu;
+  static std::map<std::vector<int>, std::pair<hccx_mcomm_t, std::uint64_t>> cache;
+  std::lock_guard<std::mutex> lock(mu);
+  auto& slot = cache[devices];
+  if (slot.first && slot.second >= max_n) return slot.first;
+  if (slot.first) hccx_mcomm_destroy(slot.first);
+  slot = {nullptr, 0};
+  const std::uint64_t cap = std::max<std::uint64_t>({max_n, 2 * slot.second, 1u << 16});
+  hccx_mcomm_t m = nullptr;
+  check(hccx_mcomm_create(static_cast<int>(devices.size()), devices.data(), cap, &m), "mcomm_create");
+  slot = {m, cap};
+  return m;
+}
+
+// The reference's per-collective cost record (src/collectives.cpp:9-14).
+struct PhaseCost {
+  double duration = 0;
+  std::uint64_t raw_total = 0, wire_total = 0;
+  int rounds = 0;
+};
+
+// Ring reduce-scatter cost (src/collectives.cpp:34-64): every round's
+// duration is its slowest hop; msg(round, j) = payload member j sends.
+template <class Msg>
+PhaseCost rs_cost(const SimClock& clock, const Communicator& comm, const CodecSpec& spec, std::uint64_t chunk,
+                  Msg&& msg) {
+  const int p = comm.size();
+  const std::uint64_t raw_msg = 4 * chunk;
+  const Topology& t = clock.topology();
+  PhaseCost cost;
+  for (int round = 0; round < p - 1; ++round) {
+    double round_dur = 0;
+    for (int j = 0; j < p; ++j) {
+      const std::uint64_t payload = msg(round, j);
+      const double hop = codec_time(t, raw_msg, spec) +
+                         transfer_time(t, payload, link_class(t, comm.ranks[j], comm.ranks[(j + 1) % p])) +
+                         codec_time(t, raw_msg, spec);
+      round_dur = std::max(round_dur, hop);
+      cost.raw_total += raw_msg;
+      cost.wire_total += payload;
+    }
+    cost.duration += round_dur;
+  }
+  cost.rounds = p - 1;
+  return cost;
+}
+
+// Ring allgather cost (src/collectives.cpp:93-109): shard c, compressed once
+// at its origin, forwarded by member j in round (j - c) mod p.
+template <class Shard>
+PhaseCost ag_cost(const SimClock& clock, const Communicator& comm, const CodecSpec& spec, std::uint64_t chunk,
+                  Shard&& shard) {
+  const int p = comm.size();
+  const std::uint64_t raw_msg = 4 * chunk;
+  const Topology& t = clock.topology();
+  PhaseCost cost;
+  for (int round = 0; round < p - 1; ++round) {
+    double round_dur = 0;
+    for (int j = 0; j < p; ++j) {
+      const std::uint64_t payload = shard(((j - round) % p + p) % p);
+      double hop = transfer_time(t, payload, link_class(t, comm.ranks[j], comm.ranks[(j + 1) % p])) +
+                   codec_time(t, raw_msg, spec);
+      if (round == 0) hop += codec_time(t, raw_msg, spec);
+      round_dur = std::max(round_dur, hop);
+      cost.raw_total += raw_msg;
+      cost.wire_total += payload;
+    }
+    cost.duration += round_dur;
+  }
+  cost.rounds = p - 1;
+  return cost;
+}
+
+// Per-message payload bytes: the size law, or the device-sized messages of
+// the LosslessPredictor ring (hccx_lossless_ring_hops).
+std::vector<std::uint64_t> lossless_hops(const std::vector<const float*>& in, std::uint64_t n, int collective) {
+  const int p = static_cast<int>(in.size());
+  std::vector<std::uint64_t> hop(static_cast<size_t>(p) * p + p, 0);
+  check(hccx_lossless_ring_hops_host(in.data(), p, n, collective, hop.data(), g_device), "lossless wire accounting");
+  return hop;
+}
+
+// src/collectives.cpp:113-126, plus the measured device time.
+void commit(SimClock& clock, const Communicator& comm, const PhaseCost& cost, double device_s, CommPath path,
+            CollectiveKind kind) {
+  clock.sync_to_max(comm.ranks);
+  for (int r : comm.ranks) clock.advance(r, cost.duration);
+  const auto p = static_cast<std::uint64_t>(comm.size());
+  TraceEvent e;
+  e.path = path;
+  e.collective = kind;
+  e.comm_size = comm.size();
+  e.raw_bytes = cost.raw_total / p;
+  e.wire_bytes = cost.wire_total / p;
+  e.duration_s = cost.duration;
+  e.round_count = cost.rounds;
+  e.device_s = device_s;
+  clock.record(e);
+}
+
+void check_ranks(const SimClock& clock, const Communicator& comm, const char* what) {
+  if (comm.ranks.empty()) throw Error(std::string(what) + ": empty communicator");
+  for (int r : comm.ranks)
+    if (r < 0 || r >= clock.topology().world_size()) throw Error(std::string(what) + ": rank out of range");
+}
+
+}  // namespace
+
 FloatBuffer p2p(SimClock& clock, int src, int dst, const FloatBuffer& buf, const CodecSpec& spec, CommPath path) {
   if (src == dst) throw Error("p2p: src == dst");
   const std::uint64_t n = buf.size();
   const std::uint64_t wire = message_wire(spec, buf);
   FloatBuffer out(n);
-  double dur = 0.0;
-  if (n) check(hccx_group_p2p_host(group_for(2), buf.data(), out.data(), n, c_of(spec), &dur), "p2p");
+  double dev_s = 0.0;
+  if (n) {
+    hccx_mcomm_t m = mcomm_for(member_devices({src, dst}), n);
+    check(hccx_mcomm_p2p_host(m, 0, 1, buf.data(), out.data(), n, c_of(spec), &dev_s), "p2p");
+  }
+  // src/collectives.cpp:133-151
+  const Topology& t = clock.topology();
+  const std::uint64_t raw = 4 * n;
+  const double dur = codec_time(t, raw, spec) + transfer_time(t, wire, link_class(t, src, dst)) +
+                     codec_time(t, raw, spec);
   const int pair[2] = {src, dst};
   clock.sync_to_max(pair);
   clock.advance(src, dur);
@@ -325,10 +475,11 @@ FloatBuffer p2p(SimClock& clock, int src, int dst, const FloatBuffer& buf, const
   e.path = path;
   e.collective = CollectiveKind::P2P;
   e.comm_size = 2;
-  e.raw_bytes = 4 * n;
+  e.raw_bytes = raw;
   e.wire_bytes = wire;
   e.duration_s = dur;
   e.round_count = 1;
+  e.device_s = dev_s;
   clock.record(e);
   return out;
 }
@@ -336,8 +487,9 @@ FloatBuffer p2p(SimClock& clock, int src, int dst, const FloatBuffer& buf, const
 std::vector<FloatBuffer> ring_reduce_scatter(SimClock& clock, const Communicator& comm,
                                              const std::vector<FloatBuffer>& inputs, const CodecSpec& spec,
                                              CommPath path) {
+  check_ranks(clock, comm, "reduce_scatter");
   const int p = comm.size();
-  if (p < 1 || static_cast<int>(inputs.size()) != p) throw Error("reduce_scatter: one input per member");
+  if (static_cast<int>(inputs.size()) != p) throw Error("reduce_scatter: one input per member");
   const std::size_t n = inputs[0].size();
   if (n % p != 0)
     throw BadChunkingError("reduce_scatter: length " + std::to_string(n) + " not divisible by " + std::to_string(p));
@@ -348,19 +500,27 @@ std::vector<FloatBuffer> ring_reduce_scatter(SimClock& clock, const Communicator
   std::vector<FloatBuffer> shards(p, FloatBuffer(c));
   auto in = cptrs(inputs);
   auto out = mptrs(shards);
-  double dur = 0.0;
-  check(hccx_group_reduce_scatter_host(group_for(p), in.data(), out.data(), n, c_of(spec), &dur), "reduce_scatter");
-  const std::uint64_t rounds = p - 1;
-  commit(clock, comm, dur, rounds * p * 4 * c, ring_wire(spec, in, n, 0, rounds * p, c), p - 1,
-         path, CollectiveKind::ReduceScatter);
+  double dev_s = 0.0;
+  hccx_mcomm_t m = mcomm_for(member_devices(comm.ranks), n);
+  check(hccx_mcomm_reduce_scatter_host(m, in.data(), out.data(), n, c_of(spec), &dev_s), "reduce_scatter");
+  PhaseCost cost;
+  if (lossless(spec)) {
+    const auto hop = lossless_hops(in, n, 0);
+    cost = rs_cost(clock, comm, spec, c, [&](int r, int j) { return hop[static_cast<size_t>(r) * p + j]; });
+  } else {
+    const std::uint64_t w = wire_size_bytes(spec, c);
+    cost = rs_cost(clock, comm, spec, c, [&](int, int) { return w; });
+  }
+  commit(clock, comm, cost, dev_s, path, CollectiveKind::ReduceScatter);
   return shards;
 }
 
 std::vector<FloatBuffer> ring_allgather(SimClock& clock, const Communicator& comm,
                                         const std::vector<FloatBuffer>& shards, const CodecSpec& spec,
                                         CommPath path) {
+  check_ranks(clock, comm, "allgather");
   const int p = comm.size();
-  if (p < 1 || static_cast<int>(shards.size()) != p) throw Error("allgather: one shard per member");
+  if (static_cast<int>(shards.size()) != p) throw Error("allgather: one shard per member");
   const std::size_t c = shards[0].size();
   for (const auto& s : shards)
     if (s.size() != c) throw BadChunkingError("allgather: mismatched shard lengths");
@@ -368,18 +528,26 @@ std::vector<FloatBuffer> ring_allgather(SimClock& clock, const Communicator& com
   std::vector<FloatBuffer> outs(p, FloatBuffer(c * p));
   auto in = cptrs(shards);
   auto out = mptrs(outs);
-  double dur = 0.0;
-  check(hccx_group_allgather_host(group_for(p), in.data(), out.data(), c, c_of(spec), &dur), "allgather");
-  const std::uint64_t rounds = p - 1;
-  commit(clock, comm, dur, rounds * p * 4 * c, ring_wire(spec, in, c, 1, rounds * p, c), p - 1,
-         path, CollectiveKind::AllGather);
+  double dev_s = 0.0;
+  hccx_mcomm_t m = mcomm_for(member_devices(comm.ranks), c * p);
+  check(hccx_mcomm_allgather_host(m, in.data(), out.data(), c, c_of(spec), &dev_s), "allgather");
+  PhaseCost cost;
+  if (lossless(spec)) {
+    const auto hop = lossless_hops(in, c, 1);
+    cost = ag_cost(clock, comm, spec, c, [&](int s) { return hop[s]; });
+  } else {
+    const std::uint64_t w = wire_size_bytes(spec, c);
+    cost = ag_cost(clock, comm, spec, c, [&](int) { return w; });
+  }
+  commit(clock, comm, cost, dev_s, path, CollectiveKind::AllGather);
   return outs;
 }
 
 std::vector<FloatBuffer> allreduce(SimClock& clock, const Communicator& comm, const std::vector<FloatBuffer>& inputs,
                                    const CodecSpec& spec, CommPath path, ReduceMode mode) {
+  check_ranks(clock, comm, "allreduce");
   const int p = comm.size();
-  if (p < 1 || static_cast<int>(inputs.size()) != p) throw Error("allreduce: one input per member");
+  if (static_cast<int>(inputs.size()) != p) throw Error("allreduce: one input per member");
   const std::size_t n = inputs[0].size();
   if (n % p != 0)
     throw BadChunkingError("allreduce: length " + std::to_string(n) + " not divisible by " + std::to_string(p));
@@ -390,28 +558,62 @@ std::vector<FloatBuffer> allreduce(SimClock& clock, const Communicator& comm, co
   std::vector<FloatBuffer> outs(p, FloatBuffer(n));
   auto in = cptrs(inputs);
   auto out = mptrs(outs);
-  double dur = 0.0;
-  check(hccx_group_allreduce_host(group_for(p), in.data(), out.data(), n, c_of(spec),
-                                  mode == ReduceMode::Average ? HCCX_AVERAGE : HCCX_SUM, &dur),
+  double dev_s = 0.0;
+  hccx_mcomm_t m = mcomm_for(member_devices(comm.ranks), n);
+  check(hccx_mcomm_allreduce_host(m, in.data(), out.data(), n, c_of(spec),
+                                  mode == ReduceMode::Average ? HCCX_AVERAGE : HCCX_SUM, &dev_s),
         "allreduce");
-  const std::uint64_t rounds = p - 1;
-  commit(clock, comm, dur, 2 * rounds * p * 4 * c, ring_wire(spec, in, n, 2, 2 * rounds * p, c),
-         2 * (p - 1), path, CollectiveKind::AllReduce);
+  // src/collectives.cpp:219-246: RS cost + AG cost of the reduced shards
+  PhaseCost rs, ag;
+  if (lossless(spec)) {
+    const auto hop = lossless_hops(in, n, 2);
+    const size_t nrs = static_cast<size_t>(p - 1) * p;
+    rs = rs_cost(clock, comm, spec, c, [&](int r, int j) { return hop[static_cast<size_t>(r) * p + j]; });
+    ag = ag_cost(clock, comm, spec, c, [&](int s) { return hop[nrs + s]; });
+  } else {
+    const std::uint64_t w = wire_size_bytes(spec, c);
+    rs = rs_cost(clock, comm, spec, c, [&](int, int) { return w; });
+    ag = ag_cost(clock, comm, spec, c, [&](int) { return w; });
+  }
+  PhaseCost total;
+  total.duration = rs.duration + ag.duration;
+  total.raw_total = rs.raw_total + ag.raw_total;
+  total.wire_total = rs.wire_total + ag.wire_total;
+  total.rounds = rs.rounds + ag.rounds;
+  commit(clock, comm, total, dev_s, path, CollectiveKind::AllReduce);
   return outs;
 }
 
 std::vector<FloatBuffer> broadcast(SimClock& clock, const Communicator& comm, int root, const FloatBuffer& buf,
                                    const CodecSpec& spec, CommPath path) {
+  check_ranks(clock, comm, "broadcast");
   const int p = comm.size();
   if (root < 0 || root >= p) throw Error("broadcast: root out of range");
   if (p == 1) return {buf};
   const std::uint64_t n = buf.size();
   std::vector<FloatBuffer> outs(p, FloatBuffer(n));
   auto out = mptrs(outs);
-  double dur = 0.0;
-  if (n) check(hccx_group_broadcast_host(group_for(p), root, buf.data(), out.data(), n, c_of(spec), &dur), "broadcast");
-  const std::uint64_t rounds = p - 1;
-  commit(clock, comm, dur, rounds * 4 * n, rounds * message_wire(spec, buf), p - 1, path, CollectiveKind::Broadcast);
+  double dev_s = 0.0;
+  if (n) {
+    hccx_mcomm_t m = mcomm_for(member_devices(comm.ranks), n);
+    check(hccx_mcomm_broadcast_host(m, root, buf.data(), out.data(), n, c_of(spec), &dev_s), "broadcast");
+  }
+  // By analogy with the allgather of one shard: the
+  // root's payload crosses p-1 ring hops.
+  const std::uint64_t w = message_wire(spec, buf);
+  const Topology& t = clock.topology();
+  const std::uint64_t raw = 4 * n;
+  PhaseCost cost;
+  for (int round = 0; round < p - 1; ++round) {
+    const int j = ((root + round) % p + p) % p;
+    double hop = transfer_time(t, w, link_class(t, comm.ranks[j], comm.ranks[(j + 1) % p])) + codec_time(t, raw, spec);
+    if (round == 0) hop += codec_time(t, raw, spec);
+    cost.duration += hop;
+    cost.raw_total += raw;
+    cost.wire_total += w;
+  }
+  cost.rounds = p - 1;  // commit() reports the per-rank share (total / p), like the group accounting
+  commit(clock, comm, cost, dev_s, path, CollectiveKind::Broadcast);
   return outs;
 }
 
