@@ -20,20 +20,39 @@ if [ ! -d "$REF/tests" ]; then
   echo "refsuite: $REF absent, keeping the prebuilt $OUT/hcc_ref_tests"
   exit 0
 fi
-mkdir -p "$OUT"
-CXX="${CXX:-g++}"
-SRCS=("$REF"/tests/test_*.cpp "$REF"/tests/support/*.cpp "$REF/src/toymodel.cpp" "$REF/src/linalg.cpp"
-      "$ROOT/tests/cpp/gtest/gtest_main.cpp")
-OBJS=()
-for s in "${SRCS[@]}"; do
-  o="$OUT/$(basename "${s%.cpp}").o"
-  OBJS+=("$o")
-  if [ ! -f "$o" ] || [ "$s" -nt "$o" ] || [ "$ROOT/include/hcc/hcc_b200.hpp" -nt "$o" ]; then
-    "$CXX" -std=c++20 -O2 -ffp-contract=off -w -I"$ROOT/include" -I"$ROOT/tests/cpp" -I"$REF/include" -I"$REF/tests" \
-      -c "$s" -o "$o" &
-  fi
-done
-wait
+CXX=g++  # the system g++ (libgomp for the reference library; $CXX may point elsewhere)
+
+# compile <objdir> <stamp-header> <flags...> -- <sources...>
+compile() {
+  local dir="$1" stamp="$2"
+  shift 2
+  local flags=()
+  while [ "$1" != "--" ]; do flags+=("$1"); shift; done
+  shift
+  mkdir -p "$dir"
+  OBJS=()
+  for s in "$@"; do
+    local o="$dir/$(basename "${s%.cpp}").o"
+    OBJS+=("$o")
+    if [ ! -f "$o" ] || [ "$s" -nt "$o" ] || [ "$stamp" -nt "$o" ]; then
+      "$CXX" -std=c++20 -O2 -ffp-contract=off -w "${flags[@]}" -c "$s" -o "$o" &
+    fi
+  done
+  wait
+}
+
+SUITE=("$REF"/tests/test_*.cpp "$REF"/tests/support/*.cpp "$ROOT/tests/cpp/gtest/gtest_main.cpp")
+
+# (1) the suite + the reference trainer against the B200 drop-in
+compile "$OUT" "$ROOT/include/hcc/hcc_b200.hpp" -I"$ROOT/include" -I"$ROOT/tests/cpp" -I"$REF/include" -I"$REF/tests" \
+  -- "${SUITE[@]}" "$REF/src/toymodel.cpp" "$REF/src/linalg.cpp"
 "$CXX" -o "$OUT/hcc_ref_tests" "${OBJS[@]}" -L"$ROOT/paper_2409_02423_b200" -lhcc_b200 -lhccx \
   -Wl,-rpath,'$ORIGIN/../../../paper_2409_02423_b200'
 echo "refsuite: built $OUT/hcc_ref_tests"
+
+# (2) the same suite against the reference's own library (every src/*.cpp,
+# OpenMP, CPU): its pass/fail record is what the drop-in must reproduce
+compile "$OUT/reflib" "$REF/include/hcc/codec.hpp" -fopenmp -I"$REF/include" -I"$ROOT/tests/cpp" -I"$REF/tests" -I"$REF/src" \
+  -- "${SUITE[@]}" "$REF"/src/*.cpp
+"$CXX" -fopenmp -o "$OUT/hcc_ref_tests_reflib" "${OBJS[@]}"
+echo "refsuite: built $OUT/hcc_ref_tests_reflib"
