@@ -93,7 +93,11 @@ def make_topology(cfg: Dict[str, Any]) -> Topology:
         return topo
     lay = cfg.get("layout", {})
     world = int(lay.get("dp", 1)) * int(lay.get("pp", 1)) * int(lay.get("tp", 1))
-    return Topology(int(t.get("num_nodes", 1)), int(t.get("gpus_per_node", world)))
+    # no preset: the given shape with one B200 box's link / codec / compute rates
+    nn = int(t.get("num_nodes", 1))
+    topo = Topology.b200_box(int(t.get("gpus_per_node", world)))
+    topo.num_nodes = nn
+    return topo
 
 
 def make_scheme(cfg: Dict[str, Any], name: str = "") -> SchemeTable:

@@ -273,6 +273,7 @@ class Trainer3D:
 
     def __init__(self, cfg: ToyModelConfig, layout: ParallelLayout, topo: Topology, scheme: SchemeTable,
                  zero: ZeroMode):
+        topo.validate()  # toymodel.cpp:128
         if layout.world() != topo.world_size():
             raise BadLayoutError("layout world does not match topology world")
         cfg.validate(layout)

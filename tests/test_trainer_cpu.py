@@ -83,7 +83,7 @@ def test_host_math_with_oracle_collectives(monkeypatch, case):
     g = np.load(GOLD)
     cfg = T.ToyModelConfig(**dict(SMALL_CFG, **over))
     world = dp * pp * tp
-    tr = T.Trainer3D(cfg, build_layout(dp, pp, tp, world), Topology(1, world), scheme_from_name(scheme),
+    tr = T.Trainer3D(cfg, build_layout(dp, pp, tp, world), Topology.b200_box(world), scheme_from_name(scheme),
                      T.ZeroMode(zero))
     met = tr.run()
     assert met.steps_completed == int(g[f"{name}__steps_completed"])

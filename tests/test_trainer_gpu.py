@@ -31,7 +31,7 @@ def _run(over, dp, pp, tp, scheme, zero, trace=None):
 
     cfg = T.ToyModelConfig(**dict(SMALL_CFG, **over))
     world = dp * pp * tp
-    tr = T.Trainer3D(cfg, build_layout(dp, pp, tp, world), Topology(1, world), scheme_from_name(scheme),
+    tr = T.Trainer3D(cfg, build_layout(dp, pp, tp, world), Topology.b200_box(world), scheme_from_name(scheme),
                      T.ZeroMode(zero))
     met = tr.run()
     if trace is not None:
