@@ -165,6 +165,7 @@ extern "C" int hccx_device_count(void) {
 
 extern "C" hccx_status_t hccx_compress(hccx_codec_t codec, const float* d_in, uint64_t n,
                                        uint8_t* d_out, uint32_t* d_err, void* stream) {
+  HCCX_NVTX("hccx_compress");
   hccx_status_t st = check_codec(codec);
   if (st != HCCX_OK) return st;
   if (codec.kind == HCCX_CODEC_LOSSLESS) return HCCX_ERR_UNSUPPORTED;
@@ -184,6 +185,7 @@ extern "C" hccx_status_t hccx_compress(hccx_codec_t codec, const float* d_in, ui
 
 extern "C" hccx_status_t hccx_decompress(hccx_codec_t codec, const uint8_t* d_in, uint64_t payload,
                                          uint64_t n, float* d_out, void* stream) {
+  HCCX_NVTX("hccx_decompress");
   hccx_status_t st = check_codec(codec);
   if (st != HCCX_OK) return st;
   if (codec.kind == HCCX_CODEC_LOSSLESS) return HCCX_ERR_UNSUPPORTED;
@@ -314,6 +316,7 @@ hccx_status_t host_codec(bool compress, hccx_codec_t codec, const void* h_in, ui
 
 extern "C" hccx_status_t hccx_compress_host(hccx_codec_t codec, const float* h_in, uint64_t n,
                                             uint8_t* h_out, int device) {
+  HCCX_NVTX("hccx_compress_host");
   hccx_status_t st = check_codec(codec);
   if (st != HCCX_OK) return st;
   if (codec.kind == HCCX_CODEC_LOSSLESS) return HCCX_ERR_UNSUPPORTED;
@@ -324,6 +327,7 @@ extern "C" hccx_status_t hccx_compress_host(hccx_codec_t codec, const float* h_i
 
 extern "C" hccx_status_t hccx_decompress_host(hccx_codec_t codec, const uint8_t* h_in, uint64_t payload,
                                               uint64_t n, float* h_out, int device) {
+  HCCX_NVTX("hccx_decompress_host");
   hccx_status_t st = check_codec(codec);
   if (st != HCCX_OK) return st;
   if (codec.kind == HCCX_CODEC_LOSSLESS) return HCCX_ERR_UNSUPPORTED;
@@ -474,6 +478,7 @@ extern "C" hccx_status_t hccx_group_destroy(hccx_group_t g) {
 
 extern "C" hccx_status_t hccx_group_allreduce(hccx_group_t g, const float* const* d_in, float* const* d_out,
                                               uint64_t n, hccx_codec_t codec, int mode, void* stream) {
+  HCCX_NVTX("hccx_group_allreduce");
   hccx_status_t st = check_group(g, codec);
   if (st != HCCX_OK) return st;
   const int p = g->p;
@@ -496,6 +501,7 @@ extern "C" hccx_status_t hccx_group_allreduce(hccx_group_t g, const float* const
 extern "C" hccx_status_t hccx_group_reduce_scatter(hccx_group_t g, const float* const* d_in,
                                                    float* const* d_shard, uint64_t n, hccx_codec_t codec,
                                                    void* stream) {
+  HCCX_NVTX("hccx_group_reduce_scatter");
   hccx_status_t st = check_group(g, codec);
   if (st != HCCX_OK) return st;
   const int p = g->p;
@@ -512,6 +518,7 @@ extern "C" hccx_status_t hccx_group_reduce_scatter(hccx_group_t g, const float* 
 
 extern "C" hccx_status_t hccx_group_allgather(hccx_group_t g, const float* const* d_shard, float* const* d_out,
                                               uint64_t shard_n, hccx_codec_t codec, void* stream) {
+  HCCX_NVTX("hccx_group_allgather");
   hccx_status_t st = check_group(g, codec);
   if (st != HCCX_OK) return st;
   const int p = g->p;
@@ -542,6 +549,7 @@ extern "C" hccx_status_t hccx_group_allgather(hccx_group_t g, const float* const
 
 extern "C" hccx_status_t hccx_group_broadcast(hccx_group_t g, int root, const float* d_in, float* const* d_out,
                                               uint64_t n, hccx_codec_t codec, void* stream) {
+  HCCX_NVTX("hccx_group_broadcast");
   hccx_status_t st = check_group(g, codec);
   if (st != HCCX_OK) return st;
   const int p = g->p;
@@ -576,6 +584,7 @@ extern "C" hccx_status_t hccx_group_broadcast(hccx_group_t g, int root, const fl
 
 extern "C" hccx_status_t hccx_group_p2p(hccx_group_t g, const float* d_in, float* d_out, uint64_t n,
                                         hccx_codec_t codec, void* stream) {
+  HCCX_NVTX("hccx_group_p2p");
   hccx_status_t st = check_group(g, codec);
   if (st != HCCX_OK) return st;
   DeviceGuard guard(g->device);
@@ -652,6 +661,7 @@ hccx_status_t d2h(float* h, const float* d, uint64_t n) {
 
 extern "C" hccx_status_t hccx_group_allreduce_host(hccx_group_t g, const float* const* h_in, float* const* h_out,
                                                    uint64_t n, hccx_codec_t codec, int mode, double* secs) {
+  HCCX_NVTX("hccx_group_allreduce_host");
   hccx_status_t st = check_group(g, codec);
   if (st != HCCX_OK) return st;
   if (n % static_cast<uint64_t>(g->p) != 0) return HCCX_ERR_BAD_CHUNKING;
@@ -674,6 +684,7 @@ extern "C" hccx_status_t hccx_group_allreduce_host(hccx_group_t g, const float* 
 extern "C" hccx_status_t hccx_group_reduce_scatter_host(hccx_group_t g, const float* const* h_in,
                                                         float* const* h_shard, uint64_t n, hccx_codec_t codec,
                                                         double* secs) {
+  HCCX_NVTX("hccx_group_reduce_scatter_host");
   hccx_status_t st = check_group(g, codec);
   if (st != HCCX_OK) return st;
   if (n % static_cast<uint64_t>(g->p) != 0) return HCCX_ERR_BAD_CHUNKING;
@@ -696,6 +707,7 @@ extern "C" hccx_status_t hccx_group_reduce_scatter_host(hccx_group_t g, const fl
 
 extern "C" hccx_status_t hccx_group_allgather_host(hccx_group_t g, const float* const* h_shard, float* const* h_out,
                                                    uint64_t shard_n, hccx_codec_t codec, double* secs) {
+  HCCX_NVTX("hccx_group_allgather_host");
   hccx_status_t st = check_group(g, codec);
   if (st != HCCX_OK) return st;
   DeviceGuard guard(g->device);
@@ -717,6 +729,7 @@ extern "C" hccx_status_t hccx_group_allgather_host(hccx_group_t g, const float* 
 
 extern "C" hccx_status_t hccx_group_broadcast_host(hccx_group_t g, int root, const float* h_in, float* const* h_out,
                                                    uint64_t n, hccx_codec_t codec, double* secs) {
+  HCCX_NVTX("hccx_group_broadcast_host");
   hccx_status_t st = check_group(g, codec);
   if (st != HCCX_OK) return st;
   DeviceGuard guard(g->device);
@@ -738,6 +751,7 @@ extern "C" hccx_status_t hccx_group_broadcast_host(hccx_group_t g, int root, con
 
 extern "C" hccx_status_t hccx_group_p2p_host(hccx_group_t g, const float* h_in, float* h_out, uint64_t n,
                                              hccx_codec_t codec, double* secs) {
+  HCCX_NVTX("hccx_group_p2p_host");
   hccx_status_t st = check_group(g, codec);
   if (st != HCCX_OK) return st;
   DeviceGuard guard(g->device);

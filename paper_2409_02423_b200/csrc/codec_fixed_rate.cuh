@@ -37,6 +37,8 @@ struct FixedRateCodec {
   static constexpr uint32_t kGroupBytes = 4 * kBlockBytes;  // 256 values
   static constexpr int kWords = (R + 3) / 4;                // lane chunk (R bytes) in words
   static constexpr bool kFastPath = (R % 4) == 0;
+  static constexpr bool kNeedsInit = false;
+  __device__ __forceinline__ static void kernel_init() {}
   static constexpr uint32_t kBias = 1u << (R - 1);
   static constexpr uint32_t kMask = R == 32 ? 0xffffffffu : ((1u << R) - 1u);
 

@@ -14,6 +14,8 @@ struct IdentityCodec {
   static constexpr uint32_t kGroupBytes = 4 * kGroupVals;
   static constexpr int kWords = 8;
   static constexpr bool kFastPath = true;
+  static constexpr bool kNeedsInit = false;
+  __device__ __forceinline__ static void kernel_init() {}
 
   __host__ __device__ static uint64_t wire_bytes(uint64_t n) { return 4 * n; }
   __host__ __device__ static uint32_t group_bytes_live(uint32_t live) { return 4 * live; }

@@ -142,6 +142,10 @@ struct ZfpRateCodec {
   static constexpr uint32_t kGroupBytes = 32 * R;
   static constexpr int kWords = (R + 3) / 4;
   static constexpr bool kFastPath = (R % 4) == 0;
+  // the plane-code tables live in shared memory: every kernel calls
+  // kernel_init() with all threads, then a CTA barrier, before coding
+  static constexpr bool kNeedsInit = true;
+  __device__ __forceinline__ static void kernel_init() { zfp_planes::lut_init(); }
 
   __host__ __device__ static uint64_t wire_bytes(uint64_t n) {
     return (((n + 3) / 4) * 4 * static_cast<uint64_t>(R) + 7) / 8;

@@ -111,6 +111,7 @@ struct hccx_comm {
 };
 
 extern "C" hccx_status_t hccx_comm_create(int rank, int nranks, int device, uint64_t max_n, hccx_comm_t* out) {
+  HCCX_NVTX("hccx_comm_create");
   if (!out || nranks < 1 || nranks > kMaxRanks || rank < 0 || rank >= nranks || max_n == 0)
     return HCCX_ERR_INVALID_ARGUMENT;
   DeviceGuard guard(device);
@@ -224,11 +225,8 @@ FusedParams base_params(hccx_comm* c, int op, uint64_t n_chunk, const float* in,
   P.err = c->d_err;
   P.timeout_ns = timeout_ns();
   P.max_grid = c->max_grid;
-  static const int dbg = [] {
-    const char* e = std::getenv("HCCX_DEBUG");
-    return e ? std::atoi(e) : 0;
-  }();
-  P.debug = dbg;
+  const char* dbg = std::getenv("HCCX_DEBUG");  // per call: A/B of development knobs in one process
+  P.debug = dbg ? std::atoi(dbg) : 0;
   static const uint32_t step_segs = [] {
     const char* e = std::getenv("HCCX_STEP_SEGS");
     const int v = e ? std::atoi(e) : 0;
@@ -447,6 +445,7 @@ hccx_status_t exec_rank(hccx_comm* c, hccx_codec_t codec, const RankWork& w, cud
 
 extern "C" hccx_status_t hccx_allreduce(hccx_comm_t c, const float* d_in, float* d_out, uint64_t n,
                                         hccx_codec_t codec, int mode, void* stream) {
+  HCCX_NVTX("hccx_allreduce");
   RankWork w;
   hccx_status_t st = plan_allreduce(c, d_in, d_out, n, codec, mode, w);
   return st != HCCX_OK ? st : exec_rank(c, codec, w, static_cast<cudaStream_t>(stream));
@@ -454,6 +453,7 @@ extern "C" hccx_status_t hccx_allreduce(hccx_comm_t c, const float* d_in, float*
 
 extern "C" hccx_status_t hccx_reduce_scatter(hccx_comm_t c, const float* d_in, float* d_shard, uint64_t n,
                                              hccx_codec_t codec, void* stream) {
+  HCCX_NVTX("hccx_reduce_scatter");
   RankWork w;
   hccx_status_t st = plan_reduce_scatter(c, d_in, d_shard, n, codec, w);
   return st != HCCX_OK ? st : exec_rank(c, codec, w, static_cast<cudaStream_t>(stream));
@@ -461,6 +461,7 @@ extern "C" hccx_status_t hccx_reduce_scatter(hccx_comm_t c, const float* d_in, f
 
 extern "C" hccx_status_t hccx_allgather(hccx_comm_t c, const float* d_shard, float* d_out, uint64_t shard_n,
                                         hccx_codec_t codec, void* stream) {
+  HCCX_NVTX("hccx_allgather");
   RankWork w;
   hccx_status_t st = plan_allgather(c, d_shard, d_out, shard_n, codec, w);
   return st != HCCX_OK ? st : exec_rank(c, codec, w, static_cast<cudaStream_t>(stream));
@@ -468,6 +469,7 @@ extern "C" hccx_status_t hccx_allgather(hccx_comm_t c, const float* d_shard, flo
 
 extern "C" hccx_status_t hccx_broadcast(hccx_comm_t c, int root, const float* d_in, float* d_out, uint64_t n,
                                         hccx_codec_t codec, void* stream) {
+  HCCX_NVTX("hccx_broadcast");
   RankWork w;
   hccx_status_t st = plan_broadcast(c, root, d_in, d_out, n, codec, w);
   return st != HCCX_OK ? st : exec_rank(c, codec, w, static_cast<cudaStream_t>(stream));
@@ -475,6 +477,7 @@ extern "C" hccx_status_t hccx_broadcast(hccx_comm_t c, int root, const float* d_
 
 extern "C" hccx_status_t hccx_p2p(hccx_comm_t c, int src, int dst, const float* d_in, float* d_out, uint64_t n,
                                   hccx_codec_t codec, void* stream) {
+  HCCX_NVTX("hccx_p2p");
   RankWork w;
   hccx_status_t st = plan_p2p(c, src, dst, d_in, d_out, n, codec, w);
   return st != HCCX_OK ? st : exec_rank(c, codec, w, static_cast<cudaStream_t>(stream));
@@ -573,6 +576,7 @@ hccx_status_t mcomm_check(hccx_mcomm* m, hccx_codec_t codec) {
 }  // namespace
 
 extern "C" hccx_status_t hccx_mcomm_create(int nmembers, const int* devices, uint64_t max_n, hccx_mcomm_t* out) {
+  HCCX_NVTX("hccx_mcomm_create");
   if (!out || !devices || nmembers < 1 || nmembers > kMaxRanks || max_n == 0) return HCCX_ERR_INVALID_ARGUMENT;
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess) return HCCX_ERR_CUDA;
@@ -645,6 +649,7 @@ extern "C" int hccx_mcomm_size(hccx_mcomm_t m) { return m ? m->p : 0; }
 
 extern "C" hccx_status_t hccx_mcomm_allreduce(hccx_mcomm_t m, const float* const* d_in, float* const* d_out,
                                               uint64_t n, hccx_codec_t codec, int mode, void* const* streams) {
+  HCCX_NVTX("hccx_mcomm_allreduce");
   hccx_status_t st = mcomm_check(m, codec);
   if (st != HCCX_OK) return st;
   if (n % static_cast<uint64_t>(m->p) != 0) return HCCX_ERR_BAD_CHUNKING;
@@ -656,6 +661,7 @@ extern "C" hccx_status_t hccx_mcomm_allreduce(hccx_mcomm_t m, const float* const
 
 extern "C" hccx_status_t hccx_mcomm_reduce_scatter(hccx_mcomm_t m, const float* const* d_in, float* const* d_shard,
                                                    uint64_t n, hccx_codec_t codec, void* const* streams) {
+  HCCX_NVTX("hccx_mcomm_reduce_scatter");
   hccx_status_t st = mcomm_check(m, codec);
   if (st != HCCX_OK) return st;
   if (n % static_cast<uint64_t>(m->p) != 0) return HCCX_ERR_BAD_CHUNKING;
@@ -667,6 +673,7 @@ extern "C" hccx_status_t hccx_mcomm_reduce_scatter(hccx_mcomm_t m, const float* 
 
 extern "C" hccx_status_t hccx_mcomm_allgather(hccx_mcomm_t m, const float* const* d_shard, float* const* d_out,
                                               uint64_t shard_n, hccx_codec_t codec, void* const* streams) {
+  HCCX_NVTX("hccx_mcomm_allgather");
   hccx_status_t st = mcomm_check(m, codec);
   if (st != HCCX_OK) return st;
   std::vector<RankWork> w(m->p);
@@ -677,6 +684,7 @@ extern "C" hccx_status_t hccx_mcomm_allgather(hccx_mcomm_t m, const float* const
 
 extern "C" hccx_status_t hccx_mcomm_broadcast(hccx_mcomm_t m, int root, const float* d_in, float* const* d_out,
                                               uint64_t n, hccx_codec_t codec, void* const* streams) {
+  HCCX_NVTX("hccx_mcomm_broadcast");
   hccx_status_t st = mcomm_check(m, codec);
   if (st != HCCX_OK) return st;
   if (root < 0 || root >= m->p) return HCCX_ERR_INVALID_ARGUMENT;
@@ -689,6 +697,7 @@ extern "C" hccx_status_t hccx_mcomm_broadcast(hccx_mcomm_t m, int root, const fl
 
 extern "C" hccx_status_t hccx_mcomm_p2p(hccx_mcomm_t m, int src, int dst, const float* d_in, float* d_out,
                                         uint64_t n, hccx_codec_t codec, void* const* streams) {
+  HCCX_NVTX("hccx_mcomm_p2p");
   hccx_status_t st = mcomm_check(m, codec);
   if (st != HCCX_OK) return st;
   if (src < 0 || src >= m->p || dst < 0 || dst >= m->p || src == dst) return HCCX_ERR_INVALID_ARGUMENT;
@@ -793,6 +802,7 @@ hccx_status_t mcomm_host_run(hccx_mcomm* m, const float* const* h_in, uint64_t i
 
 extern "C" hccx_status_t hccx_mcomm_allreduce_host(hccx_mcomm_t m, const float* const* h_in, float* const* h_out,
                                                    uint64_t n, hccx_codec_t codec, int mode, double* secs) {
+  HCCX_NVTX("hccx_mcomm_allreduce_host");
   hccx_status_t st = mcomm_check(m, codec);
   if (st != HCCX_OK) return st;
   if (n % static_cast<uint64_t>(m->p) != 0) return HCCX_ERR_BAD_CHUNKING;
@@ -804,6 +814,7 @@ extern "C" hccx_status_t hccx_mcomm_allreduce_host(hccx_mcomm_t m, const float* 
 extern "C" hccx_status_t hccx_mcomm_reduce_scatter_host(hccx_mcomm_t m, const float* const* h_in,
                                                         float* const* h_shard, uint64_t n, hccx_codec_t codec,
                                                         double* secs) {
+  HCCX_NVTX("hccx_mcomm_reduce_scatter_host");
   hccx_status_t st = mcomm_check(m, codec);
   if (st != HCCX_OK) return st;
   if (n % static_cast<uint64_t>(m->p) != 0) return HCCX_ERR_BAD_CHUNKING;
@@ -814,6 +825,7 @@ extern "C" hccx_status_t hccx_mcomm_reduce_scatter_host(hccx_mcomm_t m, const fl
 
 extern "C" hccx_status_t hccx_mcomm_allgather_host(hccx_mcomm_t m, const float* const* h_shard, float* const* h_out,
                                                    uint64_t shard_n, hccx_codec_t codec, double* secs) {
+  HCCX_NVTX("hccx_mcomm_allgather_host");
   hccx_status_t st = mcomm_check(m, codec);
   if (st != HCCX_OK) return st;
   return mcomm_host_run(m, h_shard, shard_n, -1, h_out, shard_n * m->p, std::vector<char>(m->p, 1), secs, [&] {
@@ -823,6 +835,7 @@ extern "C" hccx_status_t hccx_mcomm_allgather_host(hccx_mcomm_t m, const float* 
 
 extern "C" hccx_status_t hccx_mcomm_broadcast_host(hccx_mcomm_t m, int root, const float* h_in, float* const* h_out,
                                                    uint64_t n, hccx_codec_t codec, double* secs) {
+  HCCX_NVTX("hccx_mcomm_broadcast_host");
   hccx_status_t st = mcomm_check(m, codec);
   if (st != HCCX_OK) return st;
   if (root < 0 || root >= m->p) return HCCX_ERR_INVALID_ARGUMENT;
@@ -834,6 +847,7 @@ extern "C" hccx_status_t hccx_mcomm_broadcast_host(hccx_mcomm_t m, int root, con
 
 extern "C" hccx_status_t hccx_mcomm_p2p_host(hccx_mcomm_t m, int src, int dst, const float* h_in, float* h_out,
                                              uint64_t n, hccx_codec_t codec, double* secs) {
+  HCCX_NVTX("hccx_mcomm_p2p_host");
   hccx_status_t st = mcomm_check(m, codec);
   if (st != HCCX_OK) return st;
   if (src < 0 || src >= m->p || dst < 0 || dst >= m->p || src == dst) return HCCX_ERR_INVALID_ARGUMENT;

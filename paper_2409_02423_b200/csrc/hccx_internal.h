@@ -1,6 +1,7 @@
 // hccx_internal.h -- host helpers shared by capi.cu and comm.cu.
 #pragma once
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>  // header-only: ranges cost nothing unless a tool (nsys, ncu) is attached
 
 #include "hccx.h"
 #include "hccx_kernels.h"
@@ -14,6 +15,17 @@ void finalize_params(StepParams& p, CodecSel c, int op);
 void set_divisor(StepParams& p, int mode, int nranks);
 hccx_status_t run_step(CodecSel c, int op, StepParams& p, cudaStream_t s);
 hccx_status_t read_flag(uint32_t* d_err, cudaStream_t s);
+
+// NVTX range around one C-ABI entry point (the host side of a collective or
+// codec call: enqueue, or the whole call for the synchronous variants).
+class NvtxRange {
+ public:
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+#define HCCX_NVTX(name) ::hccx::NvtxRange hccx_nvtx_range_(name)
 
 // RAII: make `dev` current for the scope (no-op when dev < 0).
 class DeviceGuard {

@@ -456,6 +456,7 @@ thread_local Scratch t_scratch;
 using namespace hccx;
 
 extern "C" hccx_status_t hccx_lossless_size(const float* d_in, uint64_t n, uint64_t* bytes, void* stream) {
+  HCCX_NVTX("hccx_lossless_size");
   if (!bytes || (n && !d_in)) return HCCX_ERR_INVALID_ARGUMENT;
   if (n == 0) {
     *bytes = 0;
@@ -466,6 +467,7 @@ extern "C" hccx_status_t hccx_lossless_size(const float* d_in, uint64_t n, uint6
 
 extern "C" hccx_status_t hccx_lossless_compress(const float* d_in, uint64_t n, uint8_t* d_out, uint64_t capacity,
                                                 uint64_t* bytes, void* stream) {
+  HCCX_NVTX("hccx_lossless_compress");
   if (!bytes || (n && (!d_in || !d_out))) return HCCX_ERR_INVALID_ARGUMENT;
   if (n == 0) {
     *bytes = 0;
@@ -491,6 +493,7 @@ extern "C" hccx_status_t hccx_lossless_compress(const float* d_in, uint64_t n, u
 
 extern "C" hccx_status_t hccx_lossless_decompress(const uint8_t* d_in, uint64_t in_bytes, uint64_t n, float* d_out,
                                                   void* stream) {
+  HCCX_NVTX("hccx_lossless_decompress");
   if (n && (!d_in || !d_out)) return HCCX_ERR_INVALID_ARGUMENT;
   if (n == 0) return HCCX_OK;
   const uint64_t nch = (n + kChunk - 1) / kChunk;
@@ -549,6 +552,7 @@ extern "C" uint64_t hccx_lossless_max_bytes(uint64_t n) {
 
 extern "C" hccx_status_t hccx_lossless_compress_host(const float* h_in, uint64_t n, uint8_t* h_out,
                                                      uint64_t capacity, uint64_t* bytes, int device) {
+  HCCX_NVTX("hccx_lossless_compress_host");
   if (!bytes || (n && (!h_in || !h_out))) return HCCX_ERR_INVALID_ARGUMENT;
   if (n == 0) {
     *bytes = 0;
@@ -571,6 +575,7 @@ extern "C" hccx_status_t hccx_lossless_compress_host(const float* h_in, uint64_t
 
 extern "C" hccx_status_t hccx_lossless_decompress_host(const uint8_t* h_in, uint64_t bytes, uint64_t n, float* h_out,
                                                        int device) {
+  HCCX_NVTX("hccx_lossless_decompress_host");
   if (n && (!h_in || !h_out)) return HCCX_ERR_INVALID_ARGUMENT;
   if (n == 0) return HCCX_OK;
   DeviceGuard g(device);
@@ -591,6 +596,7 @@ extern "C" hccx_status_t hccx_lossless_decompress_host(const uint8_t* h_in, uint
 // Ring wire bytes under LosslessPredictor (see hccx.h).
 extern "C" hccx_status_t hccx_lossless_ring_hops(const float* const* d_in, int p, uint64_t n, int collective,
                                                  uint64_t* hop, void* stream) {
+  HCCX_NVTX("hccx_lossless_ring_hops");
   if (!hop || !d_in || p < 1 || p > 16 || collective < 0 || collective > 2) return HCCX_ERR_INVALID_ARGUMENT;
   if (p == 1) return HCCX_OK;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -637,6 +643,7 @@ extern "C" hccx_status_t hccx_lossless_ring_hops(const float* const* d_in, int p
 
 extern "C" hccx_status_t hccx_lossless_ring_wire(const float* const* d_in, int p, uint64_t n, int collective,
                                                  uint64_t* wire, void* stream) {
+  HCCX_NVTX("hccx_lossless_ring_wire");
   if (!wire || !d_in || p < 1 || p > 16 || collective < 0 || collective > 2) return HCCX_ERR_INVALID_ARGUMENT;
   *wire = 0;
   if (p == 1 || n == 0) return HCCX_OK;
@@ -652,6 +659,7 @@ extern "C" hccx_status_t hccx_lossless_ring_wire(const float* const* d_in, int p
 
 extern "C" hccx_status_t hccx_lossless_ring_wire_host(const float* const* h_in, int p, uint64_t n, int collective,
                                                       uint64_t* wire, int device) {
+  HCCX_NVTX("hccx_lossless_ring_wire_host");
   if (!wire || !h_in || p < 1 || p > 16) return HCCX_ERR_INVALID_ARGUMENT;
   DeviceGuard g(device);
   float* d[16] = {};
@@ -668,6 +676,7 @@ extern "C" hccx_status_t hccx_lossless_ring_wire_host(const float* const* h_in, 
 
 extern "C" hccx_status_t hccx_lossless_ring_hops_host(const float* const* h_in, int p, uint64_t n, int collective,
                                                       uint64_t* hop, int device) {
+  HCCX_NVTX("hccx_lossless_ring_hops_host");
   if (!hop || !h_in || p < 1 || p > 16) return HCCX_ERR_INVALID_ARGUMENT;
   DeviceGuard g(device);
   float* d[16] = {};

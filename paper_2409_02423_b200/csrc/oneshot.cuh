@@ -52,6 +52,10 @@ __device__ __forceinline__ void oneshot_body(const FusedParams& P, const uint32_
   const bool vec = P.vec_ok != 0;
   uint8_t* sm = stage[warp];
   uint32_t bad = 0;
+  if constexpr (Codec::kNeedsInit) {
+    Codec::kernel_init();
+    __syncthreads();
+  }
   auto raw_slot = [&](int rank, int t) {
     return reinterpret_cast<float*>(P.win[rank] + P.os_off + static_cast<uint64_t>(t) * P.os_raw_bytes);
   };

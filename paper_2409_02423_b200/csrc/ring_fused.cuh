@@ -30,6 +30,24 @@
 namespace hccx {
 
 constexpr int kMaxRanks = 16;
+
+// Role timing accumulators, per-warp progress words (timeout wait chains)
+// and their clock reads cost ~10% of the kernel's issue slots: compiled in
+// only for analysis builds (make EXTRA=-DHCCX_FUSED_PROFILE=1 OUT=...;
+// tools/nvl_trace.py reads them).  CTA-0 event timelines stay runtime-gated.
+#ifndef HCCX_FUSED_PROFILE
+#define HCCX_FUSED_PROFILE 0
+#endif
+__device__ __forceinline__ uint64_t prof_clock() {
+  if constexpr (HCCX_FUSED_PROFILE) return clock64();
+  return 0;
+}
+#define HCCX_PROG(stmt)                    \
+  do {                                     \
+    if constexpr (HCCX_FUSED_PROFILE) {    \
+      stmt;                                \
+    }                                      \
+  } while (0)
 // Compute warps per CTA of the fused kernel.  One CTA per SM with 24
 // compute warps working through the same segments: with three 8-warp CTAs
 // per SM the warp scheduler's age priority starved the SM's third CTA, which
@@ -79,7 +97,8 @@ struct FusedParams {
   uint32_t credit_all;  // bit c: slot class c (0 rs, 1 ag, 2 pp) changed geometry since its last use
   uint32_t ack_span;    // consumption-ack indices covering every CTA of any grid this communicator launches
   uint32_t max_grid;    // CTAs per rank cap shared by all ranks (0: the device's co-resident capacity)
-  int debug;  // development knobs (HCCX_DEBUG): 16 = warp-store pushes, 32 = synchronous tile release, 64 = log launches
+  int debug;  // development knobs (HCCX_DEBUG): 16 = warp-store pushes, 32 = synchronous tile release, 64 = log launches,
+            // 512 = lazy step publication, 256 = one system fence per signalled event
 };
 
 // Parameters of the virtual-rank kernels: nv ranks, G CTAs each.
@@ -148,6 +167,7 @@ __device__ __forceinline__ void spin_ge(const FusedParams& P, const uint32_t* fl
   const uint64_t t0 = globaltimer_ns();
   uint32_t spins = 0;
   while (static_cast<int32_t>(ld_acquire_sys(flag) - epoch) < 0) {
+    __nanosleep(32);
     if ((++spins & 1023u) == 0) {
       if (P.err && (ldg_u32_coherent(P.err) & kErrTimeout)) return;
       if (globaltimer_ns() - t0 > P.timeout_ns) {
@@ -173,13 +193,15 @@ __device__ __forceinline__ void mbar_wait_to(const FusedParams& P, uint64_t* bar
   if (ok) return;
   const uint64_t t0 = globaltimer_ns();
   for (uint32_t spins = 0;; ++spins) {
+    // suspended in hardware until the phase completes (or ~20 us pass): a
+    // waiting role warp takes no issue slots from the compute warps
     asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n selp.u32 %0, 1, 0, p;\n}"
         : "=r"(ok)
-        : "r"(smem_u32(bar)), "r"(parity)
+        : "r"(smem_u32(bar)), "r"(parity), "r"(20000u)
         : "memory");
     if (ok) return;
-    if ((spins & 255u) == 255u) {
+    if ((spins & 15u) == 15u) {
       if (P.err && (ldg_u32_coherent(P.err) & kErrTimeout)) return;
       if (globaltimer_ns() - t0 > P.timeout_ns) {
         if (P.err) atomicOr(P.err, kErrTimeout);
@@ -571,6 +593,7 @@ __device__ __forceinline__ void ring_fused_body(const FusedParams& P, const uint
     S.sig_events = 0;
     fence_mbar_init();
   }
+  Codec::kernel_init();
   __syncthreads();
   if (P.trace && threadIdx.x == 0 && 16384 + cta < P.trace_cap) {
     uint32_t smid;
@@ -582,7 +605,7 @@ __device__ __forceinline__ void ring_fused_body(const FusedParams& P, const uint
   if (warp == kFCompute) {
     // ------------------------------------------------------------ producer
     if (lane == 0) {
-      uint64_t c_empty = 0, c_flag = 0, c_total = clock64();
+      uint64_t c_empty = 0, c_flag = 0, c_total = prof_clock();
       uint32_t pu = 0;  // per-barrier fill parity
       for (int ph = 0; ph < nph; ++ph) {
         const Phase f = phase_of(P, ph);
@@ -593,10 +616,10 @@ __device__ __forceinline__ void ring_fused_body(const FusedParams& P, const uint
         for (uint32_t k0 = 0, k1; k0 < myseg; k0 = k1) {
           k1 = step_end(k0);
           if (f.wait_cls >= 0) {
-            const uint64_t t0 = clock64();
+            const uint64_t t0 = prof_clock();
             spin_ge(P, flag_ptr(P, j, f.wait_cls, f.wait_slot, seg_of(k0)), f.wait_ep, 0x700u | (ph << 4) | f.wait_cls);
             asm volatile("fence.proxy.async.global;" ::: "memory");
-            c_flag += clock64() - t0;
+            c_flag += prof_clock() - t0;
             trace_ev(P, cta, 1, ph, k0);
           }
           for (uint32_t k = k0; k < k1; ++k) {
@@ -615,10 +638,10 @@ __device__ __forceinline__ void ring_fused_body(const FusedParams& P, const uint
                 }
               }
             }
-            S.prog[kFCompute] = (ph << 20) | (k << 4) | 3u;
-            const uint64_t t1 = clock64();
+            HCCX_PROG(S.prog[kFCompute] = (ph << 20) | (k << 4) | 3u);
+            const uint64_t t1 = prof_clock();
             mbar_wait_to(P, &S.empty[st], ((pu >> st) & 1u) ^ 1u, 0x200u | st, S.prog);
-            c_empty += clock64() - t1;
+            c_empty += prof_clock() - t1;
             pu ^= 1u << st;
             const bool full_seg = tma_ok && seg_full(sg);
             S.direct[st] = full_seg ? 0u : 1u;
@@ -638,7 +661,7 @@ __device__ __forceinline__ void ring_fused_body(const FusedParams& P, const uint
           }
         }
       }
-      trace_acc(P, cta, 0, clock64() - c_total);
+      trace_acc(P, cta, 0, prof_clock() - c_total);
       trace_acc(P, cta, 1, c_empty);
       trace_acc(P, cta, 2, c_flag);
     }
@@ -659,15 +682,52 @@ __device__ __forceinline__ void ring_fused_body(const FusedParams& P, const uint
     int tt = 0;
     uint32_t tbit = 0;
     uint32_t seq = 0, released = 0;  // segments seen / tiles handed back (ring order)
-    uint64_t c_tfull = 0, c_read = 0, c_pub = 0, c_credit = 0, c_issue = 0, c_total = clock64();
+    uint64_t c_tfull = 0, c_read = 0, c_pub = 0, c_credit = 0, c_issue = 0, c_total = prof_clock();
     uint32_t events = 0;  // signaller events issued (lane 0)
+    // Lazy publication (lane 0): a finished step's event is queued with the
+    // bulk-group count at its end and handed to the signaller once those
+    // groups have completed -- checked kLazy groups later (by then they are
+    // done, so the wait is free) or whenever the pusher would otherwise
+    // block (waiting for a tile or a credit): the TMA engine keeps pushing
+    // across step boundaries instead of draining at every step.  Events
+    // (step publications and phase-end acks) stay in the signaller's order.
+    constexpr int kLazy = 3;
+    constexpr int kPend = 8;
+    uint32_t pend_g[kPend];  // group count at the step's end; ~0u = ack event (no bulk dependency)
+    int pend_head = 0, pend_n = 0;
+    uint32_t groups = 0;     // bulk groups committed (one per pushed segment)
     auto release_upto = [&](uint32_t upto) {
       for (; released < upto; ++released) mbar_arrive(&S.tempty[released % kT]);
+    };
+    auto emit = [&](bool drain) {  // lane 0
+      bool waited_all = false;
+      while (pend_n) {
+        const uint32_t g = pend_g[pend_head];
+        if (g != ~0u) {
+          if (groups - g >= static_cast<uint32_t>(kLazy)) {
+            asm volatile("cp.async.bulk.wait_group %0;" ::"n"(kLazy) : "memory");
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+          } else if (drain) {
+            if (!waited_all) bulk_wait_all();
+            waited_all = true;
+          } else {
+            break;
+          }
+        }
+        st_release_cta_shared(&S.sig_events, ++events);
+        pend_head = (pend_head + 1) % kPend;
+        --pend_n;
+      }
+    };
+    auto enqueue = [&](uint32_t g) {  // lane 0
+      if (pend_n == kPend) emit(true);
+      pend_g[(pend_head + pend_n) % kPend] = g;
+      ++pend_n;
     };
     for (int ph = 0; ph < nph; ++ph) {
       const Phase f = phase_of(P, ph);
       const bool push = f.push_cls >= 0;
-      const uint64_t tc = clock64();
+      const uint64_t tc = prof_clock();
       if (push) {  // credit: previous use of the destination slot(s) consumed
         // Same slot geometry as the previous use (codec, chunk size, hence
         // grid and segment bytes): this CTA's segments were read by the
@@ -676,6 +736,8 @@ __device__ __forceinline__ void ring_fused_body(const FusedParams& P, const uint
         // were read by arbitrary receiver CTAs, so wait for all of them --
         // receiver CTA r of a grid G' acked indices r, r+G', ..., so indices
         // [0, ack_span) cover every CTA of any grid <= ack_span.
+        if (lane == 0) emit(true);  // never hold a publication across a wait on a peer
+        __syncwarp();
         const bool all = ((P.credit_all >> f.push_cls) & 1u) != 0;
         for (int q = 1; q < p; ++q) {
           const int d = (j + q) % p;
@@ -691,16 +753,18 @@ __device__ __forceinline__ void ring_fused_body(const FusedParams& P, const uint
         }
       }
       __syncwarp();
-      c_credit += clock64() - tc;
+      c_credit += prof_clock() - tc;
       for (uint32_t k0 = 0, k1; k0 < myseg; k0 = k1) {
         k1 = step_end(k0);
         for (uint32_t k = k0; k < k1; ++k) {
           const uint32_t sg = seg_of(k);
           if (lane == 0) {
-            S.prog[kFCompute + 1] = (ph << 20) | (k << 4) | 2u;
-            const uint64_t t0 = clock64();
+            HCCX_PROG(S.prog[kFCompute + 1] = (ph << 20) | (k << 4) | 2u);
+            const uint64_t t0 = prof_clock();
+            // about to wait for compute: publish what has completed first
+            if (pend_n && !mbar_test(&S.tfull[tt], tbit)) emit(true);
             mbar_wait_to(P, &S.tfull[tt], tbit, 0x300u | tt, S.prog);
-            c_tfull += clock64() - t0;
+            c_tfull += prof_clock() - t0;
           }
           __syncwarp();  // the tile is complete for every lane
           bool bulk_issued = false;
@@ -712,7 +776,7 @@ __device__ __forceinline__ void ring_fused_body(const FusedParams& P, const uint
             // bit 16 selects the warp's 16-byte stores instead.
             if ((nb & 15u) == 0 && !(P.debug & 16)) {
               if (lane == 0) {
-                const uint64_t ti = clock64();
+                const uint64_t ti = prof_clock();
                 // the tile was written through the generic proxy; the bulk
                 // copy reads it through the async proxy
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -723,7 +787,8 @@ __device__ __forceinline__ void ring_fused_body(const FusedParams& P, const uint
                   bulk_s2g(slot_ptr(P, d, f.push_cls, f.push_slot) + soff, S.tile[tt], nb);
                 }
                 bulk_commit();
-                c_issue += clock64() - ti;
+                ++groups;
+                c_issue += prof_clock() - ti;
                 trace_ev(P, cta, 3, ph, k);
               }
               bulk_issued = true;
@@ -743,7 +808,7 @@ __device__ __forceinline__ void ring_fused_body(const FusedParams& P, const uint
           ++seq;
           __syncwarp();  // every lane's reads of the tile are done
           if (lane == 0) {
-            const uint64_t t1 = clock64();
+            const uint64_t t1 = prof_clock();
             if (bulk_issued && !(P.debug & 32)) {
               bulk_wait_read<kRd>();  // hand tiles back once the TMA engine has read them
               release_upto(seq > static_cast<uint32_t>(kRd) ? seq - kRd : 0);
@@ -751,33 +816,40 @@ __device__ __forceinline__ void ring_fused_body(const FusedParams& P, const uint
               if (bulk_issued) bulk_wait_read<0>();
               release_upto(seq);
             }
-            c_read += clock64() - t1;
+            if (pend_n) emit(false);
+            c_read += prof_clock() - t1;
           }
           if (++tt == kT) {
             tt = 0;
             tbit ^= 1u;
           }
         }
-        if (push) {  // the step's stores are complete: hand its publication to the signaller
-          const uint64_t t2 = clock64();
+        if (push) {  // the step is issued: its publication follows once its groups complete
+          const uint64_t t2 = prof_clock();
           if (lane == 0) {
-            bulk_wait_all();
-            release_upto(seq);
-            st_release_cta_shared(&S.sig_events, ++events);
+            // (warp-copied segments commit no group: their lanes' stores
+            // are ordered before lane 0's event release by __syncwarp)
+            // Eager by default: measured at p = 4 (tools/nvl_ab.py), lazy
+            // publication cost 6% -- consumers saw the flags later than the
+            // drain at the step end costs the pusher.  HCCX_DEBUG bit 512:
+            // lazy (development).
+            enqueue(groups);
+            if (!(P.debug & 512)) emit(true);
           }
-          c_pub += clock64() - t2;
+          c_pub += prof_clock() - t2;
           __syncwarp();
         }
       }
       // every segment of the phase has been computed (tfull) -> its inbox
       // inputs are consumed: the signaller acknowledges them
-      if (f.ack_rank >= 0 && lane == 0) st_release_cta_shared(&S.sig_events, ++events);
+      if (f.ack_rank >= 0 && lane == 0) enqueue(~0u);
       __syncwarp();
     }
     if (lane == 0) {
+      emit(true);
       bulk_wait_all();
       release_upto(seq);
-      trace_acc(P, cta, 8, clock64() - c_total);
+      trace_acc(P, cta, 8, prof_clock() - c_total);
       trace_acc(P, cta, 9, c_tfull);
       trace_acc(P, cta, 10, c_read);
       trace_acc(P, cta, 11, c_pub);
@@ -790,20 +862,25 @@ __device__ __forceinline__ void ring_fused_body(const FusedParams& P, const uint
 
   if (warp == kFCompute + 2) {
     // ----------------------------------------------------------- signaller
-    // Publishes the pusher's completed steps (one release store per
-    // destination flag) and the phase-end consumption acks (one fence, then
-    // relaxed stores).  System-scope releases cost microseconds under load;
-    // here they overlap the pusher's next step instead of stalling the tile
-    // ring.  Walks the same (phase, step) sequence as the pusher and waits
-    // for each event on S.sig_events: the pusher's release.cta store after
-    // its bulk writes completed, this warp's acquire, then the sys-scope
-    // release -- causality order carries the writes to the remote reader.
-    uint32_t events = 0;
+    // Publishes the pusher's completed steps (one flag store per
+    // destination) and the phase-end consumption acks.  Walks the same
+    // (phase, step) event sequence as the pusher; event e is ready once
+    // S.sig_events >= e (the pusher's release.cta after the step's bulk
+    // writes completed).  A system-scope fence costs microseconds while
+    // NVLink writes are in flight, so events are published in batches: one
+    // acquire of the ready count, one fence.acq_rel.sys by every lane, then
+    // relaxed system-scope stores for every event up to that count --
+    // causality order carries the data writes to the remote acquirer.
+    uint32_t events = 0, ready = 0;
     uint64_t c_sig = 0, c_ack = 0;
-    auto wait_event = [&](uint32_t ev) {
+    auto need = [&](uint32_t ev) {  // make event ev publishable (fenced)
+      if (P.debug & 256) ready = 0;  // development: one fence per event (no batching)
+      if (ev <= ready) return;
       if (lane == 0) {
         const uint64_t t0 = globaltimer_ns();
-        for (uint32_t spins = 0; ld_acquire_cta_shared(&S.sig_events) < ev; ++spins) {
+        uint32_t r;
+        for (uint32_t spins = 0; (r = ld_acquire_cta_shared(&S.sig_events)) < ev; ++spins) {
+          __nanosleep(64);  // leave the issue slots to the compute warps
           if ((spins & 255u) == 255u) {
             if (P.err && (ldg_u32_coherent(P.err) & kErrTimeout)) break;
             if (globaltimer_ns() - t0 > P.timeout_ns) {
@@ -813,35 +890,37 @@ __device__ __forceinline__ void ring_fused_body(const FusedParams& P, const uint
             }
           }
         }
+        ready = r < ev ? ev : r;
       }
       __syncwarp();
+      ready = __shfl_sync(kFull, ready, 0);
+      fence_acq_rel_sys();
     };
     for (int ph = 0; ph < nph; ++ph) {
       const Phase f = phase_of(P, ph);
       if (f.push_cls >= 0) {
         for (uint32_t k0 = 0; k0 < myseg; k0 = step_end(k0)) {
-          wait_event(++events);
-          const uint64_t ts = clock64();
+          const uint64_t ts = prof_clock();
+          need(++events);
           if (lane < p - 1) {
             const int d = (j + 1 + lane) % p;
             const bool tgt =
                 f.push_mode == 1 || (f.push_mode == 0 && lane == 0) || (f.push_mode == 2 && d == P.dst);
-            if (tgt) signal(flag_ptr(P, d, f.push_cls, f.push_slot, seg_of(k0)), push_epoch(P, f.push_cls, d));
+            if (tgt) st_relaxed_sys(flag_ptr(P, d, f.push_cls, f.push_slot, seg_of(k0)), push_epoch(P, f.push_cls, d));
           }
           __syncwarp();
-          c_sig += clock64() - ts;
+          c_sig += prof_clock() - ts;
           if (lane == 0) trace_ev(P, cta, 5, ph, k0);
         }
       }
-      if (f.ack_rank >= 0) {  // one fence, then relaxed stores of the ack words
-        wait_event(++events);
-        const uint64_t ta = clock64();
-        fence_acq_rel_sys();
+      if (f.ack_rank >= 0) {
+        const uint64_t ta = prof_clock();
+        need(++events);
         for (uint32_t kk = cta + lane * G; kk < kAckIdx; kk += G * 32) {
           st_relaxed_sys(flag_ptr(P, f.ack_rank, f.ack_cls, f.ack_slot, 0) + kk, f.ack_ep);
           if (f.ack2_rank >= 0) st_relaxed_sys(flag_ptr(P, f.ack2_rank, f.ack2_cls, f.ack2_slot, 0) + kk, f.ack_ep);
         }
-        c_ack += clock64() - ta;
+        c_ack += prof_clock() - ta;
         __syncwarp();
       }
     }
@@ -858,21 +937,21 @@ __device__ __forceinline__ void ring_fused_body(const FusedParams& P, const uint
   int tt = 0;
   uint32_t tbit = 0;
   uint8_t* gen = S.gen + warp * kStageBytes;
-  uint64_t c_full = 0, c_tile = 0, c_comp = 0, c_total = clock64();
+  uint64_t c_full = 0, c_tile = 0, c_comp = 0, c_total = prof_clock();
   for (int ph = 0; ph < nph; ++ph) {
     const Phase f = phase_of(P, ph);
     const StageGeom sg_ = stage_geom<Codec>(f.kind);
     int st = 0;
     for (uint32_t k = 0; k < myseg; ++k) {
       const uint32_t sg = seg_of(k);
-      if (lane == 0) S.prog[warp] = (ph << 20) | (k << 4) | 1u;
-      const uint64_t t0 = clock64();
+      if (lane == 0) HCCX_PROG(S.prog[warp] = (ph << 20) | (k << 4) | 1u);
+      const uint64_t t0 = prof_clock();
       mbar_wait_to(P, &S.full[st], (cu >> st) & 1u, 0x400u | st, S.prog);
       cu ^= 1u << st;
-      if (lane == 0) S.prog[warp] = (ph << 20) | (k << 4) | 2u;
-      const uint64_t t1 = clock64();
+      if (lane == 0) HCCX_PROG(S.prog[warp] = (ph << 20) | (k << 4) | 2u);
+      const uint64_t t1 = prof_clock();
       mbar_wait_to(P, &S.tempty[tt], tbit ^ 1u, 0x500u | tt, S.prog);
-      const uint64_t t2 = clock64();
+      const uint64_t t2 = prof_clock();
       c_full += t1 - t0;
       c_tile += t2 - t1;
       const bool direct = S.direct[st] != 0;
@@ -882,9 +961,9 @@ __device__ __forceinline__ void ring_fused_body(const FusedParams& P, const uint
       const uint8_t* sb = base + sg_.a + warp * 1024u;
       if (g < ngroups) compute_group<Codec>(P, f, g, direct, sa, sb, S.tile[tt] + warp * GB, gen, lane, bad);
       __syncwarp();
-      c_comp += clock64() - t2;
+      c_comp += prof_clock() - t2;
       if (warp == 0 && lane == 0) trace_ev(P, cta, 2, ph, k);
-      if (lane == 0) S.prog[warp] = (ph << 20) | (k << 4) | 3u;
+      if (lane == 0) HCCX_PROG(S.prog[warp] = (ph << 20) | (k << 4) | 3u);
       if (lane == 0) {
         mbar_arrive(&S.empty[st]);
         mbar_arrive(&S.tfull[tt]);
@@ -897,7 +976,7 @@ __device__ __forceinline__ void ring_fused_body(const FusedParams& P, const uint
     }
   }
   if (lane == 0 && warp == 0) {
-    trace_acc(P, cta, 16, clock64() - c_total);
+    trace_acc(P, cta, 16, prof_clock() - c_total);
     trace_acc(P, cta, 17, c_full);
     trace_acc(P, cta, 18, c_tile);
     trace_acc(P, cta, 19, c_comp);

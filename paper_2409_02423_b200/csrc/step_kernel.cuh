@@ -241,6 +241,10 @@ __global__ void __launch_bounds__(kStepThreads) step_kernel(const __grid_constan
   const uint64_t wid = static_cast<uint64_t>(blockIdx.x) * kStepWarps + warp;
   uint32_t bad = 0;
   uint64_t g_generic = wid;
+  if constexpr (Codec::kNeedsInit) {
+    Codec::kernel_init();
+    __syncthreads();
+  }
   pdl_wait_and_release();
   if constexpr (Codec::kFastPath) {
     if (P.vec_ok && P.fast_ok) {
@@ -356,6 +360,7 @@ __global__ void __launch_bounds__(kTmaThreads) step_tma_kernel(const __grid_cons
     }
     fence_mbar_init();
   }
+  Codec::kernel_init();
   __syncthreads();
   // programmatic dependent launch: the barrier setup above overlapped the
   // previous kernel's tail; global memory is touched only after it finished

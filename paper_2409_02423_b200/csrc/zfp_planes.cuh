@@ -228,6 +228,58 @@ HCCX_HD void decode_planes(Bits& b, uint32_t budget, uint32_t (&u)[4]) {
 }
 
 
+// Plane codes by table lookup.  enc[n*16 + x] (n < 4 significant
+// coefficients, plane bits x) = code | len << 8 | n_out << 12; dec[n*128 + w]
+// (the next 7 stream bits w; a codeword is at most 7 bits, so with >= 7
+// bits of budget left the truncation rule never applies) = x | used << 4 |
+// n_out << 8.  Built from plane_code / plane_decode above (one entry per
+// thread at kernel start on the device), so the tables carry exactly their
+// bits; a lookup replaces the per-plane loop over group tests and runs.
+// On the device they live in shared memory: 64 enc entries are 32 words,
+// one per bank (conflict-free for any index pattern).
+struct Lut {
+  uint16_t enc[64];
+  uint16_t dec[512];
+};
+constexpr uint32_t kLutEntries = 64 + 512;
+
+HCCX_HD void lut_build_entry(uint32_t i, Lut& t) {
+  if (i < 64) {
+    uint32_t code, nn;
+    const uint32_t len = plane_code(i >> 4, i & 15u, &code, &nn);
+    t.enc[i] = static_cast<uint16_t>(code | (len << 8) | (nn << 12));
+  } else if (i < kLutEntries) {
+    const uint32_t j = i - 64;
+    uint32_t nn = j >> 7, used;
+    const uint32_t x = plane_decode(j & 127u, 7, &nn, &used);
+    t.dec[j] = static_cast<uint16_t>(x | (used << 4) | (nn << 8));
+  }
+}
+
+#if defined(__CUDACC__)
+__device__ __forceinline__ Lut& lut_dev() {
+  __shared__ Lut t;  // one per CTA; filled by lut_init() before first use
+  return t;
+}
+// every thread of the CTA, then a CTA barrier before any lookup
+__device__ __forceinline__ void lut_init() {
+  for (uint32_t i = threadIdx.x; i < kLutEntries; i += blockDim.x) lut_build_entry(i, lut_dev());
+}
+#endif
+
+HCCX_HD Lut& lut() {
+#if defined(__CUDA_ARCH__)
+  return lut_dev();
+#else
+  static Lut t = [] {
+    Lut x{};
+    for (uint32_t i = 0; i < kLutEntries; ++i) lut_build_entry(i, x);
+    return x;
+  }();
+  return t;
+#endif
+}
+
 // Steppers for coding two blocks in one loop (a lane owns two blocks: the
 // joint loop runs max(planes) iterations instead of their sum and gives the
 // two independent dependency chains to the scheduler side by side).  Same
@@ -250,7 +302,12 @@ struct PlaneEnc {
   HCCX_HD void step(Bits& b) {
     const uint32_t x = plane_bits(u, k);
     uint32_t code = x, nn = 4, len = 4;  // all significant: verbatim plane
-    if (n < 4) len = plane_code(n, x, &code, &nn);
+    if (n < 4) {
+      const uint32_t e = lut().enc[n * 16 + x];
+      code = e & 0x7fu;
+      len = (e >> 8) & 7u;
+      nn = e >> 12;
+    }
     const uint32_t m = len < budget ? len : budget;
     b.put(code & ((1u << m) - 1u), static_cast<int>(m));
     budget -= m;
@@ -284,11 +341,17 @@ struct PlaneDec {
   HCCX_HD bool active() const { return budget != 0 && k >= 0; }
   HCCX_HD void step(Bits& b) {
     uint32_t used, x;
+    const uint64_t w = b.peek();
     if (n == 4) {
       used = budget < 4 ? budget : 4u;
-      x = static_cast<uint32_t>(b.peek()) & ((1u << used) - 1u);
-    } else {
-      x = plane_decode(b.peek(), budget, &n, &used);
+      x = static_cast<uint32_t>(w) & ((1u << used) - 1u);
+    } else if (budget >= 7) {
+      const uint32_t e = lut().dec[n * 128 + (static_cast<uint32_t>(w) & 127u)];
+      x = e & 15u;
+      used = (e >> 4) & 15u;
+      n = e >> 8;
+    } else {  // the block's last, truncated plane
+      x = plane_decode(w, budget, &n, &used);
     }
     b.pos += static_cast<int>(used);
     budget -= used;
