@@ -310,6 +310,18 @@ HCCX_API hccx_status_t hccx_mcomm_broadcast_host(hccx_mcomm_t m, int root, const
 HCCX_API hccx_status_t hccx_mcomm_p2p_host(hccx_mcomm_t m, int src, int dst, const float* h_in, float* h_out,
                                            uint64_t n, hccx_codec_t codec, double* device_seconds);
 
+/* Bytes this rank (member) pushed in its last collective: *payload = codec
+ * payload bytes (the reference's wire accounting, collectives.cpp:113-126,
+ * before the per-rank average), *frame = payload plus message framing.
+ * Fixed-size codecs: the size law; LosslessPredictor: the framed,
+ * data-dependent messages actually sent (HCC1 container header per message,
+ * proj/src/codec.cpp:89-99). */
+HCCX_API hccx_status_t hccx_comm_wire_bytes(hccx_comm_t c, uint64_t* payload, uint64_t* frame);
+HCCX_API hccx_status_t hccx_mcomm_wire_bytes(hccx_mcomm_t m, int member, uint64_t* payload, uint64_t* frame);
+/* Payload bytes of the framed (LosslessPredictor) messages this rank
+ * received in its last collective (0 for fixed-size codecs). */
+HCCX_API hccx_status_t hccx_comm_recv_bytes(hccx_comm_t c, uint64_t* payload);
+
 /* CUDA devices visible to this process (0 when none). */
 HCCX_API int hccx_device_count(void);
 

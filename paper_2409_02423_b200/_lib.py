@@ -107,6 +107,9 @@ hccx_mcomm_broadcast_host = _sig("hccx_mcomm_broadcast_host", _st, _p, C.c_int, 
 hccx_mcomm_p2p_host = _sig("hccx_mcomm_p2p_host", _st, _p, C.c_int, C.c_int, _p, _p, _u64, Codec, _dp)
 hccx_launch_count = _sig("hccx_launch_count", _u64)
 hccx_device_count = _sig("hccx_device_count", C.c_int)
+hccx_comm_wire_bytes = _sig("hccx_comm_wire_bytes", _st, _p, C.POINTER(_u64), C.POINTER(_u64))
+hccx_mcomm_wire_bytes = _sig("hccx_mcomm_wire_bytes", _st, _p, C.c_int, C.POINTER(_u64), C.POINTER(_u64))
+hccx_comm_recv_bytes = _sig("hccx_comm_recv_bytes", _st, _p, C.POINTER(_u64))
 
 #: every symbol include/hccx.h declares (checked by tests/test_abi.py)
 EXPORTED = [n for n in dir() if n.startswith("hccx_")]

@@ -18,6 +18,7 @@
 #include "fused_launch.cuh"
 #include "hccx.h"
 #include "hccx_internal.h"
+#include "comm_internal.h"
 
 namespace hccx {
 
@@ -83,32 +84,12 @@ uint64_t timeout_ns() {
 
 }  // namespace
 
-struct hccx_comm {
-  int rank = 0, p = 0, device = 0;
-  uint64_t chunk_cap = 0;   // values per slot (multiple of one segment)
-  uint64_t slot_bytes = 0;  // payload capacity per slot (worst codec: 257 B / 64 values)
-  uint32_t max_seg = 0;
-  uint64_t rs_off = 0, ag_off = 0, pp_off = 0, flag_off = 0, win_bytes = 0;
-  uint64_t os_cap = 0;  // one-shot allreduce: values per chunk
-  uint64_t os_off = 0, os_ag_off = 0, os_flag_off = 0, os_raw_bytes = 0, os_ag_bytes = 0;
-  uint8_t* win = nullptr;
-  uint8_t* peers[kMaxRanks] = {};
-  bool connected = false;
-  uint32_t* d_err = nullptr;
-  uint32_t epoch = 0;                  // collectives
-  uint32_t last_rs = 0, last_ag = 0;   // epoch of the last collective that used rs / ag slots
-  uint32_t send_ep[kMaxRanks] = {};    // p2p / broadcast messages sent to rank d
-  uint32_t recv_ep[kMaxRanks] = {};    // ... received from rank s
-  uint64_t* d_trace = nullptr;         // optional CTA-0 timeline (hccx_comm_trace_enable)
-  uint64_t trace_cap = 0;
-  // Slot geometry (codec, values per slot) of the last use of each slot
-  // class; a change makes the next sender wait for every receiver CTA's ack
-  // (FusedParams::credit_all).
-  uint64_t geo_rs = 0, geo_ag = 0;
-  uint64_t geo_pp[kMaxRanks] = {};     // per destination (send side)
-  uint32_t max_grid = 0;               // CTAs per rank shared by all ranks (single-process comms)
-  bool ipc = true;                     // peers[] opened with cudaIpcOpenMemHandle (closed on destroy)
-};
+namespace hccx {
+uint64_t comm_timeout_ns() { return timeout_ns(); }
+hccx_status_t ll_collective(hccx_comm* const* comms, int nr, int op, const float* const* in, float* const* out,
+                            uint64_t n, int mode, int root, int dst, const cudaStream_t* streams);
+}  // namespace hccx
+
 
 extern "C" hccx_status_t hccx_comm_create(int rank, int nranks, int device, uint64_t max_n, hccx_comm_t* out) {
   HCCX_NVTX("hccx_comm_create");
@@ -120,7 +101,9 @@ extern "C" hccx_status_t hccx_comm_create(int rank, int nranks, int device, uint
   c->p = nranks;
   c->device = device;
   c->chunk_cap = align_up((max_n + nranks - 1) / nranks, kSegVals);
-  c->slot_bytes = align_up((c->chunk_cap / 64) * 257, 256);
+  // worst fixed-size codec (257 B / 64 values) or a framed LosslessPredictor
+  // message (4 B per value + flag bytes + kFrameBytes), whichever is larger
+  c->slot_bytes = align_up((c->chunk_cap / 64) * 257 + kFrameBytes, 256);
   c->max_seg = static_cast<uint32_t>(c->chunk_cap / kSegVals);
   const uint64_t nslots = 3ull * nranks - 1;  // data-flag slots; the acks use kAckIdx per slot
   c->rs_off = 0;
@@ -227,18 +210,11 @@ FusedParams base_params(hccx_comm* c, int op, uint64_t n_chunk, const float* in,
   P.max_grid = c->max_grid;
   const char* dbg = std::getenv("HCCX_DEBUG");  // per call: A/B of development knobs in one process
   P.debug = dbg ? std::atoi(dbg) : 0;
-  static const uint32_t step_segs = [] {
-    const char* e = std::getenv("HCCX_STEP_SEGS");
-    const int v = e ? std::atoi(e) : 0;
-    return v > 0 ? static_cast<uint32_t>(v) : 0u;  // 0: chosen per launch (fused_launch.cuh)
-  }();
-  P.step_segs = step_segs;
-  static const uint32_t first_segs = [] {
-    const char* e = std::getenv("HCCX_FIRST_SEGS");
-    const int v = e ? std::atoi(e) : 0;
-    return v > 0 ? static_cast<uint32_t>(v) : 0u;  // 0: same as the step size
-  }();
-  P.first_segs = first_segs;
+  // development knobs, read per call (A/B in one process; every rank must agree)
+  const char* ss = std::getenv("HCCX_STEP_SEGS");  // 0/unset: chosen per launch (fused_launch.cuh)
+  P.step_segs = ss && std::atoi(ss) > 0 ? static_cast<uint32_t>(std::atoi(ss)) : 0u;
+  const char* fs = std::getenv("HCCX_FIRST_SEGS");  // 0/unset: same as the step size
+  P.first_segs = fs && std::atoi(fs) > 0 ? static_cast<uint32_t>(std::atoi(fs)) : 0u;
   // Allgather (and the allreduce's gather half) as a forwarding ring once a
   // chunk is large: the owner pushing to all p-1 peers at once makes that
   // phase NVLink-bound (measured p=4: ring wins at 64 MiB chunks, direct at
@@ -314,6 +290,7 @@ hccx_status_t plan_allreduce(hccx_comm* c, const float* d_in, float* d_out, uint
                              int mode, RankWork& w) {
   hccx_status_t st = check_comm(c, codec);
   if (st != HCCX_OK) return st;
+  c->last_payload = c->last_frame = 0;
   if (n % static_cast<uint64_t>(c->p) != 0) return HCCX_ERR_BAD_CHUNKING;
   if (n / c->p > c->chunk_cap) return HCCX_ERR_INVALID_ARGUMENT;
   if (c->p == 1 || n == 0) {
@@ -332,6 +309,11 @@ hccx_status_t plan_allreduce(hccx_comm* c, const float* d_in, float* d_out, uint
     note_geo(c->geo_rs, key, 0, P);
     note_geo(c->geo_ag, key, 1, P);
   }
+  {
+    const uint64_t W = payload_bytes(sel_of(codec), n / c->p);
+    c->last_payload = c->last_frame = P.op == kFOneShotAllReduce ? (c->p - 1) * (4 * (n / c->p) + W)
+                                                                  : 2ull * (c->p - 1) * W;
+  }
   StepParams tmp{};
   set_divisor(tmp, mode, c->p);
   P.div_mode = tmp.div_mode;
@@ -345,6 +327,7 @@ hccx_status_t plan_reduce_scatter(hccx_comm* c, const float* d_in, float* d_shar
                                   RankWork& w) {
   hccx_status_t st = check_comm(c, codec);
   if (st != HCCX_OK) return st;
+  c->last_payload = c->last_frame = 0;
   if (n % static_cast<uint64_t>(c->p) != 0) return HCCX_ERR_BAD_CHUNKING;
   if (n / c->p > c->chunk_cap) return HCCX_ERR_INVALID_ARGUMENT;
   if (c->p == 1 || n == 0) {
@@ -357,6 +340,7 @@ hccx_status_t plan_reduce_scatter(hccx_comm* c, const float* d_in, float* d_shar
   P.prev_rs = c->last_rs;
   c->last_rs = P.epoch;
   note_geo(c->geo_rs, geo_key(codec, n / c->p), 0, P);
+  c->last_payload = c->last_frame = (c->p - 1) * payload_bytes(sel_of(codec), n / c->p);
   w.launches.push_back(P);
   return HCCX_OK;
 }
@@ -365,6 +349,7 @@ hccx_status_t plan_allgather(hccx_comm* c, const float* d_shard, float* d_out, u
                              RankWork& w) {
   hccx_status_t st = check_comm(c, codec);
   if (st != HCCX_OK) return st;
+  c->last_payload = c->last_frame = 0;
   if (shard_n > c->chunk_cap) return HCCX_ERR_INVALID_ARGUMENT;
   if (c->p == 1 || shard_n == 0) {
     plan_copy(w, d_shard, d_out, 4 * shard_n);
@@ -375,6 +360,7 @@ hccx_status_t plan_allgather(hccx_comm* c, const float* d_shard, float* d_out, u
   P.prev_ag = c->last_ag;
   c->last_ag = P.epoch;
   note_geo(c->geo_ag, geo_key(codec, shard_n), 1, P);
+  c->last_payload = c->last_frame = (c->p - 1) * payload_bytes(sel_of(codec), shard_n);
   w.launches.push_back(P);
   return HCCX_OK;
 }
@@ -385,6 +371,7 @@ hccx_status_t plan_allgather(hccx_comm* c, const float* d_shard, float* d_out, u
 void plan_pp_passes(hccx_comm* c, int op, int root, int dst, const float* d_in, float* d_out, uint64_t n,
                     hccx_codec_t codec, RankWork& w) {
   const uint64_t pass = c->chunk_cap;  // values (multiple of one segment)
+  c->last_payload = c->last_frame = 0;
   for (uint64_t off = 0; off < n; off += pass) {
     const uint64_t m = (n - off) < pass ? (n - off) : pass;
     FusedParams P = base_params(c, op, m, d_in ? d_in + off : nullptr, d_out ? d_out + off : nullptr);
@@ -396,6 +383,8 @@ void plan_pp_passes(hccx_comm* c, int op, int root, int dst, const float* d_in, 
         if (d != root && (op == kFBroadcast || d == dst)) {
           P.pp_epoch[d] = ++c->send_ep[d];
           note_geo(c->geo_pp[d], key, 2, P);
+          c->last_payload += payload_bytes(sel_of(codec), m);
+          c->last_frame = c->last_payload;
         }
     } else {
       P.pp_epoch[root] = ++c->recv_ep[root];
@@ -408,6 +397,7 @@ hccx_status_t plan_broadcast(hccx_comm* c, int root, const float* d_in, float* d
                              hccx_codec_t codec, RankWork& w) {
   hccx_status_t st = check_comm(c, codec);
   if (st != HCCX_OK) return st;
+  c->last_payload = c->last_frame = 0;
   if (root < 0 || root >= c->p) return HCCX_ERR_INVALID_ARGUMENT;
   if (n == 0) return HCCX_OK;
   if (c->p == 1) {
@@ -422,6 +412,7 @@ hccx_status_t plan_p2p(hccx_comm* c, int src, int dst, const float* d_in, float*
                        hccx_codec_t codec, RankWork& w) {
   hccx_status_t st = check_comm(c, codec);
   if (st != HCCX_OK) return st;
+  c->last_payload = c->last_frame = 0;
   if (src < 0 || src >= c->p || dst < 0 || dst >= c->p || src == dst) return HCCX_ERR_INVALID_ARGUMENT;
   if (c->rank != src && c->rank != dst) return HCCX_OK;
   if (n == 0) return HCCX_OK;
@@ -446,6 +437,12 @@ hccx_status_t exec_rank(hccx_comm* c, hccx_codec_t codec, const RankWork& w, cud
 extern "C" hccx_status_t hccx_allreduce(hccx_comm_t c, const float* d_in, float* d_out, uint64_t n,
                                         hccx_codec_t codec, int mode, void* stream) {
   HCCX_NVTX("hccx_allreduce");
+  if (c && codec.kind == HCCX_CODEC_LOSSLESS) {
+    if (!c->connected) return HCCX_ERR_INVALID_ARGUMENT;
+    if (n % static_cast<uint64_t>(c->p) != 0) return HCCX_ERR_BAD_CHUNKING;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    return ll_collective(&c, 1, 0, &d_in, &d_out, n, mode, 0, 0, &s);
+  }
   RankWork w;
   hccx_status_t st = plan_allreduce(c, d_in, d_out, n, codec, mode, w);
   return st != HCCX_OK ? st : exec_rank(c, codec, w, static_cast<cudaStream_t>(stream));
@@ -454,6 +451,12 @@ extern "C" hccx_status_t hccx_allreduce(hccx_comm_t c, const float* d_in, float*
 extern "C" hccx_status_t hccx_reduce_scatter(hccx_comm_t c, const float* d_in, float* d_shard, uint64_t n,
                                              hccx_codec_t codec, void* stream) {
   HCCX_NVTX("hccx_reduce_scatter");
+  if (c && codec.kind == HCCX_CODEC_LOSSLESS) {
+    if (!c->connected) return HCCX_ERR_INVALID_ARGUMENT;
+    if (n % static_cast<uint64_t>(c->p) != 0) return HCCX_ERR_BAD_CHUNKING;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    return ll_collective(&c, 1, 1, &d_in, &d_shard, n, 0, 0, 0, &s);
+  }
   RankWork w;
   hccx_status_t st = plan_reduce_scatter(c, d_in, d_shard, n, codec, w);
   return st != HCCX_OK ? st : exec_rank(c, codec, w, static_cast<cudaStream_t>(stream));
@@ -462,6 +465,11 @@ extern "C" hccx_status_t hccx_reduce_scatter(hccx_comm_t c, const float* d_in, f
 extern "C" hccx_status_t hccx_allgather(hccx_comm_t c, const float* d_shard, float* d_out, uint64_t shard_n,
                                         hccx_codec_t codec, void* stream) {
   HCCX_NVTX("hccx_allgather");
+  if (c && codec.kind == HCCX_CODEC_LOSSLESS) {
+    if (!c->connected) return HCCX_ERR_INVALID_ARGUMENT;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    return ll_collective(&c, 1, 2, &d_shard, &d_out, shard_n, 0, 0, 0, &s);
+  }
   RankWork w;
   hccx_status_t st = plan_allgather(c, d_shard, d_out, shard_n, codec, w);
   return st != HCCX_OK ? st : exec_rank(c, codec, w, static_cast<cudaStream_t>(stream));
@@ -470,6 +478,12 @@ extern "C" hccx_status_t hccx_allgather(hccx_comm_t c, const float* d_shard, flo
 extern "C" hccx_status_t hccx_broadcast(hccx_comm_t c, int root, const float* d_in, float* d_out, uint64_t n,
                                         hccx_codec_t codec, void* stream) {
   HCCX_NVTX("hccx_broadcast");
+  if (c && codec.kind == HCCX_CODEC_LOSSLESS) {
+    if (!c->connected || root < 0 || root >= c->p) return HCCX_ERR_INVALID_ARGUMENT;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const float* src = c->rank == root ? d_in : nullptr;
+    return ll_collective(&c, 1, 3, &src, &d_out, n, 0, root, -1, &s);
+  }
   RankWork w;
   hccx_status_t st = plan_broadcast(c, root, d_in, d_out, n, codec, w);
   return st != HCCX_OK ? st : exec_rank(c, codec, w, static_cast<cudaStream_t>(stream));
@@ -478,6 +492,15 @@ extern "C" hccx_status_t hccx_broadcast(hccx_comm_t c, int root, const float* d_
 extern "C" hccx_status_t hccx_p2p(hccx_comm_t c, int src, int dst, const float* d_in, float* d_out, uint64_t n,
                                   hccx_codec_t codec, void* stream) {
   HCCX_NVTX("hccx_p2p");
+  if (c && codec.kind == HCCX_CODEC_LOSSLESS) {
+    if (!c->connected || src < 0 || src >= c->p || dst < 0 || dst >= c->p || src == dst)
+      return HCCX_ERR_INVALID_ARGUMENT;
+    if (c->rank != src && c->rank != dst) return HCCX_OK;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const float* in = c->rank == src ? d_in : nullptr;
+    float* out = c->rank == dst ? d_out : nullptr;
+    return ll_collective(&c, 1, 4, &in, &out, n, 0, src, dst, &s);
+  }
   RankWork w;
   hccx_status_t st = plan_p2p(c, src, dst, d_in, d_out, n, codec, w);
   return st != HCCX_OK ? st : exec_rank(c, codec, w, static_cast<cudaStream_t>(stream));
@@ -568,6 +591,13 @@ hccx_status_t mcomm_exec(hccx_mcomm* m, hccx_codec_t codec, std::vector<RankWork
   return cuda_status(cudaGetLastError());
 }
 
+std::vector<cudaStream_t> mstreams(hccx_mcomm* m, void* const* streams) {
+  std::vector<cudaStream_t> out(m->p, nullptr);
+  if (streams)
+    for (int j = 0; j < m->p; ++j) out[j] = static_cast<cudaStream_t>(streams[j]);
+  return out;
+}
+
 hccx_status_t mcomm_check(hccx_mcomm* m, hccx_codec_t codec) {
   if (!m) return HCCX_ERR_INVALID_ARGUMENT;
   return check_codec(codec);
@@ -653,6 +683,8 @@ extern "C" hccx_status_t hccx_mcomm_allreduce(hccx_mcomm_t m, const float* const
   hccx_status_t st = mcomm_check(m, codec);
   if (st != HCCX_OK) return st;
   if (n % static_cast<uint64_t>(m->p) != 0) return HCCX_ERR_BAD_CHUNKING;
+  if (codec.kind == HCCX_CODEC_LOSSLESS)
+    return ll_collective(m->members.data(), m->p, 0, d_in, d_out, n, mode, 0, 0, mstreams(m, streams).data());
   std::vector<RankWork> w(m->p);
   for (int j = 0; j < m->p; ++j)
     if ((st = plan_allreduce(m->members[j], d_in[j], d_out[j], n, codec, mode, w[j])) != HCCX_OK) return st;
@@ -665,6 +697,8 @@ extern "C" hccx_status_t hccx_mcomm_reduce_scatter(hccx_mcomm_t m, const float* 
   hccx_status_t st = mcomm_check(m, codec);
   if (st != HCCX_OK) return st;
   if (n % static_cast<uint64_t>(m->p) != 0) return HCCX_ERR_BAD_CHUNKING;
+  if (codec.kind == HCCX_CODEC_LOSSLESS)
+    return ll_collective(m->members.data(), m->p, 1, d_in, d_shard, n, 0, 0, 0, mstreams(m, streams).data());
   std::vector<RankWork> w(m->p);
   for (int j = 0; j < m->p; ++j)
     if ((st = plan_reduce_scatter(m->members[j], d_in[j], d_shard[j], n, codec, w[j])) != HCCX_OK) return st;
@@ -676,6 +710,8 @@ extern "C" hccx_status_t hccx_mcomm_allgather(hccx_mcomm_t m, const float* const
   HCCX_NVTX("hccx_mcomm_allgather");
   hccx_status_t st = mcomm_check(m, codec);
   if (st != HCCX_OK) return st;
+  if (codec.kind == HCCX_CODEC_LOSSLESS)
+    return ll_collective(m->members.data(), m->p, 2, d_shard, d_out, shard_n, 0, 0, 0, mstreams(m, streams).data());
   std::vector<RankWork> w(m->p);
   for (int j = 0; j < m->p; ++j)
     if ((st = plan_allgather(m->members[j], d_shard[j], d_out[j], shard_n, codec, w[j])) != HCCX_OK) return st;
@@ -688,6 +724,11 @@ extern "C" hccx_status_t hccx_mcomm_broadcast(hccx_mcomm_t m, int root, const fl
   hccx_status_t st = mcomm_check(m, codec);
   if (st != HCCX_OK) return st;
   if (root < 0 || root >= m->p) return HCCX_ERR_INVALID_ARGUMENT;
+  if (codec.kind == HCCX_CODEC_LOSSLESS) {
+    std::vector<const float*> ins(m->p, nullptr);
+    ins[root] = d_in;
+    return ll_collective(m->members.data(), m->p, 3, ins.data(), d_out, n, 0, root, -1, mstreams(m, streams).data());
+  }
   std::vector<RankWork> w(m->p);
   for (int j = 0; j < m->p; ++j)
     if ((st = plan_broadcast(m->members[j], root, j == root ? d_in : nullptr, d_out[j], n, codec, w[j])) != HCCX_OK)
@@ -701,6 +742,14 @@ extern "C" hccx_status_t hccx_mcomm_p2p(hccx_mcomm_t m, int src, int dst, const 
   hccx_status_t st = mcomm_check(m, codec);
   if (st != HCCX_OK) return st;
   if (src < 0 || src >= m->p || dst < 0 || dst >= m->p || src == dst) return HCCX_ERR_INVALID_ARGUMENT;
+  if (codec.kind == HCCX_CODEC_LOSSLESS) {
+    hccx_comm* two[2] = {m->members[src], m->members[dst]};
+    const float* ins[2] = {d_in, nullptr};
+    float* outs[2] = {nullptr, d_out};
+    const auto all = mstreams(m, streams);
+    const cudaStream_t ss[2] = {all[src], all[dst]};
+    return ll_collective(two, 2, 4, ins, outs, n, 0, src, dst, ss);
+  }
   std::vector<RankWork> w(m->p);
   for (int j : {src, dst})
     if ((st = plan_p2p(m->members[j], src, dst, d_in, d_out, n, codec, w[j])) != HCCX_OK) return st;
@@ -859,4 +908,22 @@ extern "C" hccx_status_t hccx_mcomm_p2p_host(hccx_mcomm_t m, int src, int dst, c
   return mcomm_host_run(m, hin, n, src, outs.data(), n, mask, secs, [&] {
     return hccx_mcomm_p2p(m, src, dst, m->hin[src], m->hout[dst], n, codec, nullptr);
   });
+}
+
+extern "C" hccx_status_t hccx_comm_wire_bytes(hccx_comm_t c, uint64_t* payload, uint64_t* frame) {
+  if (!c || !payload || !frame) return HCCX_ERR_INVALID_ARGUMENT;
+  *payload = c->last_payload;
+  *frame = c->last_frame;
+  return HCCX_OK;
+}
+
+extern "C" hccx_status_t hccx_mcomm_wire_bytes(hccx_mcomm_t m, int member, uint64_t* payload, uint64_t* frame) {
+  if (!m || member < 0 || member >= m->p) return HCCX_ERR_INVALID_ARGUMENT;
+  return hccx_comm_wire_bytes(m->members[member], payload, frame);
+}
+
+extern "C" hccx_status_t hccx_comm_recv_bytes(hccx_comm_t c, uint64_t* payload) {
+  if (!c || !payload) return HCCX_ERR_INVALID_ARGUMENT;
+  *payload = c->last_recv;
+  return HCCX_OK;
 }

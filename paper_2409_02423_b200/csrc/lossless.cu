@@ -414,6 +414,12 @@ struct Scratch {
     cap = c;
     return HCCX_OK;
   }
+  void drop_jump() {
+    cudaFree(jump[0]);
+    cudaFree(jump[1]);
+    jump[0] = jump[1] = nullptr;
+    jump_cap = 0;
+  }
   bool ensure_jump(uint64_t entries) {
     if (entries <= jump_cap) return true;
     cudaFree(jump[0]);
@@ -448,9 +454,31 @@ hccx_status_t size_pass(const float* d_in, uint64_t n, Scratch& s, cudaStream_t 
   return HCCX_OK;
 }
 
-thread_local Scratch t_scratch;
+// One scratch per device and host thread (a single-process communicator
+// drives several GPUs from one thread).
+Scratch& scratch() {
+  thread_local Scratch s[16];
+  int d = 0;
+  cudaGetDevice(&d);
+  return s[d & 15];
+}
+
+// Pointer-doubling tables cost 8 bytes per payload bit: above this budget
+// the serial walk is used instead, and tables above kJumpKeepBytes are
+// freed after the call rather than pinned for the thread's lifetime.
+constexpr uint64_t kJumpMaxBytes = 1ull << 30;
+constexpr uint64_t kJumpKeepBytes = 256ull << 20;
 
 }  // namespace
+
+// part = part + x on `stream` (the lossless ring's fold, used by the engine)
+cudaError_t ll_fold(float* part, const float* x, uint64_t n, cudaStream_t stream) {
+  if (n == 0) return cudaSuccess;
+  ll_fold_kernel<<<grid_for(n, 256 * 4), 256, 0, stream>>>(part, x, n);
+  count_launch();
+  return cudaGetLastError();
+}
+
 }  // namespace hccx
 
 using namespace hccx;
@@ -462,7 +490,7 @@ extern "C" hccx_status_t hccx_lossless_size(const float* d_in, uint64_t n, uint6
     *bytes = 0;
     return HCCX_OK;
   }
-  return size_pass(d_in, n, t_scratch, static_cast<cudaStream_t>(stream), bytes);
+  return size_pass(d_in, n, scratch(), static_cast<cudaStream_t>(stream), bytes);
 }
 
 extern "C" hccx_status_t hccx_lossless_compress(const float* d_in, uint64_t n, uint8_t* d_out, uint64_t capacity,
@@ -474,6 +502,7 @@ extern "C" hccx_status_t hccx_lossless_compress(const float* d_in, uint64_t n, u
     return HCCX_OK;
   }
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  Scratch& t_scratch = scratch();
   hccx_status_t r = size_pass(d_in, n, t_scratch, st, bytes);
   if (r != HCCX_OK) return r;
   if (*bytes > capacity) return HCCX_ERR_INVALID_ARGUMENT;
@@ -499,6 +528,7 @@ extern "C" hccx_status_t hccx_lossless_decompress(const uint8_t* d_in, uint64_t 
   const uint64_t nch = (n + kChunk - 1) / kChunk;
   if (in_bytes < (nch + 7) / 8) return HCCX_ERR_CORRUPT_PAYLOAD;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  Scratch& t_scratch = scratch();
   hccx_status_t r = t_scratch.ensure(nch);
   if (r != HCCX_OK) return r;
   cudaMemsetAsync(t_scratch.err, 0, 4, st);
@@ -506,7 +536,8 @@ extern "C" hccx_status_t hccx_lossless_decompress(const uint8_t* d_in, uint64_t 
   // full chunks and the tables fit (8 bytes per stream bit), else the
   // serial walk (cheap for all-raw payloads: O(1) per raw chunk).
   const uint64_t S = 8 * in_bytes;
-  bool jump = nch >= 64 && S + 2 < (1ull << 32) && std::getenv("HCCX_LL_SERIAL") == nullptr;
+  bool jump = nch >= 64 && S + 2 < (1ull << 32) && 8 * (S + 2) <= kJumpMaxBytes &&
+              std::getenv("HCCX_LL_SERIAL") == nullptr;
   if (jump) {  // worth it only with many coded chunks: count them from the flag bytes
     std::vector<uint8_t> flags((nch + 7) / 8);
     if (cudaMemcpyAsync(flags.data(), d_in, flags.size(), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
@@ -541,6 +572,7 @@ extern "C" hccx_status_t hccx_lossless_decompress(const uint8_t* d_in, uint64_t 
       cudaStreamSynchronize(st) != cudaSuccess)
     return HCCX_ERR_CUDA;
   (void)end;  // trailing bytes are ignored, as in codec_serial.cpp:85-107
+  if (8 * t_scratch.jump_cap > kJumpKeepBytes) t_scratch.drop_jump();  // do not pin large tables
   if (e) return HCCX_ERR_CORRUPT_PAYLOAD;
   return HCCX_OK;
 }

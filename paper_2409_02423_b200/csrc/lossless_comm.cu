@@ -1,0 +1,488 @@
+// lossless_comm.cu -- LosslessPredictor collectives over the NVLink
+// communicator: the compressed bytes themselves go on the wire.
+//
+// The reference's MZHybrid scheme sends TP / PP / ZeRO traffic through the
+// LosslessPredictor (proj/src/parallel3d.cpp:63-69): every ring hop carries
+// compress(partial) (proj/src/collectives.cpp:44), whose size is data
+// dependent.  Here each hop is a framed message in the receiver's slot:
+//
+//   [u64 container bytes][HCC1 container header (18 B, codec.cpp:89-99)]
+//   [pad to kFrameBytes][LosslessPredictor payload]
+//
+// The sender compresses straight into the peer's slot (the emit kernel's
+// stores cross NVLink), writes the frame, and publishes the slot's data
+// flag with a system-scope fence + store; the receiver waits for the flag on
+// the device, reads and validates the frame like hcc::from_bytes
+// (codec.cpp:101-121: magic, kind, lengths -> CorruptPayloadError),
+// decompresses, folds (acc = dec + acc, collectives.cpp:50) and acks the
+// slot.  The codec's sizes are host-visible (its size pass synchronises), so
+// the sequence is host-driven per rank; a single-process communicator runs
+// every member's stage before any member's next stage, so no host wait ever
+// depends on work not yet enqueued.  Values are exact (the codec is
+// lossless), so results equal the identity ring's bit for bit; the traced
+// wire bytes are the payload bytes actually pushed.
+#include <cstdlib>
+#include <cstring>
+#include <vector>
+
+#include "comm_internal.h"
+#include "device_common.cuh"
+#include "hccx.h"
+#include "hccx_internal.h"
+
+namespace hccx {
+
+cudaError_t ll_fold(float* part, const float* x, uint64_t n, cudaStream_t stream);
+
+namespace {
+
+__global__ void ll_signal_kernel(uint32_t* flags, uint32_t count, uint32_t value) {
+  fence_acq_rel_sys();  // every prior write of this stream (payload, frame) before the flags
+  for (uint32_t i = threadIdx.x; i < count; i += blockDim.x) st_relaxed_sys(flags + i, value);
+}
+
+__global__ void ll_wait_kernel(const uint32_t* flags, uint32_t count, uint32_t epoch, uint32_t* err,
+                               uint64_t timeout_ns) {
+  for (uint32_t i = threadIdx.x; i < count; i += blockDim.x) {
+    const uint64_t t0 = globaltimer_ns();
+    uint32_t spins = 0;
+    while (static_cast<int32_t>(ld_acquire_sys(flags + i) - epoch) < 0) {
+      __nanosleep(64);
+      if ((++spins & 255u) == 0) {
+        if (ldg_u32_coherent(err) & kErrTimeout) return;
+        if (globaltimer_ns() - t0 > timeout_ns) {
+          atomicOr(err, kErrTimeout);
+          return;
+        }
+      }
+    }
+  }
+}
+
+__global__ void ll_frame_kernel(uint8_t* dst, uint64_t container_bytes, uint64_t n, uint32_t chunks) {
+  if (threadIdx.x != 0) return;
+  uint8_t h[26];
+  for (int i = 0; i < 8; ++i) h[i] = static_cast<uint8_t>(container_bytes >> (8 * i));
+  h[8] = 'H', h[9] = 'C', h[10] = 'C', h[11] = '1';
+  h[12] = HCCX_CODEC_LOSSLESS;  // kind
+  h[13] = 0;                    // rate_bits
+  for (int i = 0; i < 8; ++i) h[14 + i] = static_cast<uint8_t>(n >> (8 * i));
+  for (int i = 0; i < 4; ++i) h[22 + i] = static_cast<uint8_t>(chunks >> (8 * i));
+  for (int i = 0; i < 26; ++i) dst[i] = h[i];
+}
+
+__global__ void ll_scale_kernel(float* x, uint64_t n, int div_mode, float recip, float divisor) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    x[i] = div_mode == 1 ? __fmul_rn(x[i], recip) : __fdiv_rn(x[i], divisor);
+}
+
+constexpr uint32_t kPredictorChunk = 4096;
+
+uint32_t* host_flag(const hccx_comm* c, int rank, int cls, int slot, uint32_t idx) {
+  uint32_t* f = reinterpret_cast<uint32_t*>(c->peers[rank] + c->flag_off);
+  const int p = c->p;
+  if (cls < 3) {
+    const int base[3] = {0, p - 1, 2 * p - 1};
+    return f + static_cast<uint64_t>(base[cls] + slot) * c->max_seg + idx;
+  }
+  const int base[4] = {0, p - 1, 2 * p - 1, 3 * p - 1};
+  return f + static_cast<uint64_t>(3 * p - 1) * c->max_seg + static_cast<uint64_t>(base[cls - 3] + slot) * kAckIdx +
+         idx;
+}
+
+uint8_t* host_slot(const hccx_comm* c, int rank, int cls, int slot) {
+  const uint64_t off = cls == 0 ? c->rs_off : (cls == 1 ? c->ag_off : c->pp_off);
+  return c->peers[rank] + off + static_cast<uint64_t>(slot) * c->slot_bytes;
+}
+
+hccx_status_t ensure(float*& buf, uint64_t& cap, uint64_t n) {
+  if (n <= cap && buf) return HCCX_OK;
+  cudaFree(buf);
+  buf = nullptr;
+  cap = 0;
+  if (cudaMalloc(&buf, 4 * (n ? n : 1)) != cudaSuccess) return HCCX_ERR_CUDA;
+  cap = n;
+  return HCCX_OK;
+}
+
+hccx_status_t launched() { return cuda_status(cudaGetLastError()); }
+
+// One framed message: compress `m` values into slot (cls, slot) of `dst`.
+hccx_status_t send_frame(hccx_comm* c, const float* src, uint64_t m, int dst, int cls, int slot, cudaStream_t s,
+                         uint64_t* payload) {
+  uint8_t* base = host_slot(c, dst, cls, slot);
+  uint64_t bytes = 0;
+  hccx_status_t st = hccx_lossless_compress(src, m, base + kFrameBytes, c->slot_bytes - kFrameBytes, &bytes, s);
+  if (st != HCCX_OK) return st;
+  ll_frame_kernel<<<1, 32, 0, s>>>(base, 18 + bytes, m, static_cast<uint32_t>((m + kPredictorChunk - 1) / kPredictorChunk));
+  count_launch();
+  *payload = bytes;
+  c->last_payload += bytes;
+  c->last_frame += kFrameBytes + bytes;
+  return launched();
+}
+
+// Copy an already framed message (local slot) into `dst`'s slot.
+hccx_status_t copy_frame(hccx_comm* c, const uint8_t* frame, uint64_t payload, int dst, int cls, int slot,
+                         cudaStream_t s) {
+  if (cudaMemcpyAsync(host_slot(c, dst, cls, slot), frame, kFrameBytes + payload, cudaMemcpyDeviceToDevice, s) !=
+      cudaSuccess)
+    return HCCX_ERR_CUDA;
+  c->last_payload += payload;
+  c->last_frame += kFrameBytes + payload;
+  return HCCX_OK;
+}
+
+hccx_status_t signal(hccx_comm* c, int rank, int cls, int slot, uint32_t count, uint32_t value, cudaStream_t s) {
+  ll_signal_kernel<<<1, 32, 0, s>>>(host_flag(c, rank, cls, slot, 0), count, value);
+  count_launch();
+  return launched();
+}
+
+hccx_status_t wait(hccx_comm* c, int cls, int slot, uint32_t count, uint32_t epoch, cudaStream_t s) {
+  ll_wait_kernel<<<1, 32, 0, s>>>(host_flag(c, c->rank, cls, slot, 0), count, epoch, c->d_err, comm_timeout_ns());
+  count_launch();
+  return launched();
+}
+
+// Receive side: wait for the slot's data flag, read the frame back and
+// validate it as hcc::from_bytes would, decompress into `out`.
+hccx_status_t recv_frame(hccx_comm* c, int cls, int slot, uint32_t epoch, uint64_t m, float* out, cudaStream_t s) {
+  hccx_status_t st = wait(c, cls, slot, 1, epoch, s);
+  if (st != HCCX_OK) return st;
+  const uint8_t* base = host_slot(c, c->rank, cls, slot);
+  uint8_t h[26];
+  uint32_t err = 0;
+  if (cudaMemcpyAsync(h, base, 26, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+      cudaMemcpyAsync(&err, c->d_err, 4, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+      cudaStreamSynchronize(s) != cudaSuccess)
+    return HCCX_ERR_CUDA;
+  if (err & kErrTimeout) return HCCX_ERR_TIMEOUT;
+  uint64_t container = 0, n = 0;
+  uint32_t chunks = 0;
+  for (int i = 0; i < 8; ++i) container |= static_cast<uint64_t>(h[i]) << (8 * i);
+  for (int i = 0; i < 8; ++i) n |= static_cast<uint64_t>(h[14 + i]) << (8 * i);
+  for (int i = 0; i < 4; ++i) chunks |= static_cast<uint32_t>(h[22 + i]) << (8 * i);
+  if (container < 18 || kFrameBytes + container - 18 > c->slot_bytes || std::memcmp(h + 8, "HCC1", 4) != 0 ||
+      h[12] != HCCX_CODEC_LOSSLESS || n != m || chunks != (m + kPredictorChunk - 1) / kPredictorChunk)
+    return HCCX_ERR_CORRUPT_PAYLOAD;
+  c->last_recv += container - 18;
+  return hccx_lossless_decompress(base + kFrameBytes, container - 18, m, out, s);
+}
+
+// Consumption ack of slot (cls, slot) in `rank`'s window: every index, so
+// fused-kernel senders (which wait on their own CTA's index, or on all of
+// them after a geometry change) see it too.
+hccx_status_t ack(hccx_comm* c, int rank, int cls, int slot, uint32_t epoch, cudaStream_t s) {
+  return signal(c, rank, cls, slot, kAckIdx, epoch, s);
+}
+
+hccx_status_t credit(hccx_comm* c, int cls, int slot, uint32_t need, cudaStream_t s) {
+  return wait(c, cls, slot, kAckIdx, need, s);
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// Per-rank stage machine of one lossless collective.  Ops: 0 allreduce,
+// 1 reduce-scatter, 2 allgather, 3 broadcast, 4 p2p.
+
+struct LLRank {
+  hccx_comm* c = nullptr;
+  cudaStream_t s = nullptr;
+  int op = 0, mode = 0, root = 0, dst = 0;
+  uint64_t n = 0, chunk = 0;
+  const float* in = nullptr;
+  float* out = nullptr;
+  float* work = nullptr;
+  uint32_t epoch = 0, prev_rs = 0, prev_ag = 0;
+  uint32_t pp_ep = 0;       // broadcast / p2p: this message's epoch (sender: per destination)
+  uint32_t pp_send[kMaxRanks] = {};
+  uint64_t shard_payload = 0;
+};
+
+hccx_status_t ll_setup(LLRank& r, hccx_comm* c, int op, const float* in, float* out, uint64_t n, int mode, int root,
+                       int dst, cudaStream_t s) {
+  r = LLRank{};
+  r.c = c;
+  r.s = s;
+  r.op = op;
+  r.in = in;
+  r.out = out;
+  r.n = n;
+  r.mode = mode;
+  r.root = root;
+  r.dst = dst;
+  c->last_payload = c->last_frame = c->last_recv = 0;
+  const int p = c->p;
+  // the lossless geometry differs from every fused-kernel geometry: the next
+  // fused use of these slots waits for every receiver CTA's ack
+  const uint64_t lossless_key = 1ull << 62;
+  if (op <= 2) {
+    r.chunk = op == 2 ? n : n / p;
+    r.epoch = ++c->epoch;
+    if (op != 2) {
+      r.prev_rs = c->last_rs;
+      c->last_rs = r.epoch;
+      c->geo_rs = lossless_key;
+    }
+    if (op != 1) {
+      r.prev_ag = c->last_ag;
+      c->last_ag = r.epoch;
+      c->geo_ag = lossless_key;
+    }
+  } else {
+    r.chunk = n;
+    if (c->rank == root) {
+      for (int d = 0; d < p; ++d)
+        if (d != root && (op == 3 || d == dst)) {
+          r.pp_send[d] = ++c->send_ep[d];
+          c->geo_pp[d] = lossless_key;
+        }
+    } else if (op == 3 || c->rank == dst) {
+      r.pp_ep = ++c->recv_ep[root];
+    }
+  }
+  DeviceGuard guard(c->device);
+  if (op == 0 || op == 1) {  // the ring folds into a work copy of the input
+    float* w = out;
+    if (op == 1) {
+      if (ensure(c->ll_work, c->ll_work_cap, n) != HCCX_OK) return HCCX_ERR_CUDA;
+      w = c->ll_work;
+    }
+    if (w != in && cudaMemcpyAsync(w, in, 4 * n, cudaMemcpyDeviceToDevice, s) != cudaSuccess) return HCCX_ERR_CUDA;
+    r.work = w;
+  }
+  if (ensure(c->ll_tmp, c->ll_tmp_cap, r.chunk) != HCCX_OK) return HCCX_ERR_CUDA;
+  return HCCX_OK;
+}
+
+// Reduce-scatter round t (collectives.cpp:34-52): send this rank's partial
+// of chunk (j-1-t) to the right neighbour's rs[t].
+hccx_status_t ll_rs_send(LLRank& r, int t) {
+  hccx_comm* c = r.c;
+  DeviceGuard guard(c->device);
+  const int p = c->p, j = c->rank, right = (j + 1) % p;
+  hccx_status_t st = credit(c, 3, t, r.prev_rs, r.s);
+  if (st != HCCX_OK) return st;
+  const int ch = ((j - 1 - t) % p + p) % p;
+  uint64_t bytes = 0;
+  st = send_frame(c, r.work + static_cast<uint64_t>(ch) * r.chunk, r.chunk, right, 0, t, r.s, &bytes);
+  if (st != HCCX_OK) return st;
+  return signal(c, right, 0, t, 1, r.epoch, r.s);
+}
+
+// ... and its receive: acc(chunk j-2-t) = dec(msg) + acc, ack the left neighbour.
+hccx_status_t ll_rs_recv(LLRank& r, int t) {
+  hccx_comm* c = r.c;
+  DeviceGuard guard(c->device);
+  const int p = c->p, j = c->rank, left = (j + p - 1) % p;
+  hccx_status_t st = recv_frame(c, 0, t, r.epoch, r.chunk, c->ll_tmp, r.s);
+  if (st != HCCX_OK) return st;
+  const int ch = ((j - 2 - t) % p + p) % p;
+  if (ll_fold(r.work + static_cast<uint64_t>(ch) * r.chunk, c->ll_tmp, r.chunk, r.s) != cudaSuccess)
+    return HCCX_ERR_CUDA;
+  return ack(c, left, 3, t, r.epoch, r.s);
+}
+
+// Allgather (collectives.cpp:77-107): the owner compresses its shard once
+// into its own (otherwise unused) ag[j] slot and copies the frame into every
+// peer's ag[j] slot -- each shard's payload crosses the wire p-1 times.
+hccx_status_t ll_ag_send(LLRank& r) {
+  hccx_comm* c = r.c;
+  DeviceGuard guard(c->device);
+  const int p = c->p, j = c->rank;
+  const float* shard = r.op == 2 ? r.in : r.work + static_cast<uint64_t>(j) * r.chunk;
+  for (int q = 1; q < p; ++q) {
+    const hccx_status_t st = credit(c, 4, (j + q) % p, r.prev_ag, r.s);
+    if (st != HCCX_OK) return st;
+  }
+  uint64_t bytes = 0;
+  hccx_status_t st = send_frame(c, shard, r.chunk, j, 1, j, r.s, &bytes);
+  if (st != HCCX_OK) return st;
+  c->last_payload -= bytes;  // the local staging copy is not on the wire
+  c->last_frame -= kFrameBytes + bytes;
+  const uint8_t* frame = host_slot(c, j, 1, j);
+  for (int q = 1; q < p; ++q) {
+    const int d = (j + q) % p;
+    if ((st = copy_frame(c, frame, bytes, d, 1, j, r.s)) != HCCX_OK) return st;
+    if ((st = signal(c, d, 1, j, 1, r.epoch, r.s)) != HCCX_OK) return st;
+  }
+  // the owner's own chunk: dec(comp(shard)) == shard
+  float* own = r.out + static_cast<uint64_t>(j) * r.chunk;
+  if (own != shard && cudaMemcpyAsync(own, shard, 4 * r.chunk, cudaMemcpyDeviceToDevice, r.s) != cudaSuccess)
+    return HCCX_ERR_CUDA;
+  return HCCX_OK;
+}
+
+hccx_status_t ll_ag_recv(LLRank& r) {
+  hccx_comm* c = r.c;
+  DeviceGuard guard(c->device);
+  const int p = c->p, j = c->rank, left = (j + p - 1) % p;
+  for (int q = 1; q < p; ++q) {
+    const int i = (j - q + p) % p;
+    hccx_status_t st = recv_frame(c, 1, i, r.epoch, r.chunk, r.out + static_cast<uint64_t>(i) * r.chunk, r.s);
+    if (st != HCCX_OK) return st;
+    // ack to the owner (direct-gather credit) and to the left neighbour
+    // (ring-gather credit), like the fused kernel's gather receives
+    if ((st = ack(c, i, 4, j, r.epoch, r.s)) != HCCX_OK) return st;
+    if ((st = ack(c, left, 6, i, r.epoch, r.s)) != HCCX_OK) return st;
+  }
+  return HCCX_OK;
+}
+
+// Broadcast / p2p (one pass of at most chunk_cap values).
+hccx_status_t ll_pp_send(LLRank& r) {
+  hccx_comm* c = r.c;
+  DeviceGuard guard(c->device);
+  const int p = c->p, j = c->rank;
+  if (j != r.root) return HCCX_OK;
+  for (int d = 0; d < p; ++d) {
+    if (!r.pp_send[d]) continue;
+    const hccx_status_t st = credit(c, 5, d, r.pp_send[d] - 1, r.s);
+    if (st != HCCX_OK) return st;
+  }
+  uint64_t bytes = 0;
+  hccx_status_t st = send_frame(c, r.in, r.n, j, 2, j, r.s, &bytes);  // staging: own pp[root] slot
+  if (st != HCCX_OK) return st;
+  c->last_payload -= bytes;
+  c->last_frame -= kFrameBytes + bytes;
+  const uint8_t* frame = host_slot(c, j, 2, j);
+  for (int d = 0; d < p; ++d) {
+    if (!r.pp_send[d]) continue;
+    if ((st = copy_frame(c, frame, bytes, d, 2, j, r.s)) != HCCX_OK) return st;
+    if ((st = signal(c, d, 2, j, 1, r.pp_send[d], r.s)) != HCCX_OK) return st;
+  }
+  if (r.op == 3 && r.out && r.out != r.in &&
+      cudaMemcpyAsync(r.out, r.in, 4 * r.n, cudaMemcpyDeviceToDevice, r.s) != cudaSuccess)
+    return HCCX_ERR_CUDA;
+  return HCCX_OK;
+}
+
+hccx_status_t ll_pp_recv(LLRank& r) {
+  hccx_comm* c = r.c;
+  if (!r.pp_ep) return HCCX_OK;
+  DeviceGuard guard(c->device);
+  hccx_status_t st = recv_frame(c, 2, r.root, r.pp_ep, r.n, r.out, r.s);
+  if (st != HCCX_OK) return st;
+  return ack(c, r.root, 5, c->rank, r.pp_ep, r.s);
+}
+
+hccx_status_t ll_finish(LLRank& r, const StepParams& div) {
+  hccx_comm* c = r.c;
+  DeviceGuard guard(c->device);
+  if (r.op == 1) {  // reduce-scatter: this rank's reduced chunk
+    if (cudaMemcpyAsync(r.out, r.work + static_cast<uint64_t>(c->rank) * r.chunk, 4 * r.chunk,
+                        cudaMemcpyDeviceToDevice, r.s) != cudaSuccess)
+      return HCCX_ERR_CUDA;
+  }
+  if (r.op == 0 && div.div_mode != 0) {  // Average: IEEE v / float(p) after the gather (collectives.cpp:234-239)
+    ll_scale_kernel<<<148 * 4, 256, 0, r.s>>>(r.out, r.n, div.div_mode, div.recip, div.divisor);
+    count_launch();
+    return launched();
+  }
+  return HCCX_OK;
+}
+
+// Runs the stages of every rank in `ranks` in lockstep (one rank for a
+// multi-process communicator, all members for a single-process one).
+hccx_status_t ll_run(std::vector<LLRank>& ranks, const StepParams& div) {
+  if (ranks.empty()) return HCCX_OK;
+  const LLRank& r0 = ranks[0];
+  const int p = r0.c->p;
+  hccx_status_t st = HCCX_OK;
+  auto all = [&](auto&& fn) {
+    for (LLRank& r : ranks)
+      if ((st = fn(r)) != HCCX_OK) return false;
+    return true;
+  };
+  if (r0.op == 0 || r0.op == 1) {
+    for (int t = 0; t < p - 1; ++t) {
+      if (!all([&](LLRank& r) { return ll_rs_send(r, t); })) return st;
+      if (!all([&](LLRank& r) { return ll_rs_recv(r, t); })) return st;
+    }
+  }
+  if (r0.op == 0 || r0.op == 2) {
+    if (!all([&](LLRank& r) { return ll_ag_send(r); })) return st;
+    if (!all([&](LLRank& r) { return ll_ag_recv(r); })) return st;
+  }
+  if (r0.op == 3 || r0.op == 4) {
+    if (!all([&](LLRank& r) { return ll_pp_send(r); })) return st;
+    if (!all([&](LLRank& r) { return ll_pp_recv(r); })) return st;
+  }
+  all([&](LLRank& r) { return ll_finish(r, div); });
+  return st;
+}
+
+}  // namespace hccx
+
+namespace hccx {
+
+// Entry for the communicators (comm.cu): one LosslessPredictor collective
+// for the ranks `comms[0..nr)` (one rank: multi-process; all members: a
+// single-process communicator).  op 0 allreduce, 1 reduce-scatter,
+// 2 allgather (n = shard values), 3 broadcast, 4 p2p.  Synchronous: the
+// codec's sizes are read on the host.
+hccx_status_t ll_collective(hccx_comm* const* comms, int nr, int op, const float* const* in, float* const* out,
+                            uint64_t n, int mode, int root, int dst, const cudaStream_t* streams) {
+  if (nr < 1) return HCCX_OK;
+  const int p = comms[0]->p;
+  for (int k = 0; k < nr; ++k) {
+    hccx_comm* c = comms[k];
+    DeviceGuard guard(c->device);
+    c->last_payload = c->last_frame = c->last_recv = 0;
+  }
+  StepParams div{};
+  set_divisor(div, mode, p);
+  if (op <= 2) {
+    if (p == 1 || n == 0) {
+      for (int k = 0; k < nr; ++k) {
+        DeviceGuard guard(comms[k]->device);
+        if (n && out[k] != in[k] &&
+            cudaMemcpyAsync(out[k], in[k], 4 * n, cudaMemcpyDeviceToDevice, streams[k]) != cudaSuccess)
+          return HCCX_ERR_CUDA;
+      }
+      return HCCX_OK;
+    }
+    const uint64_t chunk = op == 2 ? n : n / p;
+    if (chunk > comms[0]->chunk_cap) return HCCX_ERR_INVALID_ARGUMENT;
+    std::vector<LLRank> ranks(nr);
+    for (int k = 0; k < nr; ++k) {
+      const hccx_status_t st = ll_setup(ranks[k], comms[k], op, in[k], out[k], n, mode, root, dst, streams[k]);
+      if (st != HCCX_OK) return st;
+    }
+    return ll_run(ranks, div);
+  }
+  // broadcast / p2p: passes of whole 4096-value predictor chunks (the codec
+  // restarts at every pass start, exactly like hcc::compress on a slice
+  // boundary that is a chunk multiple... so the concatenated passes are one
+  // message's values)
+  const uint64_t pass = comms[0]->chunk_cap / kPredictorChunk * kPredictorChunk;
+  uint64_t acc_payload[kMaxRanks] = {}, acc_frame[kMaxRanks] = {}, acc_recv[kMaxRanks] = {};
+  for (uint64_t off = 0; off < n; off += pass) {
+    const uint64_t m = n - off < pass ? n - off : pass;
+    std::vector<LLRank> ranks(nr);
+    for (int k = 0; k < nr; ++k) {
+      const float* src = in[k] ? in[k] + off : nullptr;
+      float* dstp = out[k] ? out[k] + off : nullptr;
+      const hccx_status_t st = ll_setup(ranks[k], comms[k], op, src, dstp, m, mode, root, dst, streams[k]);
+      if (st != HCCX_OK) return st;
+    }
+    const hccx_status_t st = ll_run(ranks, div);
+    if (st != HCCX_OK) return st;
+    for (int k = 0; k < nr; ++k) {
+      acc_payload[k] += comms[k]->last_payload;
+      acc_frame[k] += comms[k]->last_frame;
+      acc_recv[k] += comms[k]->last_recv;
+    }
+  }
+  for (int k = 0; k < nr; ++k) {
+    comms[k]->last_payload = acc_payload[k];
+    comms[k]->last_frame = acc_frame[k];
+    comms[k]->last_recv = acc_recv[k];
+  }
+  return HCCX_OK;
+}
+
+}  // namespace hccx

@@ -124,6 +124,20 @@ class NvlinkComm:
               "p2p")
         return out
 
+    def wire_bytes(self):
+        """(payload, frame) bytes this rank pushed in its last collective
+        (hccx_comm_wire_bytes): the size law for fixed-size codecs, the
+        framed messages actually sent under LosslessPredictor."""
+        a, b = C.c_uint64(), C.c_uint64()
+        check(self._lib.hccx_comm_wire_bytes(self.h, C.byref(a), C.byref(b)), "wire_bytes")
+        return int(a.value), int(b.value)
+
+    def recv_bytes(self) -> int:
+        """Framed payload bytes this rank received in its last collective."""
+        a = C.c_uint64()
+        check(self._lib.hccx_comm_recv_bytes(self.h, C.byref(a)), "recv_bytes")
+        return int(a.value)
+
     def close(self) -> None:
         import torch.distributed as dist
 

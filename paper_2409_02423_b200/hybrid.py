@@ -18,7 +18,11 @@ through ``scheme.at(path)`` exactly like the reference trainer's call sites
   tp_allgather   TpAllGather        (policy row; the reference never emits it)
 
 Every call records a TraceEvent (raw/wire bytes per rank as the reference
-accounts them, measured device seconds) in ``self.trace``.
+accounts them, measured device seconds) in ``self.trace``.  Under
+LosslessPredictor (MZHybrid's TP / PP / ZeRO paths) the compressed bytes
+themselves cross NVLink as framed messages (HCC1 container header per
+message, csrc/lossless_comm.cu) and the traced wire bytes are the payload
+bytes the engine actually pushed.
 """
 from __future__ import annotations
 
@@ -122,39 +126,18 @@ class HybridComm:
     def _lossless(spec) -> bool:
         return spec.kind == CodecKind.LosslessPredictor
 
-    def _lossless_wire(self, g, x, what: str) -> int:
-        """Per-rank wire bytes (wire_total / p) under LosslessPredictor, whose
-        hop messages have data-dependent sizes (collectives.cpp:34-61,
-        :94-106).  The codec is value-transparent, so each hop's message is a
-        plain partial fold: member `me` gathers chunk `me` of every member
-        (one all-to-all), sizes the p-1 folds S_t = S_(t-1) + x[me+1+t][me]
-        that carry it round the ring (plus the folded shard's p-1 allgather
-        hops for an all-reduce) with the device size pass, and the totals are
-        summed over the group.  Accounting only: runs after the timed call."""
+    def _lossless_wire(self, g) -> int:
+        """Per-rank wire bytes (wire_total / p, collectives.cpp:113-126) of a
+        LosslessPredictor collective: the engine sent every hop as a framed
+        compressed message (csrc/lossless_comm.cu) and counted the payload
+        bytes this rank pushed; the group total is one 8-byte sum."""
         import torch
         import torch.distributed as dist
 
-        from . import lossless
-
-        p = len(g.ranks)
-        me = g.ranks.index(self.rank)
-        torch.cuda.synchronize()  # no fused kernel in flight across an NCCL call
-        if what == "ag":
-            mine = (p - 1) * lossless.size(x)
-        else:
-            c = x.numel() // p
-            got = torch.empty(p, c, dtype=torch.float32, device=x.device)
-            dist.all_to_all_single(got, x.contiguous().view(p, c), group=g.pg)
-            part = got[(me + 1) % p].clone()
-            mine = 0
-            for t in range(p - 1):
-                mine += lossless.size(part)
-                part = part + got[(me + 2 + t) % p]
-            if what == "ar":
-                mine += (p - 1) * lossless.size(part)
-        w = torch.tensor([mine], dtype=torch.int64, device=x.device)
+        mine = g.comm.wire_bytes()[0]
+        w = torch.tensor([mine], dtype=torch.int64, device="cuda")
         dist.all_reduce(w, group=g.pg)
-        return int(w.item()) // p
+        return int(w.item()) // len(g.ranks)
 
     # -------------------------------------------------------------- paths
     def dp_allreduce(self, grad, mode: int = 1):
@@ -173,7 +156,7 @@ class HybridComm:
             return x
         out, ev = self._timed(lambda: g.comm.allreduce(x, spec, mode))
         c = x.numel() // p
-        wire = (lambda: self._lossless_wire(g, x, "ar")) if self._lossless(spec) else \
+        wire = (lambda: self._lossless_wire(g)) if self._lossless(spec) else \
             2 * (p - 1) * wire_size_bytes(spec, c)
         self._record(path, CollectiveKind.AllReduce, p, 2 * (p - 1) * 4 * c, wire, 2 * (p - 1), ev)
         return out
@@ -186,7 +169,7 @@ class HybridComm:
             return shard
         out, ev = self._timed(lambda: g.comm.allgather(shard, spec))
         c = shard.numel()
-        wire = (lambda: self._lossless_wire(g, shard, "ag")) if self._lossless(spec) else \
+        wire = (lambda: self._lossless_wire(g)) if self._lossless(spec) else \
             (p - 1) * wire_size_bytes(spec, c)
         self._record(CommPath.TpAllGather, CollectiveKind.AllGather, p, (p - 1) * 4 * c, wire, p - 1, ev)
         return out
@@ -200,20 +183,12 @@ class HybridComm:
         out, ev = self._timed(lambda: g.comm.p2p(x, src_stage, dst_stage, spec))
         me = g.ranks.index(self.rank)
         if me in (src_stage, dst_stage):
-            if self._lossless(spec):
-                wire = self._p2p_lossless_wire(g, x, out, src_stage)
+            if self._lossless(spec):  # the framed message's payload, as sent / as received
+                wire = g.comm.wire_bytes()[0] if me == src_stage else g.comm.recv_bytes()
             else:
                 wire = wire_size_bytes(spec, x.numel())
             self._record(CommPath.PpP2p, CollectiveKind.P2P, 2, 4 * x.numel(), wire, 1, ev)
         return out
-
-    def _p2p_lossless_wire(self, g, x, out, src_stage: int) -> int:
-        """The payload size of dec(comp(x)) == x (the codec is transparent):
-        the source sizes its input, the destination what it received."""
-        from . import lossless
-
-        me = g.ranks.index(self.rank)
-        return lossless.size(x if me == src_stage else out)
 
     def zero_reduce_scatter(self, grad):
         """ZeRO-1 gradient reduce-scatter over the DP group (Zero1ReduceScatter)."""
@@ -224,7 +199,7 @@ class HybridComm:
             return grad
         out, ev = self._timed(lambda: g.comm.reduce_scatter(grad, spec))
         c = grad.numel() // p
-        wire = (lambda: self._lossless_wire(g, grad, "rs")) if self._lossless(spec) else \
+        wire = (lambda: self._lossless_wire(g)) if self._lossless(spec) else \
             (p - 1) * wire_size_bytes(spec, c)
         self._record(CommPath.Zero1ReduceScatter, CollectiveKind.ReduceScatter, p, (p - 1) * 4 * c, wire, p - 1, ev)
         return out
@@ -238,7 +213,7 @@ class HybridComm:
             return shard
         out, ev = self._timed(lambda: g.comm.allgather(shard, spec))
         c = shard.numel()
-        wire = (lambda: self._lossless_wire(g, shard, "ag")) if self._lossless(spec) else \
+        wire = (lambda: self._lossless_wire(g)) if self._lossless(spec) else \
             (p - 1) * wire_size_bytes(spec, c)
         self._record(CommPath.Zero1AllGather, CollectiveKind.AllGather, p, (p - 1) * 4 * c, wire, p - 1, ev)
         return out

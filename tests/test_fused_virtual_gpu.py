@@ -236,3 +236,75 @@ def test_single_process_multi_gpu(cuda, env, layout):
     got, st = m.p2p(x, "fixed-rate", 8, 0, p - 1)
     assert st == 0
     assert got.tobytes() == O.p2p(x, "fixed-rate", 8)[0].tobytes()
+
+
+@pytest.mark.parametrize("p", [2, 3, 4])
+def test_lossless_on_the_wire_virtual(cuda, p):
+    """LosslessPredictor collectives through the engine's framed messages
+    (csrc/lossless_comm.cu): values exact (the oracle), and the payload bytes
+    each member actually pushed sum to the reference's wire accounting
+    (collectives.cpp:113-126, total / p)."""
+    import ctypes as C
+
+    import hccx_util as U
+    from paper_2409_02423_b200 import _lib
+
+    m = U.MComm(p, 1 << 18)
+
+    def pushed():
+        tot = 0
+        for j in range(p):
+            a, b = C.c_uint64(), C.c_uint64()
+            assert _lib.hccx_mcomm_wire_bytes(m.h, j, C.byref(a), C.byref(b)) == 0
+            assert b.value >= a.value
+            tot += a.value
+        return tot
+
+    for n_per, mode in ((1000, "sparse"), (4096 * 3 + 17, "normal"), (20000, "uniform")):
+        n = n_per * p
+        x = _inputs(n_per + p, p, n, mode if mode != "sparse" else "uniform")
+        if mode == "sparse":
+            x[:, ::3] = 0.0
+        for avg in (False, True):
+            got, st = m.allreduce(x, "lossless", 0, avg)
+            assert st == 0
+            want, acct = O.allreduce(x, "lossless", 0, avg)
+            assert got.tobytes() == want.tobytes(), (p, n, avg)
+            assert pushed() // p == acct[1], (p, n, avg, pushed(), acct)
+        got, st = m.reduce_scatter(x, "lossless")
+        assert st == 0
+        want, acct = O.reduce_scatter(x, "lossless")
+        assert got.tobytes() == want.tobytes()
+        assert pushed() // p == acct[1]
+        s = np.ascontiguousarray(x[:, :n_per])
+        got, st = m.allgather(s, "lossless")
+        assert st == 0
+        want, acct = O.allgather(s, "lossless")
+        assert got.tobytes() == want.tobytes()
+        assert pushed() // p == acct[1]
+        v = np.ascontiguousarray(x[0])
+        got, st = m.broadcast(v, p - 1, "lossless")
+        assert st == 0
+        assert got.tobytes() == O.broadcast(v, p, "lossless")[0].tobytes()
+        got, st = m.p2p(v, "lossless", 0, 0, p - 1)
+        assert st == 0
+        want, acct = O.p2p(v, "lossless")
+        assert got.tobytes() == want.tobytes()
+        assert pushed() == acct[1]
+
+
+def test_lossless_then_fused_same_slots(cuda, env):
+    """A lossless collective (framed messages, all-index acks) followed by
+    fused-kernel collectives on the same slots and back, no host sync."""
+    import hccx_util as U
+
+    p = 4
+    env(0, 0)
+    m = U.MComm(p, 1 << 20)
+    for kind, rate, n_per in (("fixed-rate", 8, 1 << 18), ("lossless", 0, 5000), ("fixed-rate", 4, 70000),
+                              ("lossless", 0, 1 << 18), ("identity", 0, 1 << 17)):
+        x = _inputs(n_per + rate, p, n_per * p)
+        got, st = m.allreduce(x, kind, rate)
+        assert st == 0
+        want, _ = O.allreduce(x, kind, rate)
+        assert got.tobytes() == want.tobytes(), (kind, rate, n_per)
