@@ -182,6 +182,10 @@ extern "C" hccx_status_t hccx_comm_destroy(hccx_comm_t c) {
       if (r != c->rank && c->peers[r]) cudaIpcCloseMemHandle(c->peers[r]);
   cudaFree(c->win);
   cudaFree(c->d_err);
+  cudaFree(c->ll_tmp);
+  cudaFree(c->ll_work);
+  cudaFree(c->ll_stage);
+  cudaFree(c->d_trace);
   delete c;
   return HCCX_OK;
 }

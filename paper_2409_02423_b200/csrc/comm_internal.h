@@ -41,6 +41,8 @@ struct hccx_comm {
   uint64_t ll_tmp_cap = 0;
   float* ll_work = nullptr;
   uint64_t ll_work_cap = 0;
+  uint8_t* ll_stage = nullptr;  // whole framed message: root staging / receiver reassembly
+  uint64_t ll_stage_cap = 0;
 };
 
 namespace hccx {

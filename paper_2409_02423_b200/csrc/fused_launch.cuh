@@ -86,10 +86,14 @@ cudaError_t launch_fused_codec(const FusedParams* P, int nv, cudaStream_t stream
   for (int v = 0; v < nv; ++v) {
     q[v] = P[v];
     q[v].ack_span = static_cast<uint32_t>(gcap);
-    if (q[v].step_segs == 0) {  // auto: about three published steps per phase per CTA, 2..16 segments each
+    if (q[v].step_segs == 0) {
+      // auto: ~8 published steps per phase per CTA, 1..8 segments each.
+      // Measured (tools/nvl_ab.py, 256 MiB r8): p = 4 1.07-1.10x faster
+      // with 1-2 segment steps than with 3 steps per phase (consumers start
+      // earlier; the signaller batches its system fences); p = 2 flat.
       const uint64_t myseg = (nseg + grid - 1) / grid;
-      const uint64_t s = (myseg + 2) / 3;
-      q[v].step_segs = static_cast<uint32_t>(s < 2 ? 2 : (s > 16 ? 16 : s));
+      const uint64_t s = (myseg + 7) / 8;
+      q[v].step_segs = static_cast<uint32_t>(s < 1 ? 1 : (s > 8 ? 8 : s));
     }
     if (q[v].first_segs == 0) q[v].first_segs = q[v].step_segs;
   }

@@ -197,9 +197,13 @@ struct LLRank {
   float* out = nullptr;
   float* work = nullptr;
   uint32_t epoch = 0, prev_rs = 0, prev_ag = 0;
-  uint32_t pp_ep = 0;       // broadcast / p2p: this message's epoch (sender: per destination)
-  uint32_t pp_send[kMaxRanks] = {};
-  uint64_t shard_payload = 0;
+  // broadcast / p2p: one message = the whole compressed container, carried
+  // in slot-sized fragments (each fragment one pp epoch)
+  bool pp_root = false, pp_recv = false;
+  uint64_t msg_bytes = 0;   // frame + payload (root: after compress; receiver: after fragment 0)
+  uint32_t nfrag = 0;
+  uint32_t frag_send[kMaxRanks] = {};  // root: epoch of the current fragment per destination
+  uint32_t frag_recv = 0;              // receiver: epoch of the current fragment
 };
 
 hccx_status_t ll_setup(LLRank& r, hccx_comm* c, int op, const float* in, float* out, uint64_t n, int mode, int root,
@@ -234,15 +238,11 @@ hccx_status_t ll_setup(LLRank& r, hccx_comm* c, int op, const float* in, float* 
     }
   } else {
     r.chunk = n;
-    if (c->rank == root) {
+    r.pp_root = c->rank == root;
+    r.pp_recv = !r.pp_root && (op == 3 || c->rank == dst);
+    if (r.pp_root)
       for (int d = 0; d < p; ++d)
-        if (d != root && (op == 3 || d == dst)) {
-          r.pp_send[d] = ++c->send_ep[d];
-          c->geo_pp[d] = lossless_key;
-        }
-    } else if (op == 3 || c->rank == dst) {
-      r.pp_ep = ++c->recv_ep[root];
-    }
+        if (d != root && (op == 3 || d == dst)) c->geo_pp[d] = lossless_key;
   }
   DeviceGuard guard(c->device);
   if (op == 0 || op == 1) {  // the ring folds into a work copy of the input
@@ -254,7 +254,17 @@ hccx_status_t ll_setup(LLRank& r, hccx_comm* c, int op, const float* in, float* 
     if (w != in && cudaMemcpyAsync(w, in, 4 * n, cudaMemcpyDeviceToDevice, s) != cudaSuccess) return HCCX_ERR_CUDA;
     r.work = w;
   }
-  if (ensure(c->ll_tmp, c->ll_tmp_cap, r.chunk) != HCCX_OK) return HCCX_ERR_CUDA;
+  if (op <= 2 && ensure(c->ll_tmp, c->ll_tmp_cap, r.chunk) != HCCX_OK) return HCCX_ERR_CUDA;
+  if (op >= 3 && (r.pp_root || r.pp_recv)) {  // message staging (root) / reassembly (receiver)
+    const uint64_t need = kFrameBytes + hccx_lossless_max_bytes(n);
+    if (need > c->ll_stage_cap) {
+      cudaFree(c->ll_stage);
+      c->ll_stage = nullptr;
+      c->ll_stage_cap = 0;
+      if (cudaMalloc(&c->ll_stage, need) != cudaSuccess) return HCCX_ERR_CUDA;
+      c->ll_stage_cap = need;
+    }
+  }
   return HCCX_OK;
 }
 
@@ -332,41 +342,97 @@ hccx_status_t ll_ag_recv(LLRank& r) {
   return HCCX_OK;
 }
 
-// Broadcast / p2p (one pass of at most chunk_cap values).
-hccx_status_t ll_pp_send(LLRank& r) {
+// Broadcast / p2p (no reference counterpart for broadcast, SURVEY.md §8
+// a10; p2p: collectives.cpp:130-152).  The root compresses the whole
+// message once into its staging buffer -- the reference's single
+// container, so the bytes on the wire are exactly its payload -- and sends
+// it in slot-sized fragments; every receiver reassembles, then decodes.
+hccx_status_t ll_pp_prepare(LLRank& r) {
   hccx_comm* c = r.c;
+  if (!r.pp_root || r.n == 0) return HCCX_OK;
+  DeviceGuard guard(c->device);
+  uint64_t bytes = 0;
+  hccx_status_t st = hccx_lossless_compress(r.in, r.n, c->ll_stage + kFrameBytes, c->ll_stage_cap - kFrameBytes,
+                                            &bytes, r.s);
+  if (st != HCCX_OK) return st;
+  ll_frame_kernel<<<1, 32, 0, r.s>>>(c->ll_stage, 18 + bytes, r.n,
+                                     static_cast<uint32_t>((r.n + kPredictorChunk - 1) / kPredictorChunk));
+  count_launch();
+  r.msg_bytes = kFrameBytes + bytes;
+  r.nfrag = static_cast<uint32_t>((r.msg_bytes + c->slot_bytes - 1) / c->slot_bytes);
+  return launched();
+}
+
+// Fragment f: returns HCCX_OK and sets *active when this rank had work.
+hccx_status_t ll_pp_send_frag(LLRank& r, uint32_t f, bool* active) {
+  hccx_comm* c = r.c;
+  if (!r.pp_root || f >= r.nfrag) return HCCX_OK;
+  *active = true;
   DeviceGuard guard(c->device);
   const int p = c->p, j = c->rank;
-  if (j != r.root) return HCCX_OK;
+  const uint64_t off = static_cast<uint64_t>(f) * c->slot_bytes;
+  const uint64_t len = r.msg_bytes - off < c->slot_bytes ? r.msg_bytes - off : c->slot_bytes;
   for (int d = 0; d < p; ++d) {
-    if (!r.pp_send[d]) continue;
-    const hccx_status_t st = credit(c, 5, d, r.pp_send[d] - 1, r.s);
+    if (d == j || !(r.op == 3 || d == r.dst)) continue;
+    r.frag_send[d] = ++c->send_ep[d];
+    hccx_status_t st = credit(c, 5, d, r.frag_send[d] - 1, r.s);
     if (st != HCCX_OK) return st;
+    if (cudaMemcpyAsync(host_slot(c, d, 2, j), c->ll_stage + off, len, cudaMemcpyDeviceToDevice, r.s) != cudaSuccess)
+      return HCCX_ERR_CUDA;
+    if ((st = signal(c, d, 2, j, 1, r.frag_send[d], r.s)) != HCCX_OK) return st;
+    c->last_frame += len;
+    const uint64_t hdr_part = off < kFrameBytes ? (kFrameBytes - off < len ? kFrameBytes - off : len) : 0;
+    c->last_payload += len - hdr_part;
   }
-  uint64_t bytes = 0;
-  hccx_status_t st = send_frame(c, r.in, r.n, j, 2, j, r.s, &bytes);  // staging: own pp[root] slot
-  if (st != HCCX_OK) return st;
-  c->last_payload -= bytes;
-  c->last_frame -= kFrameBytes + bytes;
-  const uint8_t* frame = host_slot(c, j, 2, j);
-  for (int d = 0; d < p; ++d) {
-    if (!r.pp_send[d]) continue;
-    if ((st = copy_frame(c, frame, bytes, d, 2, j, r.s)) != HCCX_OK) return st;
-    if ((st = signal(c, d, 2, j, 1, r.pp_send[d], r.s)) != HCCX_OK) return st;
-  }
-  if (r.op == 3 && r.out && r.out != r.in &&
-      cudaMemcpyAsync(r.out, r.in, 4 * r.n, cudaMemcpyDeviceToDevice, r.s) != cudaSuccess)
-    return HCCX_ERR_CUDA;
   return HCCX_OK;
 }
 
-hccx_status_t ll_pp_recv(LLRank& r) {
+hccx_status_t ll_pp_recv_frag(LLRank& r, uint32_t f, bool* active) {
   hccx_comm* c = r.c;
-  if (!r.pp_ep) return HCCX_OK;
+  if (!r.pp_recv || r.n == 0 || (f > 0 && f >= r.nfrag)) return HCCX_OK;
+  *active = true;
   DeviceGuard guard(c->device);
-  hccx_status_t st = recv_frame(c, 2, r.root, r.pp_ep, r.n, r.out, r.s);
+  r.frag_recv = ++c->recv_ep[r.root];
+  hccx_status_t st = wait(c, 2, r.root, 1, r.frag_recv, r.s);
   if (st != HCCX_OK) return st;
-  return ack(c, r.root, 5, c->rank, r.pp_ep, r.s);
+  const uint64_t off = static_cast<uint64_t>(f) * c->slot_bytes;
+  if (f == 0) {  // the frame: how many fragments follow (hcc::from_bytes checks)
+    uint8_t h[26];
+    uint32_t err = 0;
+    if (cudaMemcpyAsync(h, host_slot(c, c->rank, 2, r.root), 26, cudaMemcpyDeviceToHost, r.s) != cudaSuccess ||
+        cudaMemcpyAsync(&err, c->d_err, 4, cudaMemcpyDeviceToHost, r.s) != cudaSuccess ||
+        cudaStreamSynchronize(r.s) != cudaSuccess)
+      return HCCX_ERR_CUDA;
+    if (err & kErrTimeout) return HCCX_ERR_TIMEOUT;
+    uint64_t container = 0, n = 0;
+    uint32_t chunks = 0;
+    for (int i = 0; i < 8; ++i) container |= static_cast<uint64_t>(h[i]) << (8 * i);
+    for (int i = 0; i < 8; ++i) n |= static_cast<uint64_t>(h[14 + i]) << (8 * i);
+    for (int i = 0; i < 4; ++i) chunks |= static_cast<uint32_t>(h[22 + i]) << (8 * i);
+    if (container < 18 || kFrameBytes + container - 18 > c->ll_stage_cap || std::memcmp(h + 8, "HCC1", 4) != 0 ||
+        h[12] != HCCX_CODEC_LOSSLESS || n != r.n || chunks != (r.n + kPredictorChunk - 1) / kPredictorChunk)
+      return HCCX_ERR_CORRUPT_PAYLOAD;
+    r.msg_bytes = kFrameBytes + container - 18;
+    r.nfrag = static_cast<uint32_t>((r.msg_bytes + c->slot_bytes - 1) / c->slot_bytes);
+  }
+  const uint64_t len = r.msg_bytes - off < c->slot_bytes ? r.msg_bytes - off : c->slot_bytes;
+  if (cudaMemcpyAsync(c->ll_stage + off, host_slot(c, c->rank, 2, r.root), len, cudaMemcpyDeviceToDevice, r.s) !=
+      cudaSuccess)
+    return HCCX_ERR_CUDA;
+  return ack(c, r.root, 5, c->rank, r.frag_recv, r.s);
+}
+
+hccx_status_t ll_pp_complete(LLRank& r) {
+  hccx_comm* c = r.c;
+  DeviceGuard guard(c->device);
+  if (r.pp_recv && r.n) {
+    c->last_recv = r.msg_bytes - kFrameBytes;
+    return hccx_lossless_decompress(c->ll_stage + kFrameBytes, r.msg_bytes - kFrameBytes, r.n, r.out, r.s);
+  }
+  if (r.pp_root && r.op == 3 && r.out && r.out != r.in && r.n &&
+      cudaMemcpyAsync(r.out, r.in, 4 * r.n, cudaMemcpyDeviceToDevice, r.s) != cudaSuccess)
+    return HCCX_ERR_CUDA;
+  return HCCX_OK;
 }
 
 hccx_status_t ll_finish(LLRank& r, const StepParams& div) {
@@ -408,8 +474,14 @@ hccx_status_t ll_run(std::vector<LLRank>& ranks, const StepParams& div) {
     if (!all([&](LLRank& r) { return ll_ag_recv(r); })) return st;
   }
   if (r0.op == 3 || r0.op == 4) {
-    if (!all([&](LLRank& r) { return ll_pp_send(r); })) return st;
-    if (!all([&](LLRank& r) { return ll_pp_recv(r); })) return st;
+    if (!all([&](LLRank& r) { return ll_pp_prepare(r); })) return st;
+    for (uint32_t f = 0;; ++f) {  // every rank's fragment f before anyone's fragment f+1
+      bool active = false;
+      if (!all([&](LLRank& r) { return ll_pp_send_frag(r, f, &active); })) return st;
+      if (!all([&](LLRank& r) { return ll_pp_recv_frag(r, f, &active); })) return st;
+      if (!active) break;
+    }
+    if (!all([&](LLRank& r) { return ll_pp_complete(r); })) return st;
   }
   all([&](LLRank& r) { return ll_finish(r, div); });
   return st;
@@ -454,35 +526,13 @@ hccx_status_t ll_collective(hccx_comm* const* comms, int nr, int op, const float
     }
     return ll_run(ranks, div);
   }
-  // broadcast / p2p: passes of whole 4096-value predictor chunks (the codec
-  // restarts at every pass start, exactly like hcc::compress on a slice
-  // boundary that is a chunk multiple... so the concatenated passes are one
-  // message's values)
-  const uint64_t pass = comms[0]->chunk_cap / kPredictorChunk * kPredictorChunk;
-  uint64_t acc_payload[kMaxRanks] = {}, acc_frame[kMaxRanks] = {}, acc_recv[kMaxRanks] = {};
-  for (uint64_t off = 0; off < n; off += pass) {
-    const uint64_t m = n - off < pass ? n - off : pass;
-    std::vector<LLRank> ranks(nr);
-    for (int k = 0; k < nr; ++k) {
-      const float* src = in[k] ? in[k] + off : nullptr;
-      float* dstp = out[k] ? out[k] + off : nullptr;
-      const hccx_status_t st = ll_setup(ranks[k], comms[k], op, src, dstp, m, mode, root, dst, streams[k]);
-      if (st != HCCX_OK) return st;
-    }
-    const hccx_status_t st = ll_run(ranks, div);
-    if (st != HCCX_OK) return st;
-    for (int k = 0; k < nr; ++k) {
-      acc_payload[k] += comms[k]->last_payload;
-      acc_frame[k] += comms[k]->last_frame;
-      acc_recv[k] += comms[k]->last_recv;
-    }
-  }
+  // broadcast / p2p: one message in fragments (ll_pp_*)
+  std::vector<LLRank> ranks(nr);
   for (int k = 0; k < nr; ++k) {
-    comms[k]->last_payload = acc_payload[k];
-    comms[k]->last_frame = acc_frame[k];
-    comms[k]->last_recv = acc_recv[k];
+    const hccx_status_t st = ll_setup(ranks[k], comms[k], op, in[k], out[k], n, mode, root, dst, streams[k]);
+    if (st != HCCX_OK) return st;
   }
-  return HCCX_OK;
+  return ll_run(ranks, div);
 }
 
 }  // namespace hccx
