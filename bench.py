@@ -39,7 +39,8 @@ sys.path.insert(0, ROOT)
 
 METRIC = "compressed allreduce effective GB/s (uncompressed bytes/s) at 8xB200; codec GB/s vs HBM"
 L2_BYTES = 126 * 1024 * 1024
-NVLINK_PEAK = 900.0  # GB/s per direction per GPU (NVLink 5, B200_PROFILING.md / BASELINE.md)
+NVLINK_PEAK = 770.0  # GB/s per direction per GPU: measured peer copy (B200_PROFILING.md; 900 nominal)
+NVLINK_NOMINAL = 900.0
 SOAK_S = 0.15        # clock-record region (seconds of back-to-back steps) before the timed K steps
 
 
@@ -571,9 +572,10 @@ def bench_allreduce(args):
                          "achieved": round(hbm_ach if bound == "hbm" else nvl_ach, 1),
                          "peak": hbm if bound == "hbm" else NVLINK_PEAK, "unit": "GB/s",
                          "frac": round((hbm_ach / hbm) if bound == "hbm" else (nvl_ach / NVLINK_PEAK), 4),
-                         "peak_source": peak_src if bound == "hbm" else "NVLink 5 nominal per direction",
+                         "peak_source": peak_src if bound == "hbm" else "NVLink measured peer copy, B200_PROFILING.md",
                          "hbm_bytes_per_launch": hbm_bytes, "nvlink_bytes_per_launch": wire_bytes,
                          "hbm_frac": round(hbm_ach / hbm, 4), "nvlink_frac": round(nvl_ach / NVLINK_PEAK, 4),
+                         "nvlink_frac_of_nominal_900": round(nvl_ach / NVLINK_NOMINAL, 4),
                          "traffic": traffic_for("ring_fused")},
             "cpu_baseline": cpu,
             "e2e": {"value": round(4 * n / e2e_s / 1e9, 3), "unit": "GB/s", "h2d_bytes_per_step": 4 * n,

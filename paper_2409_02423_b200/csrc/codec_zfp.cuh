@@ -16,6 +16,7 @@
 // values = 32R bytes).  Each lane codes its two blocks sequentially in
 // registers (two 64-bit words per block, no local memory).
 #pragma once
+#include <type_traits>
 #include "device_common.cuh"
 #include "zfp_planes.cuh"
 
@@ -55,8 +56,13 @@ __device__ __forceinline__ void inv_lift(int32_t& x, int32_t& y, int32_t& z, int
 
 // Block prologue: header (zero flag, biased emax) into b, the negabinary
 // coefficients into u; returns the bit-plane budget (0 for a zero block).
+// A block's 4R bits in the narrowest accumulator that holds them.
 template <int R>
-__device__ __forceinline__ uint32_t encode_head(const float (&v)[4], Bits128& b, uint32_t& bad, uint32_t (&u)[4]) {
+using Acc = typename std::conditional<(R <= 8), zfp_planes::Bits32,
+                                      typename std::conditional<(R <= 16), zfp_planes::Bits64, Bits128>::type>::type;
+
+template <int R, class B>
+__device__ __forceinline__ uint32_t encode_head(const float (&v)[4], B& b, uint32_t& bad, uint32_t (&u)[4]) {
   uint32_t fmax = 0;
 #pragma unroll
   for (int i = 0; i < 4; ++i) fmax = max(fmax, __float_as_uint(v[i]) & 0x7fffffffu);
@@ -82,21 +88,23 @@ __device__ __forceinline__ uint32_t encode_head(const float (&v)[4], Bits128& b,
   return 4 * R - 9;
 }
 
-// Two blocks -> 4R bits each: prologues, then both embedded codings in one
-// loop (zfp_planes.cuh steppers).
-template <int R>
-__device__ __forceinline__ void encode_pair(const float (&a)[4], const float (&c)[4], Bits128& b0, Bits128& b1,
-                                            uint32_t& bad) {
+// Two blocks -> 4R bits each: prologues, the significance planes of both
+// blocks in one loop (zfp_planes.cuh steppers, table-driven), then each
+// block's verbatim tail in one word operation.
+template <int R, class B>
+__device__ __forceinline__ void encode_pair(const float (&a)[4], const float (&c)[4], B& b0, B& b1, uint32_t& bad) {
   uint32_t ua[4], uc[4];
   const uint32_t ba = encode_head<R>(a, b0, bad, ua);
   const uint32_t bc = encode_head<R>(c, b1, bad, uc);
   zfp_planes::PlaneEnc e0, e1;
   e0.init(ua, ba, b0);
   e1.init(uc, bc, b1);
-  while (e0.active() || e1.active()) {
-    if (e0.active()) e0.step(b0);
-    if (e1.active()) e1.step(b1);
+  while (e0.sig_active() || e1.sig_active()) {
+    if (e0.sig_active()) e0.step(b0);
+    if (e1.sig_active()) e1.step(b1);
   }
+  e0.tail(b0);
+  e1.tail(b1);
 }
 
 __device__ __forceinline__ void finish_block(const uint32_t (&u)[4], int emax, bool zero, float (&v)[4]) {
@@ -114,20 +122,22 @@ __device__ __forceinline__ void finish_block(const uint32_t (&u)[4], int emax, b
   for (int i = 0; i < 4; ++i) v[i] = __double2float_rn(__dmul_rn(static_cast<double>(q[i]), s));
 }
 
-// Decode two blocks: headers, both embedded codings in one loop, then the
-// inverse transform of each.
-template <int R>
-__device__ __forceinline__ void decode_pair(Bits128& b0, Bits128& b1, float (&a)[4], float (&c)[4]) {
+// Decode two blocks: headers, the significance planes of both in one loop,
+// the verbatim tails, then the inverse transform of each.
+template <int R, class B>
+__device__ __forceinline__ void decode_pair(B& b0, B& b1, float (&a)[4], float (&c)[4]) {
   const bool z0 = !b0.get(1), z1 = !b1.get(1);
   const int e0 = z0 ? 0 : static_cast<int>(b0.get(8)) - 127;
   const int e1 = z1 ? 0 : static_cast<int>(b1.get(8)) - 127;
   zfp_planes::PlaneDec d0, d1;
   d0.init(b0, z0 ? 0u : 4u * R - 9u);
   d1.init(b1, z1 ? 0u : 4u * R - 9u);
-  while (d0.active() || d1.active()) {
-    if (d0.active()) d0.step(b0);
-    if (d1.active()) d1.step(b1);
+  while (d0.sig_active() || d1.sig_active()) {
+    if (d0.sig_active()) d0.step(b0);
+    if (d1.sig_active()) d1.step(b1);
   }
+  d0.tail(b0);
+  d1.tail(b1);
   finish_block(d0.u, e0, z0, a);
   finish_block(d1.u, e1, z1, c);
 }
@@ -163,7 +173,6 @@ struct ZfpRateCodec {
   // of this lane's values exist so partial blocks are padded like zfp.
   __device__ __forceinline__ static void encode(const float (&v)[8], Lane& s, uint32_t& bad,
                                                 uint32_t lane_live) {
-    zfp_detail::Bits128 b0, b1;
     float a[4], c[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
@@ -172,26 +181,33 @@ struct ZfpRateCodec {
     }
     pad(a, min(lane_live, 4u));
     pad(c, lane_live > 4 ? lane_live - 4 : 0u);
+    zfp_detail::Acc<R> b0, b1;
     zfp_detail::encode_pair<R>(a, c, b0, b1, bad);
-    // chunk = b0 (4R bits) | b1 << 4R
+    // lane chunk = b0 (4R bits) | b1 << 4R
     constexpr int S = 4 * R;
-    uint64_t c0 = b0.lo, c1 = b0.hi, c2 = 0, c3 = 0;
-    if constexpr (S < 64) {
-      c0 |= b1.lo << S;
-      c1 |= (b1.lo >> (64 - S)) | (b1.hi << S);
-      c2 |= b1.hi >> (64 - S);
-    } else if constexpr (S == 64) {
-      c1 |= b1.lo;
-      c2 |= b1.hi;
-    } else if constexpr (S < 128) {
-      c1 |= b1.lo << (S - 64);
-      c2 |= (b1.lo >> (128 - S)) | (b1.hi << (S - 64));
-      c3 |= b1.hi >> (128 - S);
+    uint64_t cw[4] = {0, 0, 0, 0};
+    if constexpr (R <= 8) {
+      cw[0] = static_cast<uint64_t>(b0.v) | (static_cast<uint64_t>(b1.v) << S);
+    } else if constexpr (R <= 16) {
+      cw[0] = b0.v;
+      if constexpr (S < 64) {
+        cw[0] |= b1.v << S;
+        cw[1] = b1.v >> (64 - S);
+      } else {
+        cw[1] = b1.v;
+      }
     } else {
-      c2 |= b1.lo;
-      c3 |= b1.hi;
+      uint64_t c0 = b0.lo, c1 = b0.hi, c2 = 0, c3 = 0;
+      if constexpr (S < 128) {
+        c1 |= b1.lo << (S - 64);
+        c2 |= (b1.lo >> (128 - S)) | (b1.hi << (S - 64));
+        c3 |= b1.hi >> (128 - S);
+      } else {
+        c2 |= b1.lo;
+        c3 |= b1.hi;
+      }
+      cw[0] = c0, cw[1] = c1, cw[2] = c2, cw[3] = c3;
     }
-    const uint64_t cw[4] = {c0, c1, c2, c3};
 #pragma unroll
     for (int w = 0; w < kWords; ++w) s.d[w] = static_cast<uint32_t>(cw[w >> 1] >> (32 * (w & 1)));
     s.hdr = 0;
@@ -202,23 +218,30 @@ struct ZfpRateCodec {
 #pragma unroll
     for (int w = 0; w < kWords; ++w) cw[w >> 1] |= static_cast<uint64_t>(s.d[w]) << (32 * (w & 1));
     constexpr int S = 4 * R;
-    zfp_detail::Bits128 b0, b1;
-    b0.lo = cw[0];
-    b0.hi = cw[1];
-    if constexpr (S < 64) {
-      b1.lo = (cw[0] >> S) | (cw[1] << (64 - S));
-      b1.hi = (cw[1] >> S) | (cw[2] << (64 - S));
-    } else if constexpr (S == 64) {
-      b1.lo = cw[1];
-      b1.hi = cw[2];
-    } else if constexpr (S < 128) {
-      b1.lo = (cw[1] >> (S - 64)) | (cw[2] << (128 - S));
-      b1.hi = (cw[2] >> (S - 64)) | (cw[3] << (128 - S));
+    zfp_detail::Acc<R> b0, b1;
+    if constexpr (R <= 8) {
+      b0.v = static_cast<uint32_t>(cw[0] & ((1ull << S) - 1ull));
+      b1.v = static_cast<uint32_t>(cw[0] >> S);
+    } else if constexpr (R <= 16) {
+      if constexpr (S < 64) {
+        b0.v = cw[0] & ((1ull << S) - 1ull);
+        b1.v = (cw[0] >> S) | (cw[1] << (64 - S));
+      } else {
+        b0.v = cw[0];
+        b1.v = cw[1];
+      }
     } else {
-      b1.lo = cw[2];
-      b1.hi = cw[3];
+      b0.lo = cw[0];
+      if constexpr (S < 128) {
+        b0.hi = cw[1] & ((1ull << (S - 64)) - 1ull);
+        b1.lo = (cw[1] >> (S - 64)) | (cw[2] << (128 - S));
+        b1.hi = (cw[2] >> (S - 64)) | (cw[3] << (128 - S));
+      } else {
+        b0.hi = cw[1];
+        b1.lo = cw[2];
+        b1.hi = cw[3];
+      }
     }
-    // mask block 0 to its 4R bits (decoder never reads past them, but keep it clean)
     float a[4], c[4];
     zfp_detail::decode_pair<R>(b0, b1, a, c);
 #pragma unroll

@@ -280,6 +280,86 @@ HCCX_HD Lut& lut() {
 #endif
 }
 
+// Narrow stream accumulators: a block's 4R bits fit in 32 bits for R <= 8
+// and in 64 bits for R <= 16, where put/peek are one shift and one OR.
+template <class W>
+struct BitsN {
+  static constexpr int kWidth = 8 * static_cast<int>(sizeof(W));
+  W v = 0;
+  int pos = 0;
+  HCCX_HD void put(uint64_t val, int nbits) {  // pos + nbits <= kWidth, val < 2^nbits
+    if (nbits) v |= static_cast<W>(val) << pos;
+    pos += nbits;
+  }
+  HCCX_HD uint64_t peek() const { return pos < kWidth ? static_cast<uint64_t>(v >> pos) : 0ull; }
+  HCCX_HD uint64_t get(int nbits) {
+    const uint64_t x = nbits ? peek() & ((1ull << nbits) - 1ull) : 0ull;
+    pos += nbits;
+    return x;
+  }
+};
+using Bits32 = BitsN<uint32_t>;
+using Bits64 = BitsN<uint64_t>;
+
+HCCX_HD uint32_t brev32(uint32_t v) {
+#if defined(__CUDA_ARCH__)
+  return __brev(v);
+#else
+  v = ((v >> 1) & 0x55555555u) | ((v & 0x55555555u) << 1);
+  v = ((v >> 2) & 0x33333333u) | ((v & 0x33333333u) << 2);
+  v = ((v >> 4) & 0x0f0f0f0fu) | ((v & 0x0f0f0f0fu) << 4);
+  v = ((v >> 8) & 0x00ff00ffu) | ((v & 0x00ff00ffu) << 8);
+  return (v >> 16) | (v << 16);
+#endif
+}
+
+// bit q of an 8-bit value -> bit 4q, and back
+HCCX_HD uint32_t spread4(uint32_t x) {
+  x = (x | (x << 12)) & 0x000f000fu;
+  x = (x | (x << 6)) & 0x03030303u;
+  return (x | (x << 3)) & 0x11111111u;
+}
+HCCX_HD uint32_t compact4(uint32_t x) {
+  x &= 0x11111111u;
+  x = (x | (x >> 3)) & 0x03030303u;
+  x = (x | (x >> 6)) & 0x000f000fu;
+  return (x | (x >> 12)) & 0xffu;
+}
+
+// Once all four coefficients are significant every plane is its 4 bits
+// verbatim, so the rest of the block is the plane-major interleave of the
+// coefficients' remaining bits, 8 planes per 32-bit word: nibble q = plane
+// k-q (bit i = coefficient i), truncated at the budget like the per-plane
+// codes.
+template <class B>
+HCCX_HD void put_verbatim(const uint32_t (&u)[4], int k, uint32_t budget, B& b) {
+  while (budget && k >= 0) {
+    const int m8 = k + 1 < 8 ? k + 1 : 8;
+    uint32_t v = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) v |= spread4((brev32(u[i]) >> (31 - k)) & 0xffu) << i;
+    const uint32_t bits = budget < 4u * m8 ? budget : 4u * m8;
+    b.put(bits >= 32 ? v : v & ((1u << bits) - 1u), static_cast<int>(bits));
+    budget -= bits;
+    k -= m8;
+  }
+}
+
+template <class B>
+HCCX_HD void get_verbatim(B& b, int k, uint32_t budget, uint32_t (&u)[4]) {
+  while (budget && k >= 0) {
+    const int m8 = k + 1 < 8 ? k + 1 : 8;
+    const uint32_t bits = budget < 4u * m8 ? budget : 4u * m8;
+    uint32_t w = static_cast<uint32_t>(b.peek());
+    if (bits < 32) w &= (1u << bits) - 1u;
+    b.pos += static_cast<int>(bits);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) u[i] |= brev32(compact4(w >> i)) >> (31 - k);
+    budget -= bits;
+    k -= m8;
+  }
+}
+
 // Steppers for coding two blocks in one loop (a lane owns two blocks: the
 // joint loop runs max(planes) iterations instead of their sum and gives the
 // two independent dependency chains to the scheduler side by side).  Same
@@ -288,7 +368,8 @@ struct PlaneEnc {
   uint32_t u[4];
   uint32_t budget, n;
   int k;
-  HCCX_HD void init(const uint32_t (&uu)[4], uint32_t bud, Bits& b) {
+  template <class B>
+  HCCX_HD void init(const uint32_t (&uu)[4], uint32_t bud, B& b) {
     u[0] = uu[0], u[1] = uu[1], u[2] = uu[2], u[3] = uu[3];
     const int G = max(max(top_bit(u[0]), top_bit(u[1])), max(top_bit(u[2]), top_bit(u[3])));
     const uint32_t lead = static_cast<uint32_t>(31 - G);
@@ -299,7 +380,16 @@ struct PlaneEnc {
     n = 0;
   }
   HCCX_HD bool active() const { return budget != 0 && k >= 0; }
-  HCCX_HD void step(Bits& b) {
+  // significance phase: planes until all four coefficients are significant
+  HCCX_HD bool sig_active() const { return budget != 0 && k >= 0 && n < 4; }
+  // then the verbatim tail in one go
+  template <class B>
+  HCCX_HD void tail(B& b) {
+    put_verbatim(u, k, budget, b);
+    budget = 0;
+  }
+  template <class B>
+  HCCX_HD void step(B& b) {
     const uint32_t x = plane_bits(u, k);
     uint32_t code = x, nn = 4, len = 4;  // all significant: verbatim plane
     if (n < 4) {
@@ -320,7 +410,8 @@ struct PlaneDec {
   uint32_t u[4];
   uint32_t budget, n;
   int k;
-  HCCX_HD void init(Bits& b, uint32_t bud) {
+  template <class B>
+  HCCX_HD void init(B& b, uint32_t bud) {
     u[0] = u[1] = u[2] = u[3] = 0;
     const uint64_t w = b.peek();
     uint32_t lead = w ? static_cast<uint32_t>(
@@ -339,7 +430,14 @@ struct PlaneDec {
     n = 0;
   }
   HCCX_HD bool active() const { return budget != 0 && k >= 0; }
-  HCCX_HD void step(Bits& b) {
+  HCCX_HD bool sig_active() const { return budget != 0 && k >= 0 && n < 4; }
+  template <class B>
+  HCCX_HD void tail(B& b) {
+    get_verbatim(b, k, budget, u);
+    budget = 0;
+  }
+  template <class B>
+  HCCX_HD void step(B& b) {
     uint32_t used, x;
     const uint64_t w = b.peek();
     if (n == 4) {
