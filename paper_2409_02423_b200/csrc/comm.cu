@@ -112,8 +112,9 @@ extern "C" hccx_status_t hccx_comm_create(int rank, int nranks, int device, uint
   c->flag_off = c->pp_off + nranks * c->slot_bytes;
   // one-shot region (oneshot.cuh): p-1 raw fp32 slots + p gather slots + flags
   c->os_cap = c->chunk_cap < kOneShotMaxChunk ? c->chunk_cap : kOneShotMaxChunk;
-  c->os_raw_bytes = align_up(4 * c->os_cap, 256);
-  c->os_ag_bytes = align_up((c->os_cap + 63) / 64 * 257, 256);
+  // flag-in-data pairs (oneshot.cuh): 8 bytes per raw value / payload word
+  c->os_raw_bytes = align_up(8 * c->os_cap, 256);
+  c->os_ag_bytes = align_up(2 * ((c->os_cap + 63) / 64 * 257 + 4), 256);
   // data flags: 3p-1 slots x max_seg; acks: 4p-1 slots x kAckIdx (ring_fused.cuh flag classes)
   c->os_off = c->flag_off + align_up((nslots * c->max_seg + (nslots + nranks) * kAckIdx) * 4, 256);
   c->os_ag_off = c->os_off + (nranks - 1) * c->os_raw_bytes;
