@@ -112,14 +112,20 @@ extern "C" hccx_status_t hccx_comm_create(int rank, int nranks, int device, uint
   c->flag_off = c->pp_off + nranks * c->slot_bytes;
   // one-shot region (oneshot.cuh): p-1 raw fp32 slots + p gather slots + flags
   c->os_cap = c->chunk_cap < kOneShotMaxChunk ? c->chunk_cap : kOneShotMaxChunk;
-  // flag-in-data pairs (oneshot.cuh): 8 bytes per raw value / payload word
-  c->os_raw_bytes = align_up(8 * c->os_cap, 256);
-  c->os_ag_bytes = align_up(2 * ((c->os_cap + 63) / 64 * 257 + 4), 256);
+  // flag mode: raw fp32 / payload bytes; pair mode (flag-in-data): 8 bytes
+  // per raw value / payload word -- separate regions (oneshot.cuh)
+  c->os_raw_bytes = align_up(4 * c->os_cap, 256);
+  c->os_ag_bytes = align_up((c->os_cap + 63) / 64 * 257, 256);
+  c->os_ll_raw_bytes = align_up(8 * c->os_cap, 256);
+  c->os_ll_ag_bytes = align_up(2 * ((c->os_cap + 63) / 64 * 257 + 4), 256);
   // data flags: 3p-1 slots x max_seg; acks: 4p-1 slots x kAckIdx (ring_fused.cuh flag classes)
   c->os_off = c->flag_off + align_up((nslots * c->max_seg + (nslots + nranks) * kAckIdx) * 4, 256);
   c->os_ag_off = c->os_off + (nranks - 1) * c->os_raw_bytes;
   c->os_flag_off = c->os_ag_off + nranks * c->os_ag_bytes;
-  c->win_bytes = c->os_flag_off + align_up(2ull * nranks * kAckIdx * 4, 256);
+  c->os_ll_off = c->os_flag_off + align_up(2ull * nranks * kAckIdx * 4, 256);
+  c->os_ll_ag_off = c->os_ll_off + (nranks - 1) * c->os_ll_raw_bytes;
+  // everything from os_flag_off on is zeroed: flags, and pair epochs (epochs start at 1)
+  c->win_bytes = c->os_ll_ag_off + nranks * c->os_ll_ag_bytes;
   if (cudaMalloc(&c->win, c->win_bytes) != cudaSuccess || cudaMalloc(&c->d_err, 4) != cudaSuccess) {
     cudaFree(c->win);
     delete c;
@@ -234,6 +240,10 @@ FusedParams base_params(hccx_comm* c, int op, uint64_t n_chunk, const float* in,
   P.os_flag_off = c->os_flag_off;
   P.os_raw_bytes = c->os_raw_bytes;
   P.os_ag_bytes = c->os_ag_bytes;
+  P.os_ll_off = c->os_ll_off;
+  P.os_ll_ag_off = c->os_ll_ag_off;
+  P.os_ll_raw_bytes = c->os_ll_raw_bytes;
+  P.os_ll_ag_bytes = c->os_ll_ag_bytes;
   P.trace = c->d_trace;
   P.trace_cap = c->trace_cap;
   // chunk offsets are multiples of n_chunk floats: aligned iff n_chunk % 8 == 0
@@ -262,14 +272,19 @@ hccx_status_t check_comm(hccx_comm* c, hccx_codec_t codec) {
 // Allreduce algorithm choice: the two-round one-shot path up to
 // HCCX_ONESHOT_BYTES (bytes per rank, default below; 0 disables it), the
 // fused ring above.  Both give the reference's bits.
-bool use_oneshot(const hccx_comm* c, uint64_t n) {
-  // default: 4 MiB per rank per peer count (16 MiB at p = 4, measured
-  // crossover; the ring's 2(p-1) dependent rounds grow with p while the
-  // one-shot path keeps two)
+// 0: fused ring; 1: one-shot, flag mode; 2: one-shot, pair (LL) mode.
+int use_oneshot(const hccx_comm* c, uint64_t n) {
+  // defaults: one-shot up to 4 MiB per rank per peer (16 MiB at p = 4: the
+  // ring's 2(p-1) dependent rounds grow with p while the one-shot path keeps
+  // two), pair mode up to 2 MiB per peer (measured tools/nvl_small.py, p = 4:
+  // pairs 28 us vs flags 29 us at 4 MiB, 79 vs 59 us at 16 MiB)
   const char* e = std::getenv("HCCX_ONESHOT_BYTES");
   const int64_t limit = e ? static_cast<int64_t>(std::strtoull(e, nullptr, 10)) : int64_t{-1};
   const uint64_t lim = limit >= 0 ? static_cast<uint64_t>(limit) : kOneShotBytesPerRank * c->p;
-  return 4 * n <= lim && n / c->p <= c->os_cap;
+  if (!(4 * n <= lim && n / c->p <= c->os_cap)) return 0;
+  const char* l = std::getenv("HCCX_LL_BYTES");
+  const uint64_t ll = l ? std::strtoull(l, nullptr, 10) : (2ull << 20) * c->p;
+  return 4 * n <= ll ? 2 : 1;
 }
 
 // One rank's share of a collective: a device-to-device copy (p == 1 and
@@ -304,8 +319,9 @@ hccx_status_t plan_allreduce(hccx_comm* c, const float* d_in, float* d_out, uint
   }
   FusedParams P = base_params(c, kFAllReduce, n / c->p, d_in, d_out);
   P.epoch = ++c->epoch;
-  if (use_oneshot(c, n)) {
+  if (const int os = use_oneshot(c, n)) {
     P.op = kFOneShotAllReduce;  // own slots and flags: the ring's slot epochs are untouched
+    P.os_ll = os == 2 ? 1 : 0;
   } else {
     P.prev_rs = c->last_rs;
     P.prev_ag = c->last_ag;
@@ -316,7 +332,7 @@ hccx_status_t plan_allreduce(hccx_comm* c, const float* d_in, float* d_out, uint
   }
   {
     const uint64_t W = payload_bytes(sel_of(codec), n / c->p);
-    c->last_payload = c->last_frame = P.op == kFOneShotAllReduce ? (c->p - 1) * (4 * (n / c->p) + W)
+    c->last_payload = c->last_frame = P.op == kFOneShotAllReduce ? (P.os_ll ? 2 : 1) * (c->p - 1) * (4 * (n / c->p) + W)
                                                                   : 2ull * (c->p - 1) * W;
   }
   StepParams tmp{};

@@ -15,6 +15,7 @@ struct hccx_comm {
   uint64_t rs_off = 0, ag_off = 0, pp_off = 0, flag_off = 0, win_bytes = 0;
   uint64_t os_cap = 0;  // one-shot allreduce: values per chunk
   uint64_t os_off = 0, os_ag_off = 0, os_flag_off = 0, os_raw_bytes = 0, os_ag_bytes = 0;
+  uint64_t os_ll_off = 0, os_ll_ag_off = 0, os_ll_raw_bytes = 0, os_ll_ag_bytes = 0;
   uint8_t* win = nullptr;
   uint8_t* peers[hccx::kMaxRanks] = {};
   bool connected = false;

@@ -17,12 +17,18 @@
 //      and stores the final payload m into every peer's gather slot j;
 //   C  every rank decodes the p-1 gathered payloads into its output.
 //
-// Flag-in-data (the LL idea of NCCL's low-latency protocol): every 4-byte
+// Two transports, chosen per call by size (comm.cu use_oneshot):
+//
+// Pair mode, the small end -- flag-in-data (the LL idea of NCCL's low-latency protocol): every 4-byte
 // word crosses NVLink as an 8-byte (word, epoch) pair in one store (raw
 // values go two pairs per 16-byte store), and the reader polls the pairs themselves until each
 // carries this call's epoch -- no system-scope fence, no separate flag, no
 // acquire round trip per step.  The wire carries twice the bytes, the right
 // trade below a few MiB where latency, not bandwidth, is the cost.
+//
+// Flag mode, the upper end: raw words and payload bytes as they are, one
+// system-scope release per CTA and phase (half the wire bytes).  The two
+// modes use separate window regions, so calls may alternate freely.
 //
 // Only the wire traffic differs from the ring: (p-1) raw chunks out per rank
 // instead of p-1 compressed ones.  Slot reuse needs no acks: a rank reaches
@@ -101,8 +107,131 @@ __device__ __forceinline__ uint4 wait_ll2(const FusedParams& P, const uint4* src
   }
 }
 
+// ---------------------------------------------------------------------------
+// Flag mode, for the upper end of the one-shot range: raw fp32 words and
+// plain payload bytes (half the wire bytes of the pair mode), published per
+// CTA with a system-scope release and waited for with acquire loads.
+__device__ __forceinline__ uint32_t* os_flag(const FusedParams& P, int rank, int kind, int slot, uint32_t idx) {
+  return reinterpret_cast<uint32_t*>(P.win[rank] + P.os_flag_off) +
+         (static_cast<uint64_t>(kind) * P.p + slot) * kAckIdx + idx;
+}
+
 template <class Codec>
-__device__ __forceinline__ void oneshot_body(const FusedParams& P, const uint32_t cta, const uint32_t G) {
+__device__ __forceinline__ void oneshot_flags_body(const FusedParams& P, const uint32_t cta, const uint32_t G) {
+  __shared__ __align__(16) uint8_t stage[kOsWarps][kStageBytes];
+  const int lane = static_cast<int>(lane_id()), warp = static_cast<int>(threadIdx.x >> 5);
+  const int p = P.p, j = P.rank;
+  const uint64_t c = P.n_chunk;
+  const uint64_t GB = Codec::kGroupBytes;
+  const uint64_t wire = Codec::wire_bytes(c);
+  const uint64_t gc = (c + kGroupVals - 1) / kGroupVals;
+  const uint64_t gpc = (gc + G - 1) / G;
+  const uint64_t g0 = min(cta * gpc, gc), g1 = min(g0 + gpc, gc);
+  const uint64_t v0 = min(g0 * kGroupVals, c), v1 = min(g1 * kGroupVals, c);
+  const bool vec = P.vec_ok != 0;
+  uint8_t* sm = stage[warp];
+  uint32_t bad = 0;
+  if constexpr (Codec::kNeedsInit) {
+    Codec::kernel_init();
+    __syncthreads();
+  }
+  auto raw_slot = [&](int rank, int t) {
+    return reinterpret_cast<float*>(P.win[rank] + P.os_off + static_cast<uint64_t>(t) * P.os_raw_bytes);
+  };
+  auto ag_slot = [&](int rank, int src) {
+    return P.win[rank] + P.os_ag_off + static_cast<uint64_t>(src) * P.os_ag_bytes;
+  };
+
+  // ---- A: raw scatter of this CTA's value range of every peer's chunk
+  for (int q = 1; q < p; ++q) {
+    const int d = (j + q) % p;
+    const int t = (j - d - 1 + 2 * p) % p;
+    const float* src = P.in + static_cast<uint64_t>(d) * c;
+    float* dst = raw_slot(d, t);
+    if (vec) {
+      for (uint64_t i = v0 / 4 + threadIdx.x; i < v1 / 4; i += blockDim.x)
+        reinterpret_cast<float4*>(dst)[i] = reinterpret_cast<const float4*>(src)[i];
+      for (uint64_t i = (v1 / 4) * 4 + threadIdx.x; i < v1; i += blockDim.x) dst[i] = src[i];
+    } else {
+      for (uint64_t i = v0 + threadIdx.x; i < v1; i += blockDim.x) dst[i] = src[i];
+    }
+  }
+  __syncthreads();  // every thread's stores precede the releases below (bar.sync + release cumulativity)
+  if (threadIdx.x < static_cast<unsigned>(p - 1)) {
+    const int d = (j + 1 + static_cast<int>(threadIdx.x)) % p;
+    signal(os_flag(P, d, 0, (j - d - 1 + 2 * p) % p, cta), P.epoch);
+  }
+
+  // ---- B: replay the ring chain of chunk j for this CTA's groups
+  if (threadIdx.x < static_cast<unsigned>(p - 1)) spin_ge(P, os_flag(P, j, 0, threadIdx.x, cta), P.epoch, 0xb00u);
+  __syncthreads();
+  for (uint64_t g = g0 + warp; g < g1; g += kOsWarps) {
+    const uint64_t base = g * kGroupVals;
+    const uint32_t live = static_cast<uint32_t>(c - base < kGroupVals ? c - base : kGroupVals);
+    const uint32_t ll = lane_live(live, lane);
+    typename Codec::Lane s;
+    float v[8], loc[8];
+    load_vals<false>(raw_slot(j, 0), base, live, true, lane, v);
+    Codec::encode(v, s, bad, ll);
+    for (int t = 1; t < p; ++t) {
+      Codec::decode(s, v);
+      const float* x = t < p - 1 ? raw_slot(j, t) : P.in + static_cast<uint64_t>(j) * c;
+      load_vals<false>(x, base, live, t < p - 1 ? true : vec, lane, loc);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[i] = __fadd_rn(v[i], loc[i]);  // arriving partial on the left
+      Codec::encode(v, s, bad, ll);
+    }
+    Codec::decode(s, v);
+    apply_div(v, P.div_mode, P.recip, P.divisor);
+    store_vals(P.out + static_cast<uint64_t>(j) * c, base, live, vec, lane, v);
+    // final payload -> every peer's gather slot j (4-byte stores; group
+    // offsets are 4-byte multiples, the buffer's last group may end mid-word)
+    Codec::to_stage(s, sm, lane);
+    __syncwarp();
+    const uint32_t nb = static_cast<uint32_t>(min(GB, wire - g * GB));
+    for (int q = 1; q < p; ++q) {
+      uint8_t* dst = ag_slot((j + q) % p, j) + g * GB;
+      for (uint32_t w = lane; w < nb / 4; w += 32)
+        reinterpret_cast<uint32_t*>(dst)[w] = reinterpret_cast<const uint32_t*>(sm)[w];
+      for (uint32_t b = (nb / 4) * 4 + lane; b < nb; b += 32) dst[b] = sm[b];
+    }
+    __syncwarp();
+  }
+  __syncthreads();
+  if (threadIdx.x < static_cast<unsigned>(p - 1)) {
+    const int d = (j + 1 + static_cast<int>(threadIdx.x)) % p;
+    signal(os_flag(P, d, 1, j, cta), P.epoch);
+  }
+
+  // ---- C: decode every peer's shard (this CTA's groups of it)
+  if (threadIdx.x < static_cast<unsigned>(p - 1)) {
+    const int src = (j + 1 + static_cast<int>(threadIdx.x)) % p;
+    spin_ge(P, os_flag(P, j, 1, src, cta), P.epoch, 0xc00u);
+  }
+  __syncthreads();
+  for (int q = 1; q < p; ++q) {
+    const int src = (j + q) % p;
+    const uint8_t* pay = ag_slot(j, src);
+    for (uint64_t g = g0 + warp; g < g1; g += kOsWarps) {
+      const uint64_t base = g * kGroupVals;
+      const uint32_t live = static_cast<uint32_t>(c - base < kGroupVals ? c - base : kGroupVals);
+      typename Codec::Lane s;
+      float v[8];
+      group_load<Codec, false>(s, pay + g * GB, live, true, sm, lane);
+      Codec::decode(s, v);
+      apply_div(v, P.div_mode, P.recip, P.divisor);
+      store_vals(P.out + static_cast<uint64_t>(src) * c, base, live, vec, lane, v);
+    }
+  }
+  if constexpr (Codec::kCheckFinite) {
+    if (__any_sync(kFull, bad) && lane == 0 && P.err) atomicOr(P.err, kErrNonFinite);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Pair (LL) mode.
+template <class Codec>
+__device__ __forceinline__ void oneshot_ll_body(const FusedParams& P, const uint32_t cta, const uint32_t G) {
   __shared__ __align__(16) uint8_t stage[kOsWarps][kStageBytes];
   const int lane = static_cast<int>(lane_id()), warp = static_cast<int>(threadIdx.x >> 5);
   const int p = P.p, j = P.rank;
@@ -123,12 +252,12 @@ __device__ __forceinline__ void oneshot_body(const FusedParams& P, const uint32_
   }
   // raw slot t of `rank`: value i as the pair (bits, epoch) -> 8 bytes per value
   auto raw_slot = [&](int rank, int t) {
-    return reinterpret_cast<uint4*>(P.win[rank] + P.os_off + static_cast<uint64_t>(t) * P.os_raw_bytes);
+    return reinterpret_cast<uint4*>(P.win[rank] + P.os_ll_off + static_cast<uint64_t>(t) * P.os_ll_raw_bytes);
   };
   // gather slot of owner `src` at `rank`: payload word w as the pair (word,
   // epoch), one 8-byte store each (a group's words start at any word index)
   auto ag_slot = [&](int rank, int src) {
-    return reinterpret_cast<uint2*>(P.win[rank] + P.os_ag_off + static_cast<uint64_t>(src) * P.os_ag_bytes);
+    return reinterpret_cast<uint2*>(P.win[rank] + P.os_ll_ag_off + static_cast<uint64_t>(src) * P.os_ll_ag_bytes);
   };
 
   // ---- A: raw scatter of this CTA's value range of every peer's chunk
@@ -225,6 +354,14 @@ __device__ __forceinline__ void oneshot_body(const FusedParams& P, const uint32_
   if constexpr (Codec::kCheckFinite) {
     if (__any_sync(kFull, bad) && lane == 0 && P.err) atomicOr(P.err, kErrNonFinite);
   }
+}
+
+template <class Codec>
+__device__ __forceinline__ void oneshot_body(const FusedParams& P, const uint32_t cta, const uint32_t G) {
+  if (P.os_ll)
+    oneshot_ll_body<Codec>(P, cta, G);
+  else
+    oneshot_flags_body<Codec>(P, cta, G);
 }
 
 template <class Codec>

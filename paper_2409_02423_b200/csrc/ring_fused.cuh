@@ -91,6 +91,9 @@ struct FusedParams {
   uint64_t trace_cap;
   uint64_t os_off, os_ag_off, os_flag_off;  // one-shot region: raw slots, gather slots, flags
   uint64_t os_raw_bytes, os_ag_bytes;       // one-shot slot strides
+  int os_ll;                                // one-shot transport: 1 pairs (LL), 0 flags
+  uint64_t os_ll_off, os_ll_ag_off;         // pair-mode regions: raw pairs, gather pairs
+  uint64_t os_ll_raw_bytes, os_ll_ag_bytes;
   int ag_ring;         // allgather as a forwarding ring (1) or direct owner pushes (0)
   uint32_t first_segs;  // segments in the first step of every phase
   uint32_t step_segs;  // segments per published step (one release + flag per destination)

@@ -8,7 +8,8 @@ GPU over NVLink.  Bar: bit-exact against the oracle restatement of
 proj/src/collectives.cpp:27-111 (ring), :202-248 (allreduce), :130-152 (p2p)
 and the broadcast definition of SURVEY.md §8 a10.
 
-Paths are steered per call with HCCX_ONESHOT_BYTES (0: ring everywhere) and
+Paths are steered per call with HCCX_ONESHOT_BYTES (0: ring everywhere),
+HCCX_LL_BYTES (one-shot transport: pairs below, flags above) and
 HCCX_AG_RING_BYTES (0: forwarding-ring gather; huge: direct owner pushes).
 """
 import os
@@ -26,10 +27,10 @@ CODECS = [("identity", 0), ("fixed-rate", 3), ("fixed-rate", 4), ("fixed-rate", 
 
 @pytest.fixture
 def env():
-    saved = {k: os.environ.get(k) for k in ("HCCX_ONESHOT_BYTES", "HCCX_AG_RING_BYTES")}
+    saved = {k: os.environ.get(k) for k in ("HCCX_ONESHOT_BYTES", "HCCX_AG_RING_BYTES", "HCCX_LL_BYTES")}
 
-    def set_(oneshot=None, ag_ring=None):
-        for k, v in (("HCCX_ONESHOT_BYTES", oneshot), ("HCCX_AG_RING_BYTES", ag_ring)):
+    def set_(oneshot=None, ag_ring=None, ll=None):
+        for k, v in (("HCCX_ONESHOT_BYTES", oneshot), ("HCCX_AG_RING_BYTES", ag_ring), ("HCCX_LL_BYTES", ll)):
             if v is None:
                 os.environ.pop(k, None)
             else:
@@ -47,7 +48,8 @@ def _inputs(seed, p, n, mode="uniform"):
     return np.stack([O.fill(seed + 31 * j, mode, n, 1e-3 if mode == "normal" else -1.0, 1.0) for j in range(p)])
 
 
-MODES = {"ring-direct": (0, 1 << 62), "ring-fwd": (0, 0), "oneshot": (1 << 40, None)}
+MODES = {"ring-direct": (0, 1 << 62), "ring-fwd": (0, 0), "oneshot-ll": (1 << 40, None, 1 << 40),
+         "oneshot-flags": (1 << 40, None, 0)}
 
 
 @pytest.mark.parametrize("p", [2, 4, 8])
@@ -219,7 +221,7 @@ def test_single_process_multi_gpu(cuda, env, layout):
     devices = list(range(g)) if layout == "one-per-gpu" else [j % 2 for j in range(4)]
     p = len(devices)
     m = U.MComm(p, 1 << 21, devices)
-    for mode in ("ring-fwd", "ring-direct", "oneshot"):
+    for mode in ("ring-fwd", "ring-direct", "oneshot-ll", "oneshot-flags"):
         env(*MODES[mode])
         for n_per, kind, rate in ((1000, "fixed-rate", 8), (6144 * 5 + 64, "fixed-rate", 4),
                                   ((1 << 19) + 256, "identity", 0)):
