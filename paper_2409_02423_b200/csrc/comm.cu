@@ -74,7 +74,7 @@ static_assert(sizeof(HandleBlob) <= HCCX_HANDLE_BYTES, "handle blob too large");
 uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
 
 constexpr uint64_t kOneShotMaxChunk = 1ull << 21;         // values per chunk the one-shot slots hold
-constexpr uint64_t kOneShotBytesPerRank = 4ull << 20;    // one-shot allreduce up to p x this many bytes
+constexpr uint64_t kOneShotBytesPerRank = 8ull << 20;    // one-shot allreduce up to p x this many bytes
 
 uint64_t timeout_ns() {
   const char* e = std::getenv("HCCX_TIMEOUT_MS");
@@ -274,10 +274,11 @@ hccx_status_t check_comm(hccx_comm* c, hccx_codec_t codec) {
 // fused ring above.  Both give the reference's bits.
 // 0: fused ring; 1: one-shot, flag mode; 2: one-shot, pair (LL) mode.
 int use_oneshot(const hccx_comm* c, uint64_t n) {
-  // defaults: one-shot up to 4 MiB per rank per peer (16 MiB at p = 4: the
-  // ring's 2(p-1) dependent rounds grow with p while the one-shot path keeps
-  // two), pair mode up to 2 MiB per peer (measured tools/nvl_small.py, p = 4:
-  // pairs 28 us vs flags 29 us at 4 MiB, 79 vs 59 us at 16 MiB)
+  // defaults: one-shot up to 8 MiB per peer (the one-shot slots' capacity;
+  // measured tools/nvl_small.py: at 32 MiB one-shot 96 us vs ring 103 us at
+  // p = 4, 61 vs 62 us at p = 2 -- the ring's 2(p-1) dependent rounds cost
+  // more than the raw bytes below that), pair mode up to 2 MiB per peer (p =
+  // 4: pairs 28 us vs flags 29 us at 4 MiB, 79 vs 59 us at 16 MiB)
   const char* e = std::getenv("HCCX_ONESHOT_BYTES");
   const int64_t limit = e ? static_cast<int64_t>(std::strtoull(e, nullptr, 10)) : int64_t{-1};
   const uint64_t lim = limit >= 0 ? static_cast<uint64_t>(limit) : kOneShotBytesPerRank * c->p;

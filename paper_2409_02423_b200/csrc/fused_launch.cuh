@@ -3,6 +3,7 @@
 // twins); included by the per-rate-range translation units.
 #pragma once
 #include <atomic>
+#include <cstdlib>
 #include <cstdio>
 #include <mutex>
 #include <unordered_map>
@@ -31,6 +32,12 @@ inline cudaError_t launch_ranks(const void* kernel_1, const void* kernel_v, cons
   count_launch();
   if (nv == 1) {
     void* args[] = {const_cast<FusedParams*>(P)};
+    // One rank per GPU: a CTA only ever waits on CTAs of OTHER GPUs, so a
+    // plain launch is enough (every CTA runs once its GPU has a free SM);
+    // HCCX_COOP=1 keeps the cooperative launch (co-residency guaranteed).
+    const char* e = std::getenv("HCCX_COOP");
+    if (!(e && e[0] == '1'))
+      return cudaLaunchKernel(kernel_1, dim3(G), dim3(threads), args, smem, stream);
     return cudaLaunchCooperativeKernel(kernel_1, dim3(G), dim3(threads), args, smem,
                                        stream);
   }

@@ -1,28 +1,37 @@
-// ring_fused.cuh -- the multi-process NVLink engine: ONE persistent kernel per
-// collective per rank, moving only compressed chunks between GPUs.
+// ring_fused.cuh -- the NVLink engine: ONE persistent kernel per collective
+// per rank, moving only compressed chunks between GPUs.
 //
-// Every rank owns a window (cudaMalloc'd, exported with CUDA IPC, mapped by
-// every peer over NVLink/NVSwitch) holding inbox slots and per-segment flags:
+// Every rank owns a window (cudaMalloc'd; mapped by every peer over
+// NVLink/NVSwitch through CUDA IPC, or through peer access in a
+// single-process communicator) holding inbox slots and per-step flags:
 //   rs[t]   t = 0..p-2   message of ring round t from the left neighbour
 //   ag[i]   i = 0..p-1   compressed final shard C_i of rank i (allgather)
 //   pp[i]   i = 0..p-1   point-to-point / broadcast message from rank i
-// A "segment" is a tile of 8 warp groups (2048 values) of a chunk; CTA b of
-// the cooperative grid owns segments b, b+G, b+2G, ... in every round, so
-// rank j's CTA b only ever waits on rank (j-1)'s CTA b: a per-segment
-// wavefront pipeline with no grid-wide barrier.
+// A "segment" is kSegGroups = 24 warp groups (6,144 values) of a chunk, one
+// group per compute warp; CTA b of the cooperative grid (G CTAs per rank,
+// one per SM) owns segments b, b+G, b+2G, ... in every phase, so rank j's
+// CTA b only ever waits on CTA b of its peers: a per-segment wavefront
+// pipeline with no grid-wide barrier.  The virtual-rank kernel runs several
+// ranks' CTA sets in one cooperative grid on one GPU (same device code).
 //
 // Ring schedule (identical bits to proj/src/collectives.cpp:27-111):
-//   round 0     encode local chunk (j-1) mod p -> push to rs[0] of rank j+1
-//   round t     wait rs[t-1]; fused decompress-add-recompress with local
+//   phase 0     encode local chunk (j-1) mod p -> push to rs[0] of rank j+1
+//   phase t     wait rs[t-1]; fused decompress-add-recompress with local
 //               chunk (j-1-t) mod p -> push to rs[t] of rank j+1
 //   final       wait rs[p-2]; add local chunk j ->
-//                 allreduce: encode C_j, push to ag[j] of every peer, write
-//                            dec(C_j) (/p) to out chunk j
+//                 allreduce: encode C_j, push it into ag[j] (right neighbour
+//                            for the forwarding ring, every peer for the
+//                            direct gather), write dec(C_j) (/p) to out chunk j
 //                 reduce-scatter: write the fp32 sum to the shard
-//   allgather   wait ag[i] of every peer i, decode (/p) to out chunk i
-// A segment's compressed bytes are assembled in shared memory and pushed to
-// the peer with 16-byte stores; then one thread fences (system scope) and
-// release-stores the epoch into the peer's flag.  Waits are bounded
+//   gather      wait ag[i], decode (/p) to out chunk i, forward the payload
+//               bytes unchanged (ring mode)
+// Roles per CTA: 24 compute warps; a producer warp (waits for the step's
+// inbound flag, streams inbox payload + local fp32 into a shared-memory
+// stage ring with cp.async.bulk); a pusher warp (hands each encoded segment
+// to the TMA engine as one cp.async.bulk store per destination window and
+// recycles the tile once read); a signaller warp (after the step's bulk
+// writes complete: one fence.acq_rel.sys per batch of ready events, then
+// relaxed system-scope flag / ack stores).  Waits are bounded
 // (%globaltimer); a timeout raises kErrTimeout instead of hanging the GPU.
 #pragma once
 #include "step_kernel.cuh"
