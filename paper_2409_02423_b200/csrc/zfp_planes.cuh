@@ -267,11 +267,6 @@ __device__ __forceinline__ void lut_init() {
 }
 #endif
 
-// Table reads: explicit shared-memory loads on the device (the table's
-// shared address is a link-time constant), plain loads on the host.
-HCCX_HD uint32_t lut_enc(uint32_t i);
-HCCX_HD uint32_t lut_dec(uint32_t i);
-
 HCCX_HD Lut& lut() {
 #if defined(__CUDA_ARCH__)
   return lut_dev();
@@ -282,28 +277,6 @@ HCCX_HD Lut& lut() {
     return x;
   }();
   return t;
-#endif
-}
-
-HCCX_HD uint32_t lut_enc(uint32_t i) {
-#if defined(__CUDA_ARCH__)
-  uint16_t v;
-  const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(&lut_dev().enc[0])) + 2 * i;
-  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a));
-  return v;
-#else
-  return lut().enc[i];
-#endif
-}
-
-HCCX_HD uint32_t lut_dec(uint32_t i) {
-#if defined(__CUDA_ARCH__)
-  uint16_t v;
-  const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(&lut_dev().dec[0])) + 2 * i;
-  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a));
-  return v;
-#else
-  return lut().dec[i];
 #endif
 }
 
@@ -420,7 +393,7 @@ struct PlaneEnc {
     const uint32_t x = plane_bits(u, k);
     uint32_t code = x, nn = 4, len = 4;  // all significant: verbatim plane
     if (n < 4) {
-      const uint32_t e = lut_enc(n * 16 + x);
+      const uint32_t e = lut().enc[n * 16 + x];
       code = e & 0x7fu;
       len = (e >> 8) & 7u;
       nn = e >> 12;
@@ -471,7 +444,7 @@ struct PlaneDec {
       used = budget < 4 ? budget : 4u;
       x = static_cast<uint32_t>(w) & ((1u << used) - 1u);
     } else if (budget >= 7) {
-      const uint32_t e = lut_dec(n * 128 + (static_cast<uint32_t>(w) & 127u));
+      const uint32_t e = lut().dec[n * 128 + (static_cast<uint32_t>(w) & 127u)];
       x = e & 15u;
       used = (e >> 4) & 15u;
       n = e >> 8;

@@ -9,6 +9,8 @@
           (tp = N, pp = N, dp = N) because one box has N <= 8 GPUs
   zero    config 5: ZeRO-1 reduce-scatter of a 2 GiB fp32 gradient buffer plus
           all-gather of the parameters, rates 16 and 8
+  mz      MZHybrid's LosslessPredictor paths with the compressed bytes on the
+          wire (TP allreduce, PP send/recv), traced wire bytes
 
 Device time per call, max over ranks.  Prints one JSON line per row on
 rank 0.  Development/evidence tool; bench.py is the driver contract.
@@ -117,6 +119,37 @@ def hybrid(rank, p):
         del x, y
 
 
+def mz(rank, p):
+    """MZHybrid's lossless paths on the wire (csrc/lossless_comm.cu): TP
+    allreduce and PP send/recv under LosslessPredictor, 16 MiB of smooth
+    (compressible) and of random activations; traced wire bytes are the
+    framed payloads the engine pushed."""
+    scheme = scheme_from_name("mz-hybrid:8")
+    n = 1 << 22
+    for name, lay in (("tp", ParallelLayout(1, 1, p)), ("pp", ParallelLayout(1, p, 1))):
+        hc = HybridComm(lay, scheme, n + p)
+        for data in ("smooth", "random"):
+            if data == "smooth":
+                t = torch.arange(n, device="cuda", dtype=torch.float32)
+                x = torch.sin(t * 1e-4 + rank) * 1e-2
+                x = (x * 4096).round() / 4096  # few mantissa bits: what the XOR predictor compresses
+            else:
+                x = torch.randn(n, device="cuda")
+            if name == "tp":
+                ms = timed(lambda: hc.tp_allreduce(x), 3, 1)
+                path = "TpAllReduce"
+            else:
+                ms = timed(lambda: hc.pp_send_recv(x, 0, 1), 3, 1)
+                path = "PpP2p"
+            ev = hc.trace[-1] if hc.trace else None
+            emit(rank, {"config": "mz-hybrid:8 lossless on the wire", "path": path, "data": data, "p": p,
+                        "values": n, "us": round(ms * 1e3, 1), "GBps": round(4 * n / (ms * 1e-3) / 1e9, 2),
+                        "trace_raw_bytes": ev.raw_bytes if ev else None,
+                        "trace_wire_bytes": ev.wire_bytes if ev else None})
+        hc.status()
+        hc.close()
+
+
 def zero(rank, p):
     n = (1 << 29) - ((1 << 29) % p)  # 2 GiB fp32
     comm = D.NvlinkComm(n)
@@ -155,6 +188,8 @@ def main():
         hybrid(rank, p)
     if "zero" in which:
         zero(rank, p)
+    if "mz" in which:
+        mz(rank, p)
     dist.destroy_process_group()
 
 
