@@ -409,11 +409,11 @@ def bench_allreduce(args):
     from paper_2409_02423_b200.codec import CodecSpec, wire_size_bytes
     from paper_2409_02423_b200.dist import NvlinkComm
 
-    # the image exports NCCL_DEBUG=VERSION, which prints NCCL's version line
-    # on stdout: keep stdout to the one JSON line (NCCL's own log of the
-    # baseline is tools/nccl_info.py)
-    if os.environ.get("NCCL_DEBUG", "VERSION").upper() == "VERSION":
-        os.environ["NCCL_DEBUG"] = "WARN"
+    # the image exports NCCL_DEBUG=VERSION, and NCCL prints its version line
+    # on stdout at VERSION and WARN levels: keep stdout to the one JSON line
+    # (NCCL's own log of the baseline is tools/nccl_info.py)
+    if os.environ.get("NCCL_DEBUG", "").upper() in ("VERSION", "WARN"):
+        os.environ.pop("NCCL_DEBUG")
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
