@@ -103,17 +103,6 @@ cudaError_t launch_fused_codec(const FusedParams* P, int nv, cudaStream_t stream
       q[v].step_segs = static_cast<uint32_t>(s < 1 ? 1 : (s > 8 ? 8 : s));
     }
     if (q[v].first_segs == 0) q[v].first_segs = q[v].step_segs;
-    // item-schedule lag (ring_fused.cuh Sched): the longest step + 2 rounds
-    // of slack for the neighbour's publication; HCCX_LAG=0 runs the phases
-    // one after another, HCCX_LAG=n forces n (clamped to >= the longest step)
-    const uint32_t longest = q[v].first_segs > q[v].step_segs ? q[v].first_segs : q[v].step_segs;
-    const char* le = std::getenv("HCCX_LAG");
-    if (le && std::atoi(le) == 0) {
-      q[v].lag = 0;
-    } else {
-      const uint32_t want = le ? static_cast<uint32_t>(std::atoi(le)) : longest + 2;
-      q[v].lag = want < longest ? longest : want;
-    }
   }
   if (P[0].debug & 64) {
     int b = 0;

@@ -109,7 +109,6 @@ struct FusedParams {
   uint32_t credit_all;  // bit c: slot class c (0 rs, 1 ag, 2 pp) changed geometry since its last use
   uint32_t ack_span;    // consumption-ack indices covering every CTA of any grid this communicator launches
   uint32_t max_grid;    // CTAs per rank cap shared by all ranks (0: the device's co-resident capacity)
-  uint32_t lag;         // item-schedule lag in rounds (Sched): 0 = phases one after another
   int debug;  // development knobs (HCCX_DEBUG): 16 = warp-store pushes, 32 = synchronous tile release, 64 = log launches,
             // 512 = lazy step publication, 256 = one system fence per signalled event
 };
@@ -277,34 +276,16 @@ struct TileGeom {
   static constexpr int kTiles = kFit > kFMaxTiles ? kFMaxTiles : (kFit < 2 ? 2 : kFit);
 };
 
-// Input rings: fp32 segments (local values, 24 KiB each) and payload
-// segments (inbox bytes, kSegGroups * GB each) in separate rings, so a
-// phase that reads only payload (decode) or only values (encode) keeps its
-// full depth when phases of different kinds are interleaved.
-template <class Codec>
-struct InGeom {
-  static constexpr uint32_t kValBytes = kSegVals * 4u;
-  static constexpr uint32_t kPayBytes = (kSegGroups * Codec::kGroupBytes + 127u) / 128u * 128u;
-  static constexpr int kVS = kPayBytes <= 8192u ? 4 : 3;
-  static constexpr int kFitP = static_cast<int>((kFArena - kVS * kValBytes) / kPayBytes);
-  static constexpr int kPS = kFitP > kFMaxStages ? kFMaxStages : kFitP;
-  static_assert(kPS >= 1, "payload ring needs a slot");
-};
-
-constexpr int kMaxPhases = 2 * kMaxRanks - 1;
-
-struct Phase;
-
 template <class Codec>
 struct FusedSmem2 {
-  uint8_t arena[kFArena];  // vals ring [kVS x kValBytes] then payload ring [kPS x kPayBytes]
+  uint8_t arena[kFArena];
   uint8_t tile[TileGeom<Codec>::kTiles][TileGeom<Codec>::kBytes];
   uint8_t gen[kFGenBytes];
-  uint64_t vfull[4], vempty[4];
-  uint64_t pfull[kFMaxStages], pempty[kFMaxStages];
+  uint64_t full[kFMaxStages];
+  uint64_t empty[kFMaxStages];
   uint64_t tfull[kFMaxTiles];
   uint64_t tempty[kFMaxTiles];
-  uint32_t vdirect[4], pdirect[kFMaxStages];
+  uint32_t direct[kFMaxStages];
   uint32_t prog[kFCompute + 3];  // debug: per-warp progress word (phase << 20 | segment << 4 | state)
   uint32_t sig_events;           // pusher -> signaller: events completed (release/acquire, CTA scope)
 };
@@ -327,6 +308,24 @@ struct Phase {
   int ack2_rank, ack2_cls, ack2_slot;  // second ack (ag slots: owner and left neighbour)
   uint32_t ack_ep;
 };
+
+// Per-phase input stage geometry: A = the phase's primary input of one
+// segment (fp32 for Enc, payload otherwise), B = local fp32 for the adds.
+struct StageGeom {
+  uint32_t a, b, stride;
+  int n;
+};
+
+template <class Codec>
+__device__ __forceinline__ StageGeom stage_geom(int kind) {
+  StageGeom g;
+  g.a = kind == kPhEnc ? kSegVals * 4u : (kSegGroups * Codec::kGroupBytes + 127u) / 128u * 128u;
+  g.b = (kind == kPhDar || kind == kPhFinAr || kind == kPhFinRs) ? kSegVals * 4u : 0u;
+  g.stride = g.a + g.b;
+  const uint32_t fit = kFArena / g.stride;
+  g.n = static_cast<int>(fit < kFMaxStages ? fit : kFMaxStages);
+  return g;
+}
 
 __device__ __forceinline__ int nphases(const FusedParams& P) {
   switch (P.op) {
@@ -563,43 +562,6 @@ __device__ __forceinline__ void compute_group(const FusedParams& P, const Phase&
 
 static_assert(kFusedWarps == 8 || kFusedWarps == 12 || kFusedWarps == 24, "CTAs per SM = 24 / compute warps");
 
-// Item schedule: every role walks the same sequence of (phase, segment)
-// items.  Round r holds item (ph, r - ph*L) for every phase with
-// 0 <= r - ph*L < myseg, in phase order: with the lag L = myseg the phases
-// run one after another; with L a few steps the CTA pipelines across phases
-// (encode pushes of one phase overlap the decodes of a later one).  Item
-// (ph, k) needs the neighbour's step of phase ph-1 that contains k, which the
-// neighbour finished L rounds earlier as long as L >= the longest step: no
-// rank ever waits on an item that is later in any schedule.
-struct Sched {
-  uint32_t myseg, L, nrounds, r;
-  int nph, ph;
-  __device__ __forceinline__ void init(uint32_t myseg_, uint32_t lag, int nph_) {
-    myseg = myseg_;
-    nph = nph_;
-    L = (lag == 0 || lag > myseg_) ? (myseg_ > 0 ? myseg_ : 1u) : lag;
-    nrounds = myseg_ == 0 ? 0u : myseg_ + static_cast<uint32_t>(nph_ - 1) * L;
-    r = 0;
-    ph = -1;
-  }
-  __device__ __forceinline__ bool next(int& ph_out, uint32_t& k_out) {
-    while (r < nrounds) {
-      ++ph;
-      if (ph >= nph || static_cast<uint32_t>(ph) * L > r) {
-        ph = -1;
-        ++r;
-        continue;
-      }
-      const uint32_t k = r - static_cast<uint32_t>(ph) * L;
-      if (k >= myseg) continue;
-      ph_out = ph;
-      k_out = k;
-      return true;
-    }
-    return false;
-  }
-};
-
 // The kernel body for one rank's CTA `cta` of `G`: the real kernel runs one
 // rank per launch (cta = blockIdx.x); the virtual-rank kernel below splits
 // one cooperative grid into several ranks on the same device (single-process
@@ -608,8 +570,6 @@ template <class Codec>
 __device__ __forceinline__ void ring_fused_body(const FusedParams& P, const uint32_t cta, const uint32_t G) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   FusedSmem2<Codec>& S = *reinterpret_cast<FusedSmem2<Codec>*>(smem_raw);
-  __shared__ Phase phs[kMaxPhases];
-  using IG = InGeom<Codec>;
   constexpr int kT = TileGeom<Codec>::kTiles;
   // Compute needs tile (s mod kT) back before segment s; the pusher frees
   // tiles up to seq - kRd after segment seq-1, so kRd must stay below kT.
@@ -624,29 +584,19 @@ __device__ __forceinline__ void ring_fused_body(const FusedParams& P, const uint
   const uint32_t myseg = nseg > cta ? (nseg - cta + G - 1) / G : 0;
   const int nph = nphases(P);
   // TMA needs whole 16B-multiple segments at 16B-aligned addresses: word
-  // codecs with 32B-aligned fp32 chunks (payload segments are 24*GB bytes,
+  // codecs with 32B-aligned fp32 chunks (payload segments are 8*GB bytes,
   // a multiple of 16, at 256B-aligned slot offsets).
   const bool tma_ok = Codec::kFastPath && P.vec_ok;
   auto seg_of = [&](uint32_t k) { return cta + k * G; };
   auto seg_full = [&](uint32_t sg) { return (static_cast<uint64_t>(sg) + 1) * kSegVals <= c; };
-  // Steps: a first step of P.first_segs segments, then P.step_segs each.
-  const uint32_t first = P.first_segs, step = P.step_segs;
-  auto step_start = [&](uint32_t k) { return k < first ? 0u : first + (k - first) / step * step; };
-  auto step_last = [&](uint32_t k) {  // is k the last segment of its step?
-    const uint32_t k0 = step_start(k);
-    return k + 1 == min(k0 == 0 ? first : k0 + step, myseg);
-  };
-  uint8_t* const vring = S.arena;
-  uint8_t* const pring = S.arena + IG::kVS * IG::kValBytes;
+  // Step boundaries within a phase: a short first step (P.first_segs) so the
+  // neighbour's next phase can start early, then P.step_segs per step.
+  auto step_end = [&](uint32_t k0) { return min(k0 == 0 ? P.first_segs : k0 + P.step_segs, myseg); };
 
   if (threadIdx.x == 0) {
-    for (int st = 0; st < IG::kVS; ++st) {
-      mbar_init(&S.vfull[st], 1);
-      mbar_init(&S.vempty[st], kFCompute);
-    }
-    for (int st = 0; st < IG::kPS; ++st) {
-      mbar_init(&S.pfull[st], 1);
-      mbar_init(&S.pempty[st], kFCompute);
+    for (int st = 0; st < kFMaxStages; ++st) {
+      mbar_init(&S.full[st], 1);
+      mbar_init(&S.empty[st], kFCompute);
     }
     for (int tt = 0; tt < kT; ++tt) {
       mbar_init(&S.tfull[tt], kFCompute);
@@ -655,7 +605,6 @@ __device__ __forceinline__ void ring_fused_body(const FusedParams& P, const uint
     S.sig_events = 0;
     fence_mbar_init();
   }
-  for (int ph = threadIdx.x; ph < nph; ph += blockDim.x) phs[ph] = phase_of(P, ph);
   Codec::kernel_init();
   __syncthreads();
   if (P.trace && threadIdx.x == 0 && 16384 + cta < P.trace_cap) {
@@ -664,65 +613,65 @@ __device__ __forceinline__ void ring_fused_body(const FusedParams& P, const uint
     P.trace[8192 + 2 * cta] = globaltimer_ns();
     P.trace[16384 + cta] = smid;
   }
-  Sched sched;
-  sched.init(myseg, P.lag, nph);
-  int ph;
-  uint32_t k;
 
   if (warp == kFCompute) {
     // ------------------------------------------------------------ producer
     if (lane == 0) {
       uint64_t c_empty = 0, c_flag = 0, c_total = prof_clock();
-      uint32_t vs = 0, ps = 0, vpar = 0, ppar = 0;  // ring positions and fill parities
-      while (sched.next(ph, k)) {
-        const Phase& f = phs[ph];
-        const uint32_t sg = seg_of(k);
-        if (f.wait_cls >= 0 && k == step_start(k)) {  // the step's inbound data
-          const uint64_t t0 = prof_clock();
-          spin_ge(P, flag_ptr(P, j, f.wait_cls, f.wait_slot, sg), f.wait_ep, 0x700u | (ph << 4) | f.wait_cls);
-          asm volatile("fence.proxy.async.global;" ::: "memory");
-          c_flag += prof_clock() - t0;
-          trace_ev(P, cta, 1, ph, k);
-        }
-        // L2 prefetch kFPrefetch segments ahead in the same step
-        if (tma_ok && k + kFPrefetch < myseg && step_start(k + kFPrefetch) == step_start(k)) {
-          const uint32_t sp = seg_of(k + kFPrefetch);
-          if (seg_full(sp)) {
-            if (f.kind != kPhEnc)
-              bulk_prefetch_l2(f.pay + static_cast<uint64_t>(sp) * kSegGroups * GB, static_cast<uint32_t>(kSegGroups * GB));
-            if (f.kind != kPhDec) bulk_prefetch_l2(f.vals + static_cast<uint64_t>(sp) * kSegVals, kSegVals * 4u);
+      uint32_t pu = 0;  // per-barrier fill parity
+      for (int ph = 0; ph < nph; ++ph) {
+        const Phase f = phase_of(P, ph);
+        const StageGeom sg_ = stage_geom<Codec>(f.kind);
+        // the arena is re-carved for this phase: every earlier fill must be consumed
+        for (int b = 0; b < kFMaxStages; ++b) mbar_wait_to(P, &S.empty[b], ((pu >> b) & 1u) ^ 1u, 0x100u | b, S.prog);
+        int st = 0;
+        for (uint32_t k0 = 0, k1; k0 < myseg; k0 = k1) {
+          k1 = step_end(k0);
+          if (f.wait_cls >= 0) {
+            const uint64_t t0 = prof_clock();
+            spin_ge(P, flag_ptr(P, j, f.wait_cls, f.wait_slot, seg_of(k0)), f.wait_ep, 0x700u | (ph << 4) | f.wait_cls);
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+            c_flag += prof_clock() - t0;
+            trace_ev(P, cta, 1, ph, k0);
+          }
+          for (uint32_t k = k0; k < k1; ++k) {
+            const uint32_t sg = seg_of(k);
+            // L2 prefetch kFPrefetch segments ahead (same step), so the
+            // bulk load issued when the stage frees up hits L2
+            if (tma_ok && k + kFPrefetch < k1) {
+              const uint32_t sp = seg_of(k + kFPrefetch);
+              if (seg_full(sp)) {
+                if (f.kind == kPhEnc) {
+                  bulk_prefetch_l2(f.vals + static_cast<uint64_t>(sp) * kSegVals, kSegVals * 4u);
+                } else {
+                  bulk_prefetch_l2(f.pay + static_cast<uint64_t>(sp) * kSegGroups * GB,
+                                   static_cast<uint32_t>(kSegGroups * GB));
+                  if (f.kind != kPhDec) bulk_prefetch_l2(f.vals + static_cast<uint64_t>(sp) * kSegVals, kSegVals * 4u);
+                }
+              }
+            }
+            HCCX_PROG(S.prog[kFCompute] = (ph << 20) | (k << 4) | 3u);
+            const uint64_t t1 = prof_clock();
+            mbar_wait_to(P, &S.empty[st], ((pu >> st) & 1u) ^ 1u, 0x200u | st, S.prog);
+            c_empty += prof_clock() - t1;
+            pu ^= 1u << st;
+            const bool full_seg = tma_ok && seg_full(sg);
+            S.direct[st] = full_seg ? 0u : 1u;
+            uint8_t* base = S.arena + st * sg_.stride;
+            if (full_seg) {
+              const uint32_t a_bytes = f.kind == kPhEnc ? kSegVals * 4u : static_cast<uint32_t>(kSegGroups * GB);
+              mbar_arrive_expect_tx(&S.full[st], a_bytes + sg_.b);
+              if (f.kind == kPhEnc)
+                bulk_g2s(base, f.vals + static_cast<uint64_t>(sg) * kSegVals, a_bytes, &S.full[st]);
+              else
+                bulk_g2s(base, f.pay + static_cast<uint64_t>(sg) * kSegGroups * GB, a_bytes, &S.full[st]);
+              if (sg_.b) bulk_g2s(base + sg_.a, f.vals + static_cast<uint64_t>(sg) * kSegVals, sg_.b, &S.full[st]);
+            } else {
+              mbar_arrive(&S.full[st]);  // consumers read this segment from global memory
+            }
+            if (++st == sg_.n) st = 0;
           }
         }
-        HCCX_PROG(S.prog[kFCompute] = (ph << 20) | (k << 4) | 3u);
-        const bool full_seg = tma_ok && seg_full(sg);
-        const uint64_t t1 = prof_clock();
-        if (f.kind != kPhEnc) {  // payload slot
-          mbar_wait_to(P, &S.pempty[ps], ((ppar >> ps) & 1u) ^ 1u, 0x200u | ps, S.prog);
-          ppar ^= 1u << ps;
-          S.pdirect[ps] = full_seg ? 0u : 1u;
-          if (full_seg) {
-            const uint32_t nb = static_cast<uint32_t>(kSegGroups * GB);
-            mbar_arrive_expect_tx(&S.pfull[ps], nb);
-            bulk_g2s(pring + ps * IG::kPayBytes, f.pay + static_cast<uint64_t>(sg) * kSegGroups * GB, nb, &S.pfull[ps]);
-          } else {
-            mbar_arrive(&S.pfull[ps]);  // consumers read this segment from global memory
-          }
-          if (++ps == IG::kPS) ps = 0;
-        }
-        if (f.kind != kPhDec) {  // local fp32 slot
-          mbar_wait_to(P, &S.vempty[vs], ((vpar >> vs) & 1u) ^ 1u, 0x280u | vs, S.prog);
-          vpar ^= 1u << vs;
-          S.vdirect[vs] = full_seg ? 0u : 1u;
-          if (full_seg) {
-            mbar_arrive_expect_tx(&S.vfull[vs], IG::kValBytes);
-            bulk_g2s(vring + vs * IG::kValBytes, f.vals + static_cast<uint64_t>(sg) * kSegVals, IG::kValBytes,
-                     &S.vfull[vs]);
-          } else {
-            mbar_arrive(&S.vfull[vs]);
-          }
-          if (++vs == IG::kVS) vs = 0;
-        }
-        c_empty += prof_clock() - t1;
       }
       trace_acc(P, cta, 0, prof_clock() - c_total);
       trace_acc(P, cta, 1, c_empty);
@@ -739,22 +688,26 @@ __device__ __forceinline__ void ring_fused_body(const FusedParams& P, const uint
     // release store per destination after its bulk writes completed.
     // Control flow is uniform across the warp: lane 0 alone waits on and
     // arrives at mbarriers, spins on credits and writes flags; the other
-    // lanes only join the 16-byte store loops.
+    // lanes only join the 16-byte store loops.  Every lane passes exactly
+    // the same sequence of __syncwarp() calls (divergent lane-0 blocks plus
+    // __syncwarp at different sites let lanes drift a segment apart).
     int tt = 0;
     uint32_t tbit = 0;
     uint32_t seq = 0, released = 0;  // segments seen / tiles handed back (ring order)
     uint64_t c_tfull = 0, c_read = 0, c_pub = 0, c_credit = 0, c_issue = 0, c_total = prof_clock();
     uint32_t events = 0;  // signaller events issued (lane 0)
-    // Publication queue (lane 0): a finished step's event carries the
-    // bulk-group count at its end and goes to the signaller once those
-    // groups completed; acks carry no bulk dependency.  Eager by default
-    // (drained at every step end: measured faster at p = 4 than lazy,
-    // HCCX_DEBUG bit 512 = lazy).  Events stay in the signaller's order.
+    // Lazy publication (lane 0): a finished step's event is queued with the
+    // bulk-group count at its end and handed to the signaller once those
+    // groups have completed -- checked kLazy groups later (by then they are
+    // done, so the wait is free) or whenever the pusher would otherwise
+    // block (waiting for a tile or a credit): the TMA engine keeps pushing
+    // across step boundaries instead of draining at every step.  Events
+    // (step publications and phase-end acks) stay in the signaller's order.
     constexpr int kLazy = 3;
     constexpr int kPend = 8;
-    uint32_t pend_g[kPend];
+    uint32_t pend_g[kPend];  // group count at the step's end; ~0u = ack event (no bulk dependency)
     int pend_head = 0, pend_n = 0;
-    uint32_t groups = 0;  // bulk groups committed (one per pushed segment)
+    uint32_t groups = 0;     // bulk groups committed (one per pushed segment)
     auto release_upto = [&](uint32_t upto) {
       for (; released < upto; ++released) mbar_arrive(&S.tempty[released % kT]);
     };
@@ -783,10 +736,11 @@ __device__ __forceinline__ void ring_fused_body(const FusedParams& P, const uint
       pend_g[(pend_head + pend_n) % kPend] = g;
       ++pend_n;
     };
-    while (sched.next(ph, k)) {
-      const Phase& f = phs[ph];
+    for (int ph = 0; ph < nph; ++ph) {
+      const Phase f = phase_of(P, ph);
       const bool push = f.push_cls >= 0;
-      if (push && k == 0) {  // credit: previous use of the destination slot(s) consumed
+      const uint64_t tc = prof_clock();
+      if (push) {  // credit: previous use of the destination slot(s) consumed
         // Same slot geometry as the previous use (codec, chunk size, hence
         // grid and segment bytes): this CTA's segments were read by the
         // receiver CTA with our index, whose ack we wait for.  Geometry
@@ -794,7 +748,6 @@ __device__ __forceinline__ void ring_fused_body(const FusedParams& P, const uint
         // were read by arbitrary receiver CTAs, so wait for all of them --
         // receiver CTA r of a grid G' acked indices r, r+G', ..., so indices
         // [0, ack_span) cover every CTA of any grid <= ack_span.
-        const uint64_t tc = prof_clock();
         if (lane == 0) emit(true);  // never hold a publication across a wait on a peer
         __syncwarp();
         const bool all = ((P.credit_all >> f.push_cls) & 1u) != 0;
@@ -805,92 +758,103 @@ __device__ __forceinline__ void ring_fused_body(const FusedParams& P, const uint
           const uint32_t need = f.push_cls == 2 ? P.pp_epoch[d] - 1u : f.credit_ep;
           const uint32_t* fl = flag_ptr(P, j, f.credit_cls, f.push_mode == 0 ? f.push_slot : d, 0);
           if (all) {
-            for (uint32_t kk = lane; kk < P.ack_span; kk += 32) spin_ge(P, fl + kk, need, 0x900u | (ph << 4) | f.credit_cls);
+            for (uint32_t k = lane; k < P.ack_span; k += 32) spin_ge(P, fl + k, need, 0x900u | (ph << 4) | f.credit_cls);
           } else if (lane == 0) {
             spin_ge(P, fl + cta, need, 0x800u | (ph << 4) | f.credit_cls);
           }
         }
-        __syncwarp();
-        c_credit += prof_clock() - tc;
       }
-      const uint32_t sg = seg_of(k);
-      if (lane == 0) {
-        HCCX_PROG(S.prog[kFCompute + 1] = (ph << 20) | (k << 4) | 2u);
-        const uint64_t t0 = prof_clock();
-        // about to wait for compute: publish what has completed first
-        if (pend_n && !mbar_test(&S.tfull[tt], tbit)) emit(true);
-        mbar_wait_to(P, &S.tfull[tt], tbit, 0x300u | tt, S.prog);
-        c_tfull += prof_clock() - t0;
-      }
-      __syncwarp();  // the tile is complete for every lane
-      bool bulk_issued = false;
-      if (push) {
-        const uint64_t soff = static_cast<uint64_t>(sg) * kSegGroups * GB;
-        const uint64_t rem = wire - soff;
-        const uint32_t nb = static_cast<uint32_t>(rem < kSegGroups * GB ? rem : kSegGroups * GB);
-        // TMA bulk push (one instruction per destination); HCCX_DEBUG
-        // bit 16 selects the warp's 16-byte stores instead.
-        if ((nb & 15u) == 0 && !(P.debug & 16)) {
+      __syncwarp();
+      c_credit += prof_clock() - tc;
+      for (uint32_t k0 = 0, k1; k0 < myseg; k0 = k1) {
+        k1 = step_end(k0);
+        for (uint32_t k = k0; k < k1; ++k) {
+          const uint32_t sg = seg_of(k);
           if (lane == 0) {
-            const uint64_t ti = prof_clock();
-            // the tile was written through the generic proxy; the bulk
-            // copy reads it through the async proxy
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            for (int q = 1; q < p; ++q) {
-              const int d = (j + q) % p;
-              if (f.push_mode == 0 && q != 1) break;
-              if (f.push_mode == 2 && d != P.dst) continue;
-              bulk_s2g(slot_ptr(P, d, f.push_cls, f.push_slot) + soff, S.tile[tt], nb);
+            HCCX_PROG(S.prog[kFCompute + 1] = (ph << 20) | (k << 4) | 2u);
+            const uint64_t t0 = prof_clock();
+            // about to wait for compute: publish what has completed first
+            if (pend_n && !mbar_test(&S.tfull[tt], tbit)) emit(true);
+            mbar_wait_to(P, &S.tfull[tt], tbit, 0x300u | tt, S.prog);
+            c_tfull += prof_clock() - t0;
+          }
+          __syncwarp();  // the tile is complete for every lane
+          bool bulk_issued = false;
+          if (push) {
+            const uint64_t soff = static_cast<uint64_t>(sg) * kSegGroups * GB;
+            const uint64_t rem = wire - soff;
+            const uint32_t nb = static_cast<uint32_t>(rem < kSegGroups * GB ? rem : kSegGroups * GB);
+            // TMA bulk push (one instruction per destination); HCCX_DEBUG
+            // bit 16 selects the warp's 16-byte stores instead.
+            if ((nb & 15u) == 0 && !(P.debug & 16)) {
+              if (lane == 0) {
+                const uint64_t ti = prof_clock();
+                // the tile was written through the generic proxy; the bulk
+                // copy reads it through the async proxy
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                for (int q = 1; q < p; ++q) {
+                  const int d = (j + q) % p;
+                  if (f.push_mode == 0 && q != 1) break;
+                  if (f.push_mode == 2 && d != P.dst) continue;
+                  bulk_s2g(slot_ptr(P, d, f.push_cls, f.push_slot) + soff, S.tile[tt], nb);
+                }
+                bulk_commit();
+                ++groups;
+                c_issue += prof_clock() - ti;
+                trace_ev(P, cta, 3, ph, k);
+              }
+              bulk_issued = true;
+            } else {
+              for (int q = 1; q < p; ++q) {
+                const int d = (j + q) % p;
+                if (f.push_mode == 0 && q != 1) break;
+                if (f.push_mode == 2 && d != P.dst) continue;
+                uint8_t* dst = slot_ptr(P, d, f.push_cls, f.push_slot) + soff;
+                const uint32_t n16 = (nb & 15u) == 0 && (reinterpret_cast<uintptr_t>(dst) & 15u) == 0 ? nb >> 4 : 0;
+                for (uint32_t i = lane; i < n16; i += 32)
+                  reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(S.tile[tt])[i];
+                for (uint32_t b = (n16 << 4) + lane; b < nb; b += 32) dst[b] = S.tile[tt][b];
+              }
             }
-            bulk_commit();
-            ++groups;
-            c_issue += prof_clock() - ti;
-            trace_ev(P, cta, 3, ph, k);
           }
-          bulk_issued = true;
-        } else {
-          for (int q = 1; q < p; ++q) {
-            const int d = (j + q) % p;
-            if (f.push_mode == 0 && q != 1) break;
-            if (f.push_mode == 2 && d != P.dst) continue;
-            uint8_t* dst = slot_ptr(P, d, f.push_cls, f.push_slot) + soff;
-            const uint32_t n16 = (nb & 15u) == 0 && (reinterpret_cast<uintptr_t>(dst) & 15u) == 0 ? nb >> 4 : 0;
-            for (uint32_t i = lane; i < n16; i += 32)
-              reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(S.tile[tt])[i];
-            for (uint32_t b = (n16 << 4) + lane; b < nb; b += 32) dst[b] = S.tile[tt][b];
+          ++seq;
+          __syncwarp();  // every lane's reads of the tile are done
+          if (lane == 0) {
+            const uint64_t t1 = prof_clock();
+            if (bulk_issued && !(P.debug & 32)) {
+              bulk_wait_read<kRd>();  // hand tiles back once the TMA engine has read them
+              release_upto(seq > static_cast<uint32_t>(kRd) ? seq - kRd : 0);
+            } else {
+              if (bulk_issued) bulk_wait_read<0>();
+              release_upto(seq);
+            }
+            if (pend_n) emit(false);
+            c_read += prof_clock() - t1;
+          }
+          if (++tt == kT) {
+            tt = 0;
+            tbit ^= 1u;
           }
         }
-      }
-      ++seq;
-      __syncwarp();  // every lane's reads of the tile are done
-      if (lane == 0) {
-        const uint64_t t1 = prof_clock();
-        if (bulk_issued && !(P.debug & 32)) {
-          bulk_wait_read<kRd>();  // hand tiles back once the TMA engine has read them
-          release_upto(seq > static_cast<uint32_t>(kRd) ? seq - kRd : 0);
-        } else {
-          if (bulk_issued) bulk_wait_read<0>();
-          release_upto(seq);
+        if (push) {  // the step is issued: its publication follows once its groups complete
+          const uint64_t t2 = prof_clock();
+          if (lane == 0) {
+            // (warp-copied segments commit no group: their lanes' stores
+            // are ordered before lane 0's event release by __syncwarp)
+            // Eager by default: measured at p = 4 (tools/nvl_ab.py), lazy
+            // publication cost 6% -- consumers saw the flags later than the
+            // drain at the step end costs the pusher.  HCCX_DEBUG bit 512:
+            // lazy (development).
+            enqueue(groups);
+            if (!(P.debug & 512)) emit(true);
+          }
+          c_pub += prof_clock() - t2;
+          __syncwarp();
         }
-        if (pend_n) emit(false);
-        c_read += prof_clock() - t1;
       }
-      if (++tt == kT) {
-        tt = 0;
-        tbit ^= 1u;
-      }
-      if (lane == 0) {
-        const uint64_t t2 = prof_clock();
-        // (warp-copied segments commit no group: their lanes' stores are
-        // ordered before lane 0's event release by the __syncwarp above)
-        if (push && step_last(k)) {
-          enqueue(groups);
-          if (!(P.debug & 512)) emit(true);
-        }
-        // the phase's last segment computed -> its inbox inputs are consumed
-        if (k + 1 == myseg && f.ack_rank >= 0) enqueue(~0u);
-        c_pub += prof_clock() - t2;
-      }
+      // every segment of the phase has been computed (tfull) -> its inbox
+      // inputs are consumed: the signaller acknowledges them
+      if (f.ack_rank >= 0 && lane == 0) enqueue(~0u);
       __syncwarp();
     }
     if (lane == 0) {
@@ -911,14 +875,14 @@ __device__ __forceinline__ void ring_fused_body(const FusedParams& P, const uint
   if (warp == kFCompute + 2) {
     // ----------------------------------------------------------- signaller
     // Publishes the pusher's completed steps (one flag store per
-    // destination) and the phase-end consumption acks, walking the same
-    // item sequence; event e is ready once S.sig_events >= e (the pusher's
-    // release.cta after the step's bulk writes completed).  A system-scope
-    // fence costs microseconds while NVLink writes are in flight, so events
-    // are published in batches: one acquire of the ready count, one
-    // fence.acq_rel.sys by every lane, then relaxed system-scope stores for
-    // every event up to that count -- causality order carries the data
-    // writes to the remote acquirer.
+    // destination) and the phase-end consumption acks.  Walks the same
+    // (phase, step) event sequence as the pusher; event e is ready once
+    // S.sig_events >= e (the pusher's release.cta after the step's bulk
+    // writes completed).  A system-scope fence costs microseconds while
+    // NVLink writes are in flight, so events are published in batches: one
+    // acquire of the ready count, one fence.acq_rel.sys by every lane, then
+    // relaxed system-scope stores for every event up to that count --
+    // causality order carries the data writes to the remote acquirer.
     uint32_t events = 0, ready = 0;
     uint64_t c_sig = 0, c_ack = 0;
     auto need = [&](uint32_t ev) {  // make event ev publishable (fenced)
@@ -944,23 +908,24 @@ __device__ __forceinline__ void ring_fused_body(const FusedParams& P, const uint
       ready = __shfl_sync(kFull, ready, 0);
       fence_acq_rel_sys();
     };
-    while (sched.next(ph, k)) {
-      const Phase& f = phs[ph];
-      if (f.push_cls >= 0 && step_last(k)) {
-        const uint64_t ts = prof_clock();
-        need(++events);
-        const uint32_t k0 = step_start(k);
-        if (lane < p - 1) {
-          const int d = (j + 1 + lane) % p;
-          const bool tgt =
-              f.push_mode == 1 || (f.push_mode == 0 && lane == 0) || (f.push_mode == 2 && d == P.dst);
-          if (tgt) st_relaxed_sys(flag_ptr(P, d, f.push_cls, f.push_slot, seg_of(k0)), push_epoch(P, f.push_cls, d));
+    for (int ph = 0; ph < nph; ++ph) {
+      const Phase f = phase_of(P, ph);
+      if (f.push_cls >= 0) {
+        for (uint32_t k0 = 0; k0 < myseg; k0 = step_end(k0)) {
+          const uint64_t ts = prof_clock();
+          need(++events);
+          if (lane < p - 1) {
+            const int d = (j + 1 + lane) % p;
+            const bool tgt =
+                f.push_mode == 1 || (f.push_mode == 0 && lane == 0) || (f.push_mode == 2 && d == P.dst);
+            if (tgt) st_relaxed_sys(flag_ptr(P, d, f.push_cls, f.push_slot, seg_of(k0)), push_epoch(P, f.push_cls, d));
+          }
+          __syncwarp();
+          c_sig += prof_clock() - ts;
+          if (lane == 0) trace_ev(P, cta, 5, ph, k0);
         }
-        __syncwarp();
-        c_sig += prof_clock() - ts;
-        if (lane == 0) trace_ev(P, cta, 5, ph, k0);
       }
-      if (k + 1 == myseg && f.ack_rank >= 0) {
+      if (f.ack_rank >= 0) {
         const uint64_t ta = prof_clock();
         need(++events);
         for (uint32_t kk = cta + lane * G; kk < kAckIdx; kk += G * 32) {
@@ -980,50 +945,46 @@ __device__ __forceinline__ void ring_fused_body(const FusedParams& P, const uint
 
   // -------------------------------------------------------------- compute
   uint32_t bad = 0;
-  uint32_t vs = 0, ps = 0, vpar = 0, ppar = 0;  // ring positions and consume parities
+  uint32_t cu = 0;  // per-barrier consume parity
   int tt = 0;
   uint32_t tbit = 0;
   uint8_t* gen = S.gen + warp * kStageBytes;
   uint64_t c_full = 0, c_tile = 0, c_comp = 0, c_total = prof_clock();
-  while (sched.next(ph, k)) {
-    const Phase& f = phs[ph];
-    const uint32_t sg = seg_of(k);
-    const bool use_p = f.kind != kPhEnc, use_v = f.kind != kPhDec;
-    if (lane == 0) HCCX_PROG(S.prog[warp] = (ph << 20) | (k << 4) | 1u);
-    const uint64_t t0 = prof_clock();
-    if (use_p) mbar_wait_to(P, &S.pfull[ps], (ppar >> ps) & 1u, 0x400u | ps, S.prog);
-    if (use_v) mbar_wait_to(P, &S.vfull[vs], (vpar >> vs) & 1u, 0x480u | vs, S.prog);
-    if (lane == 0) HCCX_PROG(S.prog[warp] = (ph << 20) | (k << 4) | 2u);
-    const uint64_t t1 = prof_clock();
-    mbar_wait_to(P, &S.tempty[tt], tbit ^ 1u, 0x500u | tt, S.prog);
-    const uint64_t t2 = prof_clock();
-    c_full += t1 - t0;
-    c_tile += t2 - t1;
-    const bool direct = (use_p ? S.pdirect[ps] : S.vdirect[vs]) != 0;
-    const uint64_t g = static_cast<uint64_t>(sg) * kSegGroups + warp;
-    const uint8_t* vbase = vring + vs * IG::kValBytes + warp * 1024u;
-    const uint8_t* sa = f.kind == kPhEnc ? vbase : pring + ps * IG::kPayBytes + warp * static_cast<uint32_t>(GB);
-    if (g < ngroups) compute_group<Codec>(P, f, g, direct, sa, vbase, S.tile[tt] + warp * GB, gen, lane, bad);
-    __syncwarp();
-    c_comp += prof_clock() - t2;
-    if (warp == 0 && lane == 0) trace_ev(P, cta, 2, ph, k);
-    if (lane == 0) {
-      HCCX_PROG(S.prog[warp] = (ph << 20) | (k << 4) | 3u);
-      if (use_p) mbar_arrive(&S.pempty[ps]);
-      if (use_v) mbar_arrive(&S.vempty[vs]);
-      mbar_arrive(&S.tfull[tt]);
-    }
-    if (use_p) {
-      ppar ^= 1u << ps;
-      if (++ps == IG::kPS) ps = 0;
-    }
-    if (use_v) {
-      vpar ^= 1u << vs;
-      if (++vs == IG::kVS) vs = 0;
-    }
-    if (++tt == kT) {
-      tt = 0;
-      tbit ^= 1u;
+  for (int ph = 0; ph < nph; ++ph) {
+    const Phase f = phase_of(P, ph);
+    const StageGeom sg_ = stage_geom<Codec>(f.kind);
+    int st = 0;
+    for (uint32_t k = 0; k < myseg; ++k) {
+      const uint32_t sg = seg_of(k);
+      if (lane == 0) HCCX_PROG(S.prog[warp] = (ph << 20) | (k << 4) | 1u);
+      const uint64_t t0 = prof_clock();
+      mbar_wait_to(P, &S.full[st], (cu >> st) & 1u, 0x400u | st, S.prog);
+      cu ^= 1u << st;
+      if (lane == 0) HCCX_PROG(S.prog[warp] = (ph << 20) | (k << 4) | 2u);
+      const uint64_t t1 = prof_clock();
+      mbar_wait_to(P, &S.tempty[tt], tbit ^ 1u, 0x500u | tt, S.prog);
+      const uint64_t t2 = prof_clock();
+      c_full += t1 - t0;
+      c_tile += t2 - t1;
+      const bool direct = S.direct[st] != 0;
+      const uint64_t g = static_cast<uint64_t>(sg) * kSegGroups + warp;
+      const uint8_t* base = S.arena + st * sg_.stride;
+      const uint8_t* sa = base + (f.kind == kPhEnc ? warp * 1024u : warp * static_cast<uint32_t>(GB));
+      const uint8_t* sb = base + sg_.a + warp * 1024u;
+      if (g < ngroups) compute_group<Codec>(P, f, g, direct, sa, sb, S.tile[tt] + warp * GB, gen, lane, bad);
+      __syncwarp();
+      c_comp += prof_clock() - t2;
+      if (warp == 0 && lane == 0) trace_ev(P, cta, 2, ph, k);
+      if (lane == 0) HCCX_PROG(S.prog[warp] = (ph << 20) | (k << 4) | 3u);
+      if (lane == 0) {
+        mbar_arrive(&S.empty[st]);
+        mbar_arrive(&S.tfull[tt]);
+      }
+      if (++st == sg_.n) st = 0;
+      if (++tt == kT) {
+        tt = 0;
+        tbit ^= 1u;
+      }
     }
   }
   if (lane == 0 && warp == 0) {

@@ -310,3 +310,44 @@ def test_lossless_then_fused_same_slots(cuda, env):
         assert st == 0
         want, _ = O.allreduce(x, kind, rate)
         assert got.tobytes() == want.tobytes(), (kind, rate, n_per)
+
+
+def test_edge_cases_virtual(cuda):
+    """Degenerate calls of the single-process communicator, as the
+    reference's wrappers treat them (collectives.cpp:154-200): empty buffers,
+    a one-member communicator (input returned untouched, not quantized),
+    ragged / indivisible lengths (BadChunkingError), bad roots and src == dst."""
+    import ctypes as C
+
+    import torch
+
+    import hccx_util as U
+    from paper_2409_02423_b200 import _lib
+
+    m = U.MComm(4, 1 << 14)
+    # n = 0: nothing happens, no error
+    z = torch.empty(0, device="cuda")
+    a, _ka = _lib.ptr_array([z.data_ptr()] * 4)
+    assert _lib.hccx_mcomm_allreduce(m.h, a, a, 0, U.codec("fixed-rate", 8), 0, None) == 0
+    assert _lib.hccx_mcomm_status(m.h, None) == 0
+    # n % p != 0 -> HCCX_ERR_BAD_CHUNKING (4)
+    x = _inputs(1, 4, 4 * 100 + 2)
+    ins = [U.dev(x[j]) for j in range(4)]
+    a, _ka = _lib.ptr_array([t.data_ptr() for t in ins])
+    assert _lib.hccx_mcomm_allreduce(m.h, a, a, 4 * 100 + 2, U.codec("fixed-rate", 8), 0, None) == 4
+    assert _lib.hccx_mcomm_reduce_scatter(m.h, a, a, 4 * 100 + 2, U.codec("fixed-rate", 8), None) == 4
+    # bad root / src == dst -> HCCX_ERR_INVALID_ARGUMENT (9); bad rate -> INVALID_SCHEME (6)
+    assert _lib.hccx_mcomm_broadcast(m.h, 4, ins[0].data_ptr(), a, 100, U.codec("fixed-rate", 8), None) == 9
+    assert _lib.hccx_mcomm_p2p(m.h, 1, 1, ins[0].data_ptr(), ins[1].data_ptr(), 100, U.codec("fixed-rate", 8),
+                               None) == 9
+    assert _lib.hccx_mcomm_allreduce(m.h, a, a, 400, U.codec("fixed-rate", 33), 0, None) == 6
+    # one-member communicator: the input comes back untouched (not quantized)
+    one = U.MComm(1, 4096)
+    x1 = _inputs(2, 1, 3000)
+    got, st = one.allreduce(x1, "fixed-rate", 4)
+    assert st == 0 and got.tobytes() == x1.tobytes()
+    # capacity: more values per chunk than the communicator was created for
+    big = _inputs(3, 4, 4 * (1 << 16))
+    _got, st = m.allreduce(big, "fixed-rate", 8)
+    assert st == 9
+    del C
