@@ -217,8 +217,19 @@ extern "C" hccx_status_t hccx_flag_status(uint32_t* d_err, void* stream) {
 
 namespace {
 
-constexpr uint64_t kSlice = uint64_t{1} << 22;  // 4 Mi values = 16 MiB fp32
-constexpr int kLanes = 3;
+// Slices of the host pipeline: ~1/16 of the buffer (so filling and draining
+// the copy pipeline costs ~1/16 of the transfer), between 256 Ki and 4 Mi
+// values, a whole number of 256-value groups; kLanes streams overlap one
+// slice's H2D with another's D2H.
+constexpr uint64_t kSlice = uint64_t{1} << 22;  // largest slice: 4 Mi values = 16 MiB fp32
+constexpr uint64_t kMinSlice = uint64_t{1} << 18;
+constexpr int kLanes = 4;
+
+uint64_t slice_for(uint64_t n) {
+  uint64_t s = (n / 16 + 255) / 256 * 256;
+  s = s < kMinSlice ? kMinSlice : (s > kSlice ? kSlice : s);
+  return s;
+}
 
 struct HostPipe {
   int device = -1;
@@ -269,14 +280,15 @@ hccx_status_t host_codec(bool compress, hccx_codec_t codec, const void* h_in, ui
   DeviceGuard guard(device);
   std::lock_guard<std::mutex> lock(g_run_mu);
   HostPipe* p = pipe_for(device);
-  const uint64_t slice = n < kSlice ? n : kSlice;
+  const uint64_t step = slice_for(n);
+  const uint64_t slice = n < step ? n : step;
   const uint64_t slice_bytes = payload_bytes(c, slice);
   hccx_status_t st = ensure_pipe(p, slice, slice_bytes);
   if (st != HCCX_OK) return st;
   const uint64_t gb = group_bytes(c);
   int lane = 0;
-  for (uint64_t off = 0; off < n; off += kSlice, lane = (lane + 1) % kLanes) {
-    const uint64_t m = (n - off) < kSlice ? (n - off) : kSlice;
+  for (uint64_t off = 0; off < n; off += step, lane = (lane + 1) % kLanes) {
+    const uint64_t m = (n - off) < step ? (n - off) : step;
     const uint64_t boff = (off / 256) * gb;  // payload offset of this slice
     const uint64_t mb = payload_bytes(c, m);
     cudaStream_t s = p->streams[lane];

@@ -58,7 +58,10 @@ cudaError_t launch_oneshot_codec(const FusedParams* P, int nv, cudaStream_t stre
   // this launch is still queued; ~8 groups per CTA, at most one CTA per SM
   uint64_t cap = static_cast<uint64_t>(fused_capacity(kv, kOsWarps * 32, 0));
   cap = cap < 148 ? cap : 148;
-  uint64_t grid = (groups + 7) / 8;
+  // groups per CTA (HCCX_OS_GPC, development knob; default below)
+  const char* ge = std::getenv("HCCX_OS_GPC");
+  const uint64_t gpc = ge && std::atoi(ge) > 0 ? static_cast<uint64_t>(std::atoi(ge)) : 8u;
+  uint64_t grid = (groups + gpc - 1) / gpc;
   const uint64_t lim = rank_grid_cap(P[0], cap, nv);
   grid = grid < lim ? grid : lim;
   return launch_ranks(reinterpret_cast<const void*>(&oneshot_allreduce_kernel<Codec>), kv, P, nv,
@@ -94,12 +97,12 @@ cudaError_t launch_fused_codec(const FusedParams* P, int nv, cudaStream_t stream
     q[v] = P[v];
     q[v].ack_span = static_cast<uint32_t>(gcap);
     if (q[v].step_segs == 0) {
-      // auto: ~8 published steps per phase per CTA, 1..8 segments each.
+      // auto: ~16 published steps per phase per CTA, 1..8 segments each.
       // Measured (tools/nvl_ab.py, 256 MiB r8): p = 4 1.07-1.10x faster
       // with 1-2 segment steps than with 3 steps per phase (consumers start
       // earlier; the signaller batches its system fences); p = 2 flat.
       const uint64_t myseg = (nseg + grid - 1) / grid;
-      const uint64_t s = (myseg + 7) / 8;
+      const uint64_t s = (myseg + 15) / 16;
       q[v].step_segs = static_cast<uint32_t>(s < 1 ? 1 : (s > 8 ? 8 : s));
     }
     if (q[v].first_segs == 0) q[v].first_segs = q[v].step_segs;
