@@ -74,6 +74,9 @@ def _load_ref():
     lib.ref_compress.argtypes = [i32, i32, i32, _f, u64, _u8, u64, C.POINTER(u64), C.POINTER(C.c_uint32)]
     lib.ref_decompress.argtypes = [i32, i32, i32, _u8, u64, u64, C.c_uint32, _f]
     lib.ref_wire_size.argtypes = [i32, i32, u64, C.POINTER(u64)]
+    if hasattr(lib, "ref_time_codec"):
+        lib.ref_time_codec.argtypes = [i32, i32, _f, u64, i32, C.POINTER(C.c_double)]
+        lib.ref_time_allreduce.argtypes = [i32, u64, _f, i32, i32, i32, C.POINTER(C.c_double)]
     lib.ref_container.argtypes = [i32, i32, _f, u64, _u8, u64, C.POINTER(u64)]
     lib.ref_allreduce.argtypes = [i32, u64, _f, i32, i32, i32, _f, _u64]
     lib.ref_reduce_scatter.argtypes = [i32, u64, _f, i32, i32, _f, _u64]
@@ -317,3 +320,25 @@ def ref_train(cfg: dict, dp: int, pp: int, tp: int, scheme: str, zero: int):
         raise RuntimeError(f"reference status {st}")
     return {"step_loss": loss[: done.value], "steps_completed": done.value, "final_eval_loss": np.float32(ev.value),
             "diverged": bool(div.value), "w1": w1, "w2": w2, "path_bytes": pb}
+
+
+def ref_time_codec(kind: str, rate: int, x: np.ndarray, reps: int = 1) -> float:
+    """Median seconds of hcc::compress + hcc::decompress on the reference
+    library itself (marshalling outside the timed region)."""
+    x = np.ascontiguousarray(x, np.float32)
+    s = C.c_double(0)
+    st = ref.ref_time_codec(KIND[kind], rate, x, x.size, reps, C.byref(s))
+    if st:
+        raise RuntimeError(f"reference status {st}")
+    return float(s.value)
+
+
+def ref_time_allreduce(inputs: np.ndarray, kind: str, rate: int = 0, reps: int = 1) -> float:
+    """Median seconds of hcc::allreduce (Sum) on the reference library."""
+    x = np.ascontiguousarray(inputs, np.float32)
+    p, n = x.shape
+    s = C.c_double(0)
+    st = ref.ref_time_allreduce(p, n, x.reshape(-1), KIND[kind], rate, reps, C.byref(s))
+    if st:
+        raise RuntimeError(f"reference status {st}")
+    return float(s.value)
