@@ -146,6 +146,23 @@ HCCX_API hccx_status_t hccx_lossless_compress_host(const float* h_in, uint64_t n
 HCCX_API hccx_status_t hccx_lossless_decompress_host(const uint8_t* h_in, uint64_t bytes, uint64_t n, float* h_out,
                                                      int device);
 
+/* The communicator's framed LosslessPredictor message (one ring hop, one
+ * p2p / broadcast message): [32 B frame: u64 container bytes + the HCC1
+ * container header][chunk index: 17 u32 per 4096-value chunk -- byte offset,
+ * 32 u16 lane bit counts][payload byte-identical to hccx_lossless_compress].
+ * Neither call synchronises: sizes stay on the device.  frame_decode
+ * validates the frame (as hcc::from_bytes) and the index against the
+ * payload; a bad message -> HCCX_ERR_CORRUPT_PAYLOAD from hccx_frame_status.
+ * fold != 0: d_out = d_out + value (the ring's accumulation). */
+HCCX_API uint64_t hccx_lossless_frame_max_bytes(uint64_t n);
+HCCX_API hccx_status_t hccx_lossless_frame_encode(const float* d_in, uint64_t n, uint8_t* d_msg, uint64_t capacity,
+                                                  void* stream);
+HCCX_API hccx_status_t hccx_lossless_frame_decode(const uint8_t* d_msg, uint64_t capacity, uint64_t n, float* d_out,
+                                                  int fold, void* stream);
+/* Synchronises `stream`; the first error of frame_decode calls since the
+ * last status call (per device and host thread). */
+HCCX_API hccx_status_t hccx_frame_status(void* stream);
+
 /* Ring wire bytes (TraceEvent::wire_bytes * p) under LosslessPredictor,
  * which the size law cannot give: every hop's message is sized by the device
  * size pass.  collective: 0 reduce-scatter (d_in[j] = member j's n values;

@@ -58,6 +58,10 @@ hccx_lossless_compress = _sig("hccx_lossless_compress", _st, _p, _u64, _p, _u64,
 hccx_lossless_decompress = _sig("hccx_lossless_decompress", _st, _p, _u64, _u64, _p, _p)
 hccx_lossless_compress_host = _sig("hccx_lossless_compress_host", _st, _p, _u64, _p, _u64, C.POINTER(_u64), C.c_int)
 hccx_lossless_decompress_host = _sig("hccx_lossless_decompress_host", _st, _p, _u64, _u64, _p, C.c_int)
+hccx_lossless_frame_max_bytes = _sig("hccx_lossless_frame_max_bytes", _u64, _u64)
+hccx_lossless_frame_encode = _sig("hccx_lossless_frame_encode", _st, _p, _u64, _p, _u64, _p)
+hccx_lossless_frame_decode = _sig("hccx_lossless_frame_decode", _st, _p, _u64, _u64, _p, C.c_int, _p)
+hccx_frame_status = _sig("hccx_frame_status", _st, _p)
 hccx_lossless_ring_wire = _sig("hccx_lossless_ring_wire", _st, _pp, C.c_int, _u64, C.c_int, C.POINTER(_u64), _p)
 hccx_lossless_ring_wire_host = _sig("hccx_lossless_ring_wire_host", _st, _pp, C.c_int, _u64, C.c_int,
                                     C.POINTER(_u64), C.c_int)

@@ -5,6 +5,8 @@
 // Every entry point validates like the reference (status codes mirror the
 // exception hierarchy of proj/include/hcc/errors.hpp) and then only enqueues
 // step kernels (step_kernel.cuh); there is no host-side compute path.
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -19,7 +21,26 @@ using namespace hccx;
 
 namespace hccx {
 
-hccx_status_t cuda_status(cudaError_t e) { return e == cudaSuccess ? HCCX_OK : HCCX_ERR_CUDA; }
+namespace {
+hccx_status_t report_cuda(cudaError_t e, const char* file, int line) {
+  static const bool verbose = std::getenv("HCCX_VERBOSE") != nullptr;
+  if (verbose) {
+    int dev = -1;
+    cudaGetDevice(&dev);
+    std::fprintf(stderr, "hccx: CUDA failure at %s:%d (device %d, error %s: %s)\n", file, line, dev,
+                 cudaGetErrorName(e), cudaGetErrorString(e));
+  }
+  return HCCX_ERR_CUDA;
+}
+}  // namespace
+
+hccx_status_t cuda_fail(const char* file, int line) { return report_cuda(cudaPeekAtLastError(), file, line); }
+
+hccx_status_t cuda_status(cudaError_t e) { return e == cudaSuccess ? HCCX_OK : report_cuda(e, "cuda_status", 0); }
+
+hccx_status_t cuda_status_at(cudaError_t e, const char* file, int line) {
+  return e == cudaSuccess ? HCCX_OK : report_cuda(e, file, line);
+}
 
 hccx_status_t check_codec(hccx_codec_t c) {
   switch (c.kind) {
@@ -81,8 +102,8 @@ void set_divisor(StepParams& p, int mode, int nranks) {
 hccx_status_t run_step(CodecSel c, int op, StepParams& p, cudaStream_t s) {
   finalize_params(p, c, op);
   const cudaError_t e = launch_step(c, op, p, s);
-  if (e != cudaSuccess) return HCCX_ERR_CUDA;
-  return cuda_status(cudaGetLastError());
+  if (e != cudaSuccess) return HCCX_CUDA_FAIL;
+  return HCCX_STATUS(cudaGetLastError());
 }
 
 DeviceGuard::DeviceGuard(int dev) {
@@ -96,13 +117,14 @@ DeviceGuard::~DeviceGuard() {
 }
 
 hccx_status_t read_flag(uint32_t* d_err, cudaStream_t s) {
-  if (cudaStreamSynchronize(s) != cudaSuccess) return HCCX_ERR_CUDA;
+  if (cudaStreamSynchronize(s) != cudaSuccess) return HCCX_CUDA_FAIL;
   uint32_t h = 0;
-  if (cudaMemcpy(&h, d_err, 4, cudaMemcpyDeviceToHost) != cudaSuccess) return HCCX_ERR_CUDA;
-  if (h != 0 && cudaMemset(d_err, 0, 4) != cudaSuccess) return HCCX_ERR_CUDA;
+  if (cudaMemcpy(&h, d_err, 4, cudaMemcpyDeviceToHost) != cudaSuccess) return HCCX_CUDA_FAIL;
+  if (h != 0 && cudaMemset(d_err, 0, 4) != cudaSuccess) return HCCX_CUDA_FAIL;
   if (h & kErrTimeout) return HCCX_ERR_TIMEOUT;
   if (h & kErrPeer) return HCCX_ERR_TIMEOUT;
   if (h & kErrNonFinite) return HCCX_ERR_NONFINITE;
+  if (h & kErrCorrupt) return HCCX_ERR_CORRUPT_PAYLOAD;
   return HCCX_OK;
 }
 
@@ -173,7 +195,7 @@ extern "C" hccx_status_t hccx_compress(hccx_codec_t codec, const float* d_in, ui
   if (!d_in || !d_out) return HCCX_ERR_INVALID_ARGUMENT;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (codec.kind == HCCX_CODEC_IDENTITY)
-    return cuda_status(cudaMemcpyAsync(d_out, d_in, 4 * n, cudaMemcpyDeviceToDevice, s));
+    return HCCX_STATUS(cudaMemcpyAsync(d_out, d_in, 4 * n, cudaMemcpyDeviceToDevice, s));
   StepParams p{};
   p.njobs = 1;
   p.n = n;
@@ -194,7 +216,7 @@ extern "C" hccx_status_t hccx_decompress(hccx_codec_t codec, const uint8_t* d_in
   if (!d_in || !d_out) return HCCX_ERR_INVALID_ARGUMENT;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (codec.kind == HCCX_CODEC_IDENTITY)
-    return cuda_status(cudaMemcpyAsync(d_out, d_in, 4 * n, cudaMemcpyDeviceToDevice, s));
+    return HCCX_STATUS(cudaMemcpyAsync(d_out, d_in, 4 * n, cudaMemcpyDeviceToDevice, s));
   StepParams p{};
   p.njobs = 1;
   p.n = n;
@@ -263,8 +285,8 @@ hccx_status_t ensure_pipe(HostPipe* p, uint64_t vals, uint64_t bytes) {
       cudaFree(p->d_bytes[i]);
       p->d_vals[i] = nullptr;
       p->d_bytes[i] = nullptr;
-      if (cudaMalloc(&p->d_vals[i], 4 * vals + 64) != cudaSuccess) return HCCX_ERR_CUDA;
-      if (cudaMalloc(&p->d_bytes[i], bytes + 64) != cudaSuccess) return HCCX_ERR_CUDA;
+      if (cudaMalloc(&p->d_vals[i], 4 * vals + 64) != cudaSuccess) return HCCX_CUDA_FAIL;
+      if (cudaMalloc(&p->d_bytes[i], bytes + 64) != cudaSuccess) return HCCX_CUDA_FAIL;
     }
     p->vals_cap = vals;
     p->bytes_cap = bytes;
@@ -299,28 +321,28 @@ hccx_status_t host_codec(bool compress, hccx_codec_t codec, const void* h_in, ui
     if (compress) {
       if (cudaMemcpyAsync(p->d_vals[lane], static_cast<const float*>(h_in) + off, 4 * m,
                           cudaMemcpyHostToDevice, s) != cudaSuccess)
-        return HCCX_ERR_CUDA;
+        return HCCX_CUDA_FAIL;
       sp.jobs[0].src = p->d_vals[lane];
       sp.jobs[0].dst = p->d_bytes[lane];
       if ((st = run_step(c, kOpEncode, sp, s)) != HCCX_OK) return st;
       if (cudaMemcpyAsync(static_cast<uint8_t*>(h_out) + boff, p->d_bytes[lane], mb,
                           cudaMemcpyDeviceToHost, s) != cudaSuccess)
-        return HCCX_ERR_CUDA;
+        return HCCX_CUDA_FAIL;
     } else {
       if (cudaMemcpyAsync(p->d_bytes[lane], static_cast<const uint8_t*>(h_in) + boff, mb,
                           cudaMemcpyHostToDevice, s) != cudaSuccess)
-        return HCCX_ERR_CUDA;
+        return HCCX_CUDA_FAIL;
       sp.jobs[0].src = p->d_bytes[lane];
       sp.jobs[0].outs[0] = p->d_vals[lane];
       sp.jobs[0].nouts = 1;
       if ((st = run_step(c, kOpDecode, sp, s)) != HCCX_OK) return st;
       if (cudaMemcpyAsync(static_cast<float*>(h_out) + off, p->d_vals[lane], 4 * m,
                           cudaMemcpyDeviceToHost, s) != cudaSuccess)
-        return HCCX_ERR_CUDA;
+        return HCCX_CUDA_FAIL;
     }
   }
   for (int i = 0; i < kLanes; ++i)
-    if (cudaStreamSynchronize(p->streams[i]) != cudaSuccess) return HCCX_ERR_CUDA;
+    if (cudaStreamSynchronize(p->streams[i]) != cudaSuccess) return HCCX_CUDA_FAIL;
   return read_flag(p->d_err, p->streams[0]);
 }
 
@@ -368,7 +390,7 @@ hccx_status_t group_ws(hccx_group* g, uint64_t need) {
   if (g->ws) cudaFree(g->ws);
   g->ws = nullptr;
   g->ws_bytes = 0;
-  if (cudaMalloc(&g->ws, need) != cudaSuccess) return HCCX_ERR_CUDA;
+  if (cudaMalloc(&g->ws, need) != cudaSuccess) return HCCX_CUDA_FAIL;
   g->ws_bytes = need;
   return HCCX_OK;
 }
@@ -473,7 +495,7 @@ extern "C" hccx_status_t hccx_group_create(int p, int device, hccx_group_t* out)
   g->device = device;
   if (cudaMalloc(&g->d_err, 4) != cudaSuccess || cudaMemset(g->d_err, 0, 4) != cudaSuccess) {
     delete g;
-    return HCCX_ERR_CUDA;
+    return HCCX_CUDA_FAIL;
   }
   *out = g;
   return HCCX_OK;
@@ -501,7 +523,7 @@ extern "C" hccx_status_t hccx_group_allreduce(hccx_group_t g, const float* const
     for (int j = 0; j < p; ++j)
       if (d_out[j] != d_in[j] && n &&
           cudaMemcpyAsync(d_out[j], d_in[j], 4 * n, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
-        return HCCX_ERR_CUDA;
+        return HCCX_CUDA_FAIL;
     return HCCX_OK;
   }
   const CodecSel c = sel_of(codec);
@@ -522,7 +544,7 @@ extern "C" hccx_status_t hccx_group_reduce_scatter(hccx_group_t g, const float* 
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (p == 1 || n == 0) {
     if (n && cudaMemcpyAsync(d_shard[0], d_in[0], 4 * n, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
-      return HCCX_ERR_CUDA;
+      return HCCX_CUDA_FAIL;
     return HCCX_OK;
   }
   return ring_rs(g, sel_of(codec), d_in, n, nullptr, d_shard, nullptr, HCCX_SUM, s);
@@ -539,7 +561,7 @@ extern "C" hccx_status_t hccx_group_allgather(hccx_group_t g, const float* const
   if (p == 1 || shard_n == 0) {
     if (shard_n &&
         cudaMemcpyAsync(d_out[0], d_shard[0], 4 * shard_n, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
-      return HCCX_ERR_CUDA;
+      return HCCX_CUDA_FAIL;
     return HCCX_OK;
   }
   const CodecSel c = sel_of(codec);
@@ -571,7 +593,7 @@ extern "C" hccx_status_t hccx_group_broadcast(hccx_group_t g, int root, const fl
   if (n == 0) return HCCX_OK;
   if (p == 1) {
     if (d_out[0] != d_in && cudaMemcpyAsync(d_out[0], d_in, 4 * n, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
-      return HCCX_ERR_CUDA;
+      return HCCX_CUDA_FAIL;
     return HCCX_OK;
   }
   const CodecSel c = sel_of(codec);
@@ -603,7 +625,7 @@ extern "C" hccx_status_t hccx_group_p2p(hccx_group_t g, const float* d_in, float
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (n == 0) return HCCX_OK;
   const CodecSel c = sel_of(codec);
-  if (c.kind == 0) return cuda_status(cudaMemcpyAsync(d_out, d_in, 4 * n, cudaMemcpyDeviceToDevice, s));
+  if (c.kind == 0) return HCCX_STATUS(cudaMemcpyAsync(d_out, d_in, 4 * n, cudaMemcpyDeviceToDevice, s));
   if ((st = group_ws(g, align_up(payload_bytes(c, n), 256) + 256)) != HCCX_OK) return st;
   StepParams sp{};
   sp.n = n;
@@ -649,7 +671,7 @@ template <class F>
 hccx_status_t timed_run(hccx_group* g, double* secs, F&& body) {
   cudaStream_t s = nullptr;
   cudaEvent_t a = nullptr, b = nullptr;
-  if (cudaEventCreate(&a) != cudaSuccess || cudaEventCreate(&b) != cudaSuccess) return HCCX_ERR_CUDA;
+  if (cudaEventCreate(&a) != cudaSuccess || cudaEventCreate(&b) != cudaSuccess) return HCCX_CUDA_FAIL;
   cudaEventRecord(a, s);
   hccx_status_t st = body(s);
   cudaEventRecord(b, s);
@@ -663,10 +685,10 @@ hccx_status_t timed_run(hccx_group* g, double* secs, F&& body) {
 }
 
 hccx_status_t h2d(float* d, const float* h, uint64_t n) {
-  return n ? cuda_status(cudaMemcpy(d, h, 4 * n, cudaMemcpyHostToDevice)) : HCCX_OK;
+  return n ? HCCX_STATUS(cudaMemcpy(d, h, 4 * n, cudaMemcpyHostToDevice)) : HCCX_OK;
 }
 hccx_status_t d2h(float* h, const float* d, uint64_t n) {
-  return n ? cuda_status(cudaMemcpy(h, d, 4 * n, cudaMemcpyDeviceToHost)) : HCCX_OK;
+  return n ? HCCX_STATUS(cudaMemcpy(h, d, 4 * n, cudaMemcpyDeviceToHost)) : HCCX_OK;
 }
 
 }  // namespace
@@ -681,7 +703,7 @@ extern "C" hccx_status_t hccx_group_allreduce_host(hccx_group_t g, const float* 
   DevBufs B;
   std::vector<float*> din(g->p), dout(g->p);
   for (int j = 0; j < g->p; ++j) {
-    if (!(din[j] = B.add(n)) || !(dout[j] = B.add(n))) return HCCX_ERR_CUDA;
+    if (!(din[j] = B.add(n)) || !(dout[j] = B.add(n))) return HCCX_CUDA_FAIL;
     if ((st = h2d(din[j], h_in[j], n)) != HCCX_OK) return st;
   }
   st = timed_run(g, secs, [&](cudaStream_t s) {
@@ -705,7 +727,7 @@ extern "C" hccx_status_t hccx_group_reduce_scatter_host(hccx_group_t g, const fl
   DevBufs B;
   std::vector<float*> din(g->p), dsh(g->p);
   for (int j = 0; j < g->p; ++j) {
-    if (!(din[j] = B.add(n)) || !(dsh[j] = B.add(c))) return HCCX_ERR_CUDA;
+    if (!(din[j] = B.add(n)) || !(dsh[j] = B.add(c))) return HCCX_CUDA_FAIL;
     if ((st = h2d(din[j], h_in[j], n)) != HCCX_OK) return st;
   }
   st = timed_run(g, secs, [&](cudaStream_t s) {
@@ -727,7 +749,7 @@ extern "C" hccx_status_t hccx_group_allgather_host(hccx_group_t g, const float* 
   DevBufs B;
   std::vector<float*> dsh(g->p), dout(g->p);
   for (int j = 0; j < g->p; ++j) {
-    if (!(dsh[j] = B.add(shard_n)) || !(dout[j] = B.add(n))) return HCCX_ERR_CUDA;
+    if (!(dsh[j] = B.add(shard_n)) || !(dout[j] = B.add(n))) return HCCX_CUDA_FAIL;
     if ((st = h2d(dsh[j], h_shard[j], shard_n)) != HCCX_OK) return st;
   }
   st = timed_run(g, secs, [&](cudaStream_t s) {
@@ -748,9 +770,9 @@ extern "C" hccx_status_t hccx_group_broadcast_host(hccx_group_t g, int root, con
   DevBufs B;
   float* din = B.add(n);
   std::vector<float*> dout(g->p);
-  if (!din) return HCCX_ERR_CUDA;
+  if (!din) return HCCX_CUDA_FAIL;
   for (int j = 0; j < g->p; ++j)
-    if (!(dout[j] = B.add(n))) return HCCX_ERR_CUDA;
+    if (!(dout[j] = B.add(n))) return HCCX_CUDA_FAIL;
   if ((st = h2d(din, h_in, n)) != HCCX_OK) return st;
   st = timed_run(g, secs, [&](cudaStream_t s) {
     return hccx_group_broadcast(g, root, din, dout.data(), n, codec, s);
@@ -770,7 +792,7 @@ extern "C" hccx_status_t hccx_group_p2p_host(hccx_group_t g, const float* h_in, 
   DevBufs B;
   float* din = B.add(n);
   float* dout = B.add(n);
-  if (!din || !dout) return HCCX_ERR_CUDA;
+  if (!din || !dout) return HCCX_CUDA_FAIL;
   if ((st = h2d(din, h_in, n)) != HCCX_OK) return st;
   st = timed_run(g, secs, [&](cudaStream_t s) { return hccx_group_p2p(g, din, dout, n, codec, s); });
   if (st != HCCX_OK) return st;

@@ -102,8 +102,9 @@ extern "C" hccx_status_t hccx_comm_create(int rank, int nranks, int device, uint
   c->device = device;
   c->chunk_cap = align_up((max_n + nranks - 1) / nranks, kSegVals);
   // worst fixed-size codec (257 B / 64 values) or a framed LosslessPredictor
-  // message (4 B per value + flag bytes + kFrameBytes), whichever is larger
-  c->slot_bytes = align_up((c->chunk_cap / 64) * 257 + kFrameBytes, 256);
+  // message (lossless_msg.h: frame + chunk index + 4 B per value + flag
+  // bytes), whichever is larger
+  c->slot_bytes = align_up(std::max((c->chunk_cap / 64) * 257 + kFrameBytes, msg_max_bytes(c->chunk_cap)), 256);
   c->max_seg = static_cast<uint32_t>(c->chunk_cap / kSegVals);
   const uint64_t nslots = 3ull * nranks - 1;  // data-flag slots; the acks use kAckIdx per slot
   c->rs_off = 0;
@@ -129,7 +130,7 @@ extern "C" hccx_status_t hccx_comm_create(int rank, int nranks, int device, uint
   if (cudaMalloc(&c->win, c->win_bytes) != cudaSuccess || cudaMalloc(&c->d_err, 4) != cudaSuccess) {
     cudaFree(c->win);
     delete c;
-    return HCCX_ERR_CUDA;
+    return HCCX_CUDA_FAIL;
   }
   if (cudaMemset(c->win + c->flag_off, 0, c->os_off - c->flag_off) != cudaSuccess ||
       cudaMemset(c->win + c->os_flag_off, 0, c->win_bytes - c->os_flag_off) != cudaSuccess ||
@@ -137,7 +138,7 @@ extern "C" hccx_status_t hccx_comm_create(int rank, int nranks, int device, uint
     cudaFree(c->win);
     cudaFree(c->d_err);
     delete c;
-    return HCCX_ERR_CUDA;
+    return HCCX_CUDA_FAIL;
   }
   c->peers[rank] = c->win;
   *out = c;
@@ -155,7 +156,7 @@ extern "C" hccx_status_t hccx_comm_export(hccx_comm_t c, void* handle) {
   b.slot_bytes = c->slot_bytes;
   b.win_bytes = c->win_bytes;
   b.chunk_cap = c->chunk_cap;
-  if (cudaIpcGetMemHandle(&b.ipc, c->win) != cudaSuccess) return HCCX_ERR_CUDA;
+  if (cudaIpcGetMemHandle(&b.ipc, c->win) != cudaSuccess) return HCCX_CUDA_FAIL;
   std::memset(handle, 0, HCCX_HANDLE_BYTES);
   std::memcpy(handle, &b, sizeof(b));
   return HCCX_OK;
@@ -173,7 +174,7 @@ extern "C" hccx_status_t hccx_comm_connect(hccx_comm_t c, const void* handles) {
       return HCCX_ERR_INVALID_ARGUMENT;
     if (r == c->rank) continue;
     void* ptr = nullptr;
-    if (cudaIpcOpenMemHandle(&ptr, b.ipc, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) return HCCX_ERR_CUDA;
+    if (cudaIpcOpenMemHandle(&ptr, b.ipc, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) return HCCX_CUDA_FAIL;
     c->peers[r] = static_cast<uint8_t*>(ptr);
   }
   c->connected = true;
@@ -189,7 +190,8 @@ extern "C" hccx_status_t hccx_comm_destroy(hccx_comm_t c) {
       if (r != c->rank && c->peers[r]) cudaIpcCloseMemHandle(c->peers[r]);
   cudaFree(c->win);
   cudaFree(c->d_err);
-  cudaFree(c->ll_tmp);
+  c->ll_msg.release();
+  cudaFree(c->ll_acct);
   cudaFree(c->ll_work);
   cudaFree(c->ll_stage);
   cudaFree(c->d_trace);
@@ -448,10 +450,10 @@ hccx_status_t exec_rank(hccx_comm* c, hccx_codec_t codec, const RankWork& w, cud
   DeviceGuard guard(c->device);
   if (w.copy_bytes &&
       cudaMemcpyAsync(w.copy_dst, w.copy_src, w.copy_bytes, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
-    return HCCX_ERR_CUDA;
+    return HCCX_CUDA_FAIL;
   for (const FusedParams& P : w.launches)
-    if (launch_fused(sel_of(codec), &P, 1, s) != cudaSuccess) return HCCX_ERR_CUDA;
-  return cuda_status(cudaGetLastError());
+    if (launch_fused(sel_of(codec), &P, 1, s) != cudaSuccess) return HCCX_CUDA_FAIL;
+  return HCCX_STATUS(cudaGetLastError());
 }
 
 }  // namespace
@@ -542,9 +544,9 @@ extern "C" hccx_status_t hccx_comm_trace_enable(hccx_comm_t c, uint64_t capacity
   c->d_trace = nullptr;
   c->trace_cap = 0;
   if (capacity == 0) return HCCX_OK;
-  if (cudaMalloc(&c->d_trace, capacity * 8) != cudaSuccess) return HCCX_ERR_CUDA;
+  if (cudaMalloc(&c->d_trace, capacity * 8) != cudaSuccess) return HCCX_CUDA_FAIL;
   c->trace_cap = capacity;
-  return cuda_status(cudaMemset(c->d_trace, 0, capacity * 8));
+  return HCCX_STATUS(cudaMemset(c->d_trace, 0, capacity * 8));
 }
 
 extern "C" hccx_status_t hccx_comm_trace_read(hccx_comm_t c, uint64_t* host, uint64_t max_words, uint64_t* words) {
@@ -552,11 +554,11 @@ extern "C" hccx_status_t hccx_comm_trace_read(hccx_comm_t c, uint64_t* host, uin
   DeviceGuard guard(c->device);
   *words = 0;
   if (!c->d_trace) return HCCX_OK;
-  if (cudaDeviceSynchronize() != cudaSuccess) return HCCX_ERR_CUDA;
+  if (cudaDeviceSynchronize() != cudaSuccess) return HCCX_CUDA_FAIL;
   const uint64_t n = max_words < c->trace_cap ? max_words : c->trace_cap;
-  if (cudaMemcpy(host, c->d_trace, n * 8, cudaMemcpyDeviceToHost) != cudaSuccess) return HCCX_ERR_CUDA;
+  if (cudaMemcpy(host, c->d_trace, n * 8, cudaMemcpyDeviceToHost) != cudaSuccess) return HCCX_CUDA_FAIL;
   *words = n;
-  return cuda_status(cudaMemset(c->d_trace, 0, c->trace_cap * 8));
+  return HCCX_STATUS(cudaMemset(c->d_trace, 0, c->trace_cap * 8));
 }
 
 // ===================================================== single process ====
@@ -589,7 +591,7 @@ hccx_status_t mcomm_exec(hccx_mcomm* m, hccx_codec_t codec, std::vector<RankWork
       DeviceGuard guard(m->devices[j]);
       if (cudaMemcpyAsync(work[j].copy_dst, work[j].copy_src, work[j].copy_bytes, cudaMemcpyDeviceToDevice,
                           stream_of(j)) != cudaSuccess)
-        return HCCX_ERR_CUDA;
+        return HCCX_CUDA_FAIL;
     }
     passes = work[j].launches.size() > passes ? work[j].launches.size() : passes;
   }
@@ -607,10 +609,10 @@ hccx_status_t mcomm_exec(hccx_mcomm* m, hccx_codec_t codec, std::vector<RankWork
         }
       if (!nv) continue;
       DeviceGuard guard(dev);
-      if (launch_fused(sel_of(codec), P, nv, stream_of(first)) != cudaSuccess) return HCCX_ERR_CUDA;
+      if (launch_fused(sel_of(codec), P, nv, stream_of(first)) != cudaSuccess) return HCCX_CUDA_FAIL;
     }
   }
-  return cuda_status(cudaGetLastError());
+  return HCCX_STATUS(cudaGetLastError());
 }
 
 std::vector<cudaStream_t> mstreams(hccx_mcomm* m, void* const* streams) {
@@ -631,7 +633,7 @@ extern "C" hccx_status_t hccx_mcomm_create(int nmembers, const int* devices, uin
   HCCX_NVTX("hccx_mcomm_create");
   if (!out || !devices || nmembers < 1 || nmembers > kMaxRanks || max_n == 0) return HCCX_ERR_INVALID_ARGUMENT;
   int ndev = 0;
-  if (cudaGetDeviceCount(&ndev) != cudaSuccess) return HCCX_ERR_CUDA;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess) return HCCX_CUDA_FAIL;
   for (int j = 0; j < nmembers; ++j)
     if (devices[j] < 0 || devices[j] >= ndev) return HCCX_ERR_INVALID_ARGUMENT;
   hccx_mcomm* m = new hccx_mcomm();
@@ -654,7 +656,7 @@ extern "C" hccx_status_t hccx_mcomm_create(int nmembers, const int* devices, uin
         cudaGetLastError();
       } else if (e != cudaSuccess) {
         delete m;
-        return HCCX_ERR_CUDA;
+        return HCCX_CUDA_FAIL;
       }
     }
   // every rank uses the same CTAs per rank: the smallest share of a device
@@ -816,7 +818,7 @@ hccx_status_t mcomm_bufs(hccx_mcomm* m, uint64_t in_n, uint64_t out_n) {
   for (int j = 0; j < m->p; ++j) {
     DeviceGuard guard(m->devices[j]);
     if (cudaMalloc(&m->hin[j], 4 * cap) != cudaSuccess || cudaMalloc(&m->hout[j], 4 * cap) != cudaSuccess)
-      return HCCX_ERR_CUDA;
+      return HCCX_CUDA_FAIL;
   }
   m->hcap = cap;
   return HCCX_OK;
@@ -832,16 +834,16 @@ hccx_status_t mcomm_host_run(hccx_mcomm* m, const float* const* h_in, uint64_t i
     if (only_in >= 0 && j != only_in) continue;
     DeviceGuard guard(m->devices[j]);
     const float* src = only_in >= 0 ? h_in[0] : h_in[j];
-    if (in_n && cudaMemcpy(m->hin[j], src, 4 * in_n, cudaMemcpyHostToDevice) != cudaSuccess) return HCCX_ERR_CUDA;
+    if (in_n && cudaMemcpy(m->hin[j], src, 4 * in_n, cudaMemcpyHostToDevice) != cudaSuccess) return HCCX_CUDA_FAIL;
   }
   for (int dev : m->dev_list) {
     DeviceGuard guard(dev);
-    if (cudaDeviceSynchronize() != cudaSuccess) return HCCX_ERR_CUDA;
+    if (cudaDeviceSynchronize() != cudaSuccess) return HCCX_CUDA_FAIL;
   }
   cudaEvent_t a = nullptr, b = nullptr;
   {
     DeviceGuard guard(m->devices[0]);
-    if (cudaEventCreate(&a) != cudaSuccess || cudaEventCreate(&b) != cudaSuccess) return HCCX_ERR_CUDA;
+    if (cudaEventCreate(&a) != cudaSuccess || cudaEventCreate(&b) != cudaSuccess) return HCCX_CUDA_FAIL;
     cudaEventRecord(a, nullptr);
   }
   st = body();
@@ -864,7 +866,7 @@ hccx_status_t mcomm_host_run(hccx_mcomm* m, const float* const* h_in, uint64_t i
   for (int j = 0; j < m->p; ++j) {
     if (!out_mask[j] || !out_n) continue;
     DeviceGuard guard(m->devices[j]);
-    if (cudaMemcpy(h_out[j], m->hout[j], 4 * out_n, cudaMemcpyDeviceToHost) != cudaSuccess) return HCCX_ERR_CUDA;
+    if (cudaMemcpy(h_out[j], m->hout[j], 4 * out_n, cudaMemcpyDeviceToHost) != cudaSuccess) return HCCX_CUDA_FAIL;
   }
   return HCCX_OK;
 }

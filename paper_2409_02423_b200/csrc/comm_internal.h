@@ -5,6 +5,7 @@
 #include <cstdint>
 
 #include "hccx.h"
+#include "lossless_msg.h"
 #include "ring_fused.cuh"
 
 struct hccx_comm {
@@ -37,9 +38,11 @@ struct hccx_comm {
   // reference's wire accounting) and whole frames (payload + message header)
   uint64_t last_payload = 0, last_frame = 0;
   uint64_t last_recv = 0;  // framed payload bytes received (LosslessPredictor collectives)
-  // LosslessPredictor collectives: fold scratch (grown on demand, this device)
-  float* ll_tmp = nullptr;
-  uint64_t ll_tmp_cap = 0;
+  // LosslessPredictor collectives (grown on demand, this device): encoder
+  // scratch, byte accounting (payload pushed, message bytes pushed, payload
+  // received), the reduce-scatter work copy
+  hccx::MsgScratch ll_msg;
+  unsigned long long* ll_acct = nullptr;
   float* ll_work = nullptr;
   uint64_t ll_work_cap = 0;
   uint8_t* ll_stage = nullptr;  // whole framed message: root staging / receiver reassembly

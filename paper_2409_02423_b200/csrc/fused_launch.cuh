@@ -55,12 +55,14 @@ cudaError_t launch_oneshot_codec(const FusedParams* P, int nv, cudaStream_t stre
   if (groups == 0) return cudaSuccess;
   const void* kv = reinterpret_cast<const void*>(&oneshot_allreduce_vkernel<Codec>);
   // co-resident (cooperative) so no CTA waits on a peer while another CTA of
-  // this launch is still queued; ~8 groups per CTA, at most one CTA per SM
+  // this launch is still queued; ~2 groups per CTA, at most one CTA per SM
   uint64_t cap = static_cast<uint64_t>(fused_capacity(kv, kOsWarps * 32, 0));
   cap = cap < 148 ? cap : 148;
-  // groups per CTA (HCCX_OS_GPC, development knob; default below)
+  // groups per CTA (HCCX_OS_GPC, development knob). Measured at p = 4,
+  // 64 KiB-256 KiB (profiles/r02_small_p4_gpc.jsonl): 2 groups per CTA
+  // 1.07-1.15x faster than 8 (more CTAs pull peer data in parallel), 1 flat.
   const char* ge = std::getenv("HCCX_OS_GPC");
-  const uint64_t gpc = ge && std::atoi(ge) > 0 ? static_cast<uint64_t>(std::atoi(ge)) : 8u;
+  const uint64_t gpc = ge && std::atoi(ge) > 0 ? static_cast<uint64_t>(std::atoi(ge)) : 2u;
   uint64_t grid = (groups + gpc - 1) / gpc;
   const uint64_t lim = rank_grid_cap(P[0], cap, nv);
   grid = grid < lim ? grid : lim;

@@ -9,6 +9,12 @@
 namespace hccx {
 
 hccx_status_t cuda_status(cudaError_t e);
+// HCCX_ERR_CUDA, reporting the pending CUDA error and the failing site on
+// stderr when HCCX_VERBOSE is set (diagnostics for multi-device failures).
+hccx_status_t cuda_fail(const char* file, int line);
+#define HCCX_CUDA_FAIL ::hccx::cuda_fail(__FILE__, __LINE__)
+hccx_status_t cuda_status_at(cudaError_t e, const char* file, int line);
+#define HCCX_STATUS(e) ::hccx::cuda_status_at((e), __FILE__, __LINE__)
 hccx_status_t check_codec(hccx_codec_t c);
 CodecSel sel_of(hccx_codec_t c);
 void finalize_params(StepParams& p, CodecSel c, int op);

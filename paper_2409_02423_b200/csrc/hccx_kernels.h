@@ -6,7 +6,7 @@
 
 namespace hccx {
 
-enum : uint32_t { kErrNonFinite = 1u, kErrTimeout = 2u, kErrPeer = 4u };
+enum : uint32_t { kErrNonFinite = 1u, kErrTimeout = 2u, kErrPeer = 4u, kErrCorrupt = 8u };
 
 enum StepOp : int { kOpEncode = 0, kOpDecode = 1, kOpDAR = 2, kOpDecodeAdd = 3 };
 

@@ -18,6 +18,7 @@
 //           each coded chunk's 5-bit fields to find where the next chunk
 //           starts (fallback chunks cost O(1)); then one warp per chunk
 //           decodes in parallel from the recovered offsets.
+#include <atomic>
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
@@ -27,6 +28,7 @@
 #include "hccx.h"
 #include "hccx_internal.h"
 #include "hccx_kernels.h"
+#include "lossless_msg.h"
 
 namespace hccx {
 namespace {
@@ -130,7 +132,8 @@ __device__ void copy_stream_out(const uint32_t* sm, uint8_t* dst, uint32_t len, 
 __global__ void __launch_bounds__(kLLWarps * 32) ll_emit_kernel(const float* __restrict__ in, uint64_t n,
                                                                 uint64_t nchunks, const uint64_t* __restrict__ offsets,
                                                                 const uint8_t* __restrict__ fallback,
-                                                                uint8_t* __restrict__ out) {
+                                                                uint8_t* __restrict__ out,
+                                                                uint32_t* __restrict__ index) {
   extern __shared__ uint32_t llsm[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint32_t* sm = llsm + warp * (kStreamWords + 2);
@@ -140,7 +143,9 @@ __global__ void __launch_bounds__(kLLWarps * 32) ll_emit_kernel(const float* __r
     const uint32_t live = static_cast<uint32_t>(n - base < kChunk ? n - base : kChunk);
     const uint32_t* x = reinterpret_cast<const uint32_t*>(in) + base;
     uint8_t* dst = out + offsets[c];
+    uint32_t* ix = index ? index + kMsgIndexWords * c : nullptr;  // lossless_msg.h
     if (fallback[c]) {  // raw chunk (codec_kernels.hpp:190-194)
+      if (ix && lane <= 16) ix[lane] = lane ? 0u : static_cast<uint32_t>(offsets[c]);
       copy_stream_out(x, dst, 4 * live, lane);
       continue;
     }
@@ -155,6 +160,11 @@ __global__ void __launch_bounds__(kLLWarps * 32) ll_emit_kernel(const float* __r
       if (lane >= o) incl += t;
     }
     const uint32_t total = __shfl_sync(kFull, incl, 31);
+    if (ix) {  // chunk offset, then the lane bit counts as u16 pairs
+      const uint32_t up = __shfl_down_sync(kFull, mybits, 1);
+      if (lane == 0) ix[0] = static_cast<uint32_t>(offsets[c]);
+      if (!(lane & 1)) ix[1 + lane / 2] = mybits | (up << 16);
+    }
     const uint32_t words = (total + 31) / 32;
     for (uint32_t w = lane; w < words + 1; w += 32) sm[w] = 0;
     __syncwarp();
@@ -385,6 +395,19 @@ int grid_for(uint64_t work, int per_block) {
   return static_cast<int>(g < 148 * 16 ? (g ? g : 1) : 148 * 16);
 }
 
+// Dynamic shared memory above 48 KiB is a per-device function attribute:
+// set it once per (kernel, device).
+void smem_attr(const void* k, size_t bytes, std::atomic<uint64_t>& configured) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint64_t bit = 1ull << (dev & 63);
+  if (!(configured.load() & bit)) {
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
+    configured.fetch_or(bit);
+  }
+}
+std::atomic<uint64_t> g_emit_attr{0}, g_decode_attr{0};
+
 struct Scratch {
   uint32_t* sizes = nullptr;
   uint8_t* fallback = nullptr;
@@ -406,11 +429,11 @@ struct Scratch {
     cudaFree(sizes);
     cudaFree(fallback);
     cudaFree(offsets);
-    if (!err && cudaMalloc(&err, 4) != cudaSuccess) return HCCX_ERR_CUDA;
+    if (!err && cudaMalloc(&err, 4) != cudaSuccess) return HCCX_CUDA_FAIL;
     const uint64_t c = nchunks + 1;
     if (cudaMalloc(&sizes, 4 * c) != cudaSuccess || cudaMalloc(&fallback, c) != cudaSuccess ||
         cudaMalloc(&offsets, 8 * c) != cudaSuccess)
-      return HCCX_ERR_CUDA;
+      return HCCX_CUDA_FAIL;
     cap = c;
     return HCCX_OK;
   }
@@ -445,11 +468,11 @@ hccx_status_t size_pass(const float* d_in, uint64_t n, Scratch& s, cudaStream_t 
   ll_size_kernel<<<grid_for(nch, kLLWarps), kLLWarps * 32, 0, st>>>(d_in, n, nch, s.sizes, s.fallback);
   ll_scan_kernel<<<1, 1024, 0, st>>>(s.sizes, nch, (nch + 7) / 8, s.offsets);
   count_launch(2);
-  if (cudaGetLastError() != cudaSuccess) return HCCX_ERR_CUDA;
+  if (cudaGetLastError() != cudaSuccess) return HCCX_CUDA_FAIL;
   if (total) {
     if (cudaMemcpyAsync(total, s.offsets + nch, 8, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
         cudaStreamSynchronize(st) != cudaSuccess)
-      return HCCX_ERR_CUDA;
+      return HCCX_CUDA_FAIL;
   }
   return HCCX_OK;
 }
@@ -508,16 +531,12 @@ extern "C" hccx_status_t hccx_lossless_compress(const float* d_in, uint64_t n, u
   if (*bytes > capacity) return HCCX_ERR_INVALID_ARGUMENT;
   const uint64_t nch = (n + kChunk - 1) / kChunk;
   const size_t smem = sizeof(uint32_t) * kLLWarps * (kStreamWords + 2);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(ll_emit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    attr = true;
-  }
+  smem_attr(reinterpret_cast<const void*>(&ll_emit_kernel), smem, g_emit_attr);
   ll_flags_kernel<<<grid_for((nch + 7) / 8, 256), 256, 0, st>>>(t_scratch.fallback, nch, d_out);
   ll_emit_kernel<<<grid_for(nch, kLLWarps), kLLWarps * 32, smem, st>>>(d_in, n, nch, t_scratch.offsets,
-                                                                      t_scratch.fallback, d_out);
+                                                                      t_scratch.fallback, d_out, nullptr);
   count_launch(2);
-  return cuda_status(cudaGetLastError());
+  return HCCX_STATUS(cudaGetLastError());
 }
 
 extern "C" hccx_status_t hccx_lossless_decompress(const uint8_t* d_in, uint64_t in_bytes, uint64_t n, float* d_out,
@@ -542,7 +561,7 @@ extern "C" hccx_status_t hccx_lossless_decompress(const uint8_t* d_in, uint64_t 
     std::vector<uint8_t> flags((nch + 7) / 8);
     if (cudaMemcpyAsync(flags.data(), d_in, flags.size(), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
         cudaStreamSynchronize(st) != cudaSuccess)
-      return HCCX_ERR_CUDA;
+      return HCCX_CUDA_FAIL;
     uint64_t raw = 0;
     for (uint64_t c = 0; c < nch; ++c) raw += (flags[c / 8] >> (c % 8)) & 1u;
     jump = nch - raw >= 64 && t_scratch.ensure_jump(S + 2);
@@ -564,13 +583,13 @@ extern "C" hccx_status_t hccx_lossless_decompress(const uint8_t* d_in, uint64_t 
                                                                           d_out);
   count_launch(1);
   count_launch(2);
-  if (cudaGetLastError() != cudaSuccess) return HCCX_ERR_CUDA;
+  if (cudaGetLastError() != cudaSuccess) return HCCX_CUDA_FAIL;
   uint32_t e = 0;
   uint64_t end = 0;
   if (cudaMemcpyAsync(&e, t_scratch.err, 4, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
       cudaMemcpyAsync(&end, t_scratch.offsets + nch, 8, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
       cudaStreamSynchronize(st) != cudaSuccess)
-    return HCCX_ERR_CUDA;
+    return HCCX_CUDA_FAIL;
   (void)end;  // trailing bytes are ignored, as in codec_serial.cpp:85-107
   if (8 * t_scratch.jump_cap > kJumpKeepBytes) t_scratch.drop_jump();  // do not pin large tables
   if (e) return HCCX_ERR_CORRUPT_PAYLOAD;
@@ -649,7 +668,7 @@ extern "C" hccx_status_t hccx_lossless_ring_hops(const float* const* d_in, int p
     return HCCX_OK;
   }
   float* part = nullptr;
-  if (cudaMalloc(&part, 4 * c) != cudaSuccess) return HCCX_ERR_CUDA;
+  if (cudaMalloc(&part, 4 * c) != cudaSuccess) return HCCX_CUDA_FAIL;
   for (int k = 0; k < p && r == HCCX_OK; ++k) {
     // chunk k: the round-t message is sent by member (k+1+t) mod p and holds
     // the fold of members k+1 .. k+1+t (collectives.cpp:34-61)
@@ -721,4 +740,306 @@ extern "C" hccx_status_t hccx_lossless_ring_hops_host(const float* const* h_in, 
   if (r == HCCX_OK) r = hccx_lossless_ring_hops(d, p, n, collective, hop, nullptr);
   for (int j = 0; j < p; ++j) cudaFree(d[j]);
   return r;
+}
+
+// ---------------------------------------------------------------------------
+// Framed messages with a chunk index (lossless_msg.h): the communicator's
+// LosslessPredictor transport.
+
+namespace hccx {
+namespace {
+
+constexpr uint32_t kMsgLaneStride = kLaneVals + 1;  // 129: conflict-free lane-major staging
+constexpr size_t kMsgDecodeSmem = sizeof(uint32_t) * kLLWarps * (32 * kMsgLaneStride + 32);
+
+__device__ __forceinline__ uint64_t ld_le64(const uint8_t* p) {
+  uint64_t v = 0;
+  for (int k = 0; k < 8; ++k) v |= static_cast<uint64_t>(p[k]) << (8 * k);
+  return v;
+}
+
+// The frame (lossless_msg.h): u64 container bytes + HCC1 header.
+__global__ void msg_header_kernel(uint8_t* msg, const uint64_t* __restrict__ offsets, uint64_t nch, uint64_t n,
+                                  uint64_t idx_bytes, unsigned long long* acct) {
+  if (threadIdx.x != 0) return;
+  const uint64_t payload = offsets[nch];
+  const uint64_t container = 18 + payload;
+  uint8_t h[26];
+  for (int i = 0; i < 8; ++i) h[i] = static_cast<uint8_t>(container >> (8 * i));
+  h[8] = 'H', h[9] = 'C', h[10] = 'C', h[11] = '1';
+  h[12] = HCCX_CODEC_LOSSLESS;  // kind
+  h[13] = 0;                    // rate_bits
+  for (int i = 0; i < 8; ++i) h[14 + i] = static_cast<uint8_t>(n >> (8 * i));
+  for (int i = 0; i < 4; ++i) h[22 + i] = static_cast<uint8_t>(nch >> (8 * i));
+  for (int i = 0; i < 26; ++i) msg[i] = h[i];
+  if (acct) {
+    atomicAdd(acct, static_cast<unsigned long long>(payload));
+    atomicAdd(acct + 1, static_cast<unsigned long long>(kMsgHeaderBytes + idx_bytes + payload));
+  }
+}
+
+struct MsgDsts {
+  uint8_t* d[kMsgMaxDsts];
+  int nd;
+};
+
+__global__ void msg_copy_kernel(const uint8_t* __restrict__ src, MsgDsts D, uint64_t idx_bytes,
+                                unsigned long long* acct) {
+  const uint64_t payload = *reinterpret_cast<const uint64_t*>(src) - 18;
+  const uint64_t bytes = kMsgHeaderBytes + idx_bytes + payload;
+  const uint64_t vec = (bytes + 15) / 16;  // msg_max_bytes leaves 16 bytes of slack
+  const uint4* s = reinterpret_cast<const uint4*>(src);
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < vec;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint4 v = s[i];
+    for (int k = 0; k < D.nd; ++k) reinterpret_cast<uint4*>(D.d[k])[i] = v;
+  }
+  if (acct && blockIdx.x == 0 && threadIdx.x == 0) {
+    atomicAdd(acct, static_cast<unsigned long long>(payload * D.nd));
+    atomicAdd(acct + 1, static_cast<unsigned long long>(bytes * D.nd));
+  }
+}
+
+// 4 bytes at an arbitrary byte offset of a 4-byte aligned buffer (may read
+// up to 3 bytes past the value: msg_max_bytes' slack).
+__device__ __forceinline__ uint32_t ld_u32_at(const uint8_t* base, uint64_t a) {
+  const uint32_t* q = reinterpret_cast<const uint32_t*>(base);
+  const uint32_t lo = q[a >> 2];
+  const uint32_t sh = static_cast<uint32_t>(a & 3);
+  return sh ? __funnelshift_r(lo, q[(a >> 2) + 1], 8 * sh) : lo;
+}
+
+// Decode: one warp per chunk.  Raw chunks are copied; coded chunks are
+// decoded by 32 lanes from their indexed bit positions (128 codes each) into
+// lane-major shared memory, the lanes' XOR carries are scanned (the
+// predictor is x_i = x_{i-1} ^ r_i within a chunk), and the warp writes the
+// chunk out coalesced, folding into `out` when asked.
+__global__ void __launch_bounds__(kLLWarps * 32) msg_decode_kernel(const uint8_t* __restrict__ msg, uint64_t msg_cap,
+                                                                   uint64_t n, uint64_t nch, uint64_t idx_bytes,
+                                                                   float* __restrict__ out, int fold,
+                                                                   uint32_t* __restrict__ err,
+                                                                   unsigned long long* recv_acct) {
+  extern __shared__ uint32_t msm[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t* sm = msm + warp * (32 * kMsgLaneStride + 32);
+  uint32_t* carry = sm + 32 * kMsgLaneStride;
+  // frame checks (hcc::from_bytes, codec.cpp:101-121)
+  const uint64_t container = *reinterpret_cast<const uint64_t*>(msg);
+  const uint64_t flag_bytes = (nch + 7) / 8;
+  const bool frame_ok = container >= 18 && msg[8] == 'H' && msg[9] == 'C' && msg[10] == 'C' && msg[11] == '1' &&
+                        msg[12] == HCCX_CODEC_LOSSLESS && ld_le64(msg + 14) == n &&
+                        (ld_le64(msg + 22) & 0xffffffffull) == nch && container - 18 >= flag_bytes &&
+                        kMsgHeaderBytes + idx_bytes + (container - 18) + 16 <= msg_cap;
+  if (!frame_ok) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(err, kErrCorrupt);
+    return;
+  }
+  const uint64_t payload = container - 18;
+  if (recv_acct && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(recv_acct, static_cast<unsigned long long>(payload));
+  const uint32_t* idx = reinterpret_cast<const uint32_t*>(msg + kMsgHeaderBytes);
+  const uint8_t* pay = msg + kMsgHeaderBytes + idx_bytes;
+  uint32_t* o32 = reinterpret_cast<uint32_t*>(out);
+  bool bad = false;
+  for (uint64_t c = static_cast<uint64_t>(blockIdx.x) * kLLWarps + warp; c < nch;
+       c += static_cast<uint64_t>(gridDim.x) * kLLWarps) {
+    const uint64_t base = c * kChunk;
+    const uint32_t live = static_cast<uint32_t>(n - base < kChunk ? n - base : kChunk);
+    const uint32_t* e = idx + kMsgIndexWords * c;
+    const uint64_t off = e[0];
+    const uint64_t end = c + 1 < nch ? idx[kMsgIndexWords * (c + 1)] : payload;
+    if (off < flag_bytes || end < off || end > payload) {
+      bad = true;
+      break;
+    }
+    if ((pay[c / 8] >> (c % 8)) & 1u) {  // raw chunk
+      if (end - off != 4ull * live) {
+        bad = true;
+        break;
+      }
+      for (uint32_t k = lane; k < live; k += 32) {
+        const uint32_t v = ld_u32_at(pay, off + 4ull * k);
+        o32[base + k] = fold ? __float_as_uint(__fadd_rn(out[base + k], __uint_as_float(v))) : v;
+      }
+      continue;
+    }
+    const uint32_t mybits = (e[1 + lane / 2] >> (16 * (lane & 1))) & 0xffffu;
+    uint32_t incl = mybits;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t t = __shfl_up_sync(kFull, incl, d);
+      if (lane >= d) incl += t;
+    }
+    const uint32_t total = __shfl_sync(kFull, incl, 31);
+    if ((total + 7ull) / 8 != end - off) {
+      bad = true;
+      break;
+    }
+    const uint32_t i0 = lane * kLaneVals, i1 = min(live, i0 + kLaneVals);
+    uint64_t bit = off * 8 + (incl - mybits);
+    const uint64_t bit0 = bit;
+    uint64_t wi = bit >> 6;
+    uint64_t lo = ll_word(pay, payload, wi), hi = ll_word(pay, payload, wi + 1);
+    uint32_t prev = 0;
+    for (uint32_t i = i0; i < i1; ++i) {
+      const uint64_t w = bit >> 6;
+      if (w != wi) {
+        lo = hi;
+        hi = ll_word(pay, payload, w + 1);
+        if (w != wi + 1) lo = ll_word(pay, payload, w);
+        wi = w;
+      }
+      const uint32_t sh = static_cast<uint32_t>(bit & 63);
+      const uint64_t win = sh ? (lo >> sh) | (hi << (64 - sh)) : lo;
+      const uint32_t nb = 32 - static_cast<uint32_t>(win & 31u);
+      const uint32_t low = static_cast<uint32_t>(win >> 5) & (nb >= 32 ? 0xffffffffu : ((1u << nb) - 1u));
+      bit += 5 + nb;
+      prev ^= low;
+      sm[lane * kMsgLaneStride + (i - i0)] = prev;
+    }
+    const bool lane_bad = bit - bit0 != mybits;
+    // exclusive XOR scan of the lanes' totals -> each lane's carry
+    uint32_t x = prev;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t t = __shfl_up_sync(kFull, x, d);
+      if (lane >= d) x ^= t;
+    }
+    carry[lane] = x ^ prev;
+    if (__any_sync(kFull, lane_bad)) {
+      bad = true;
+      break;
+    }
+    __syncwarp();
+    for (uint32_t k = lane; k < live; k += 32) {
+      const uint32_t v = sm[(k >> 7) * kMsgLaneStride + (k & 127)] ^ carry[k >> 7];
+      o32[base + k] = fold ? __float_as_uint(__fadd_rn(out[base + k], __uint_as_float(v))) : v;
+    }
+    __syncwarp();
+  }
+  if (bad && lane == 0) atomicOr(err, kErrCorrupt);
+}
+
+}  // namespace
+
+hccx_status_t MsgScratch::ensure(uint64_t nchunks) {
+  if (nchunks + 1 <= cap && sizes) return HCCX_OK;
+  release();
+  const uint64_t c = nchunks + 1;
+  if (cudaMalloc(&sizes, 4 * c) != cudaSuccess || cudaMalloc(&fallback, c) != cudaSuccess ||
+      cudaMalloc(&offsets, 8 * c) != cudaSuccess) {
+    release();
+    return HCCX_CUDA_FAIL;
+  }
+  cap = c;
+  return HCCX_OK;
+}
+
+void MsgScratch::release() {
+  cudaFree(sizes);
+  cudaFree(fallback);
+  cudaFree(offsets);
+  sizes = nullptr;
+  fallback = nullptr;
+  offsets = nullptr;
+  cap = 0;
+}
+
+hccx_status_t msg_encode(const float* in, uint64_t n, uint8_t* msg, MsgScratch& s, unsigned long long* acct,
+                         cudaStream_t st) {
+  const uint64_t nch = msg_chunks(n);
+  hccx_status_t r = s.ensure(nch);
+  if (r != HCCX_OK) return r;
+  const uint64_t ib = msg_index_bytes(n);
+  uint8_t* pay = msg + kMsgHeaderBytes + ib;
+  const size_t smem = sizeof(uint32_t) * kLLWarps * (kStreamWords + 2);
+  smem_attr(reinterpret_cast<const void*>(&ll_emit_kernel), smem, g_emit_attr);
+  if (n) {
+    ll_size_kernel<<<grid_for(nch, kLLWarps), kLLWarps * 32, 0, st>>>(in, n, nch, s.sizes, s.fallback);
+    ll_scan_kernel<<<1, 1024, 0, st>>>(s.sizes, nch, (nch + 7) / 8, s.offsets);
+    ll_flags_kernel<<<grid_for((nch + 7) / 8, 256), 256, 0, st>>>(s.fallback, nch, pay);
+    ll_emit_kernel<<<grid_for(nch, kLLWarps), kLLWarps * 32, smem, st>>>(
+        in, n, nch, s.offsets, s.fallback, pay, reinterpret_cast<uint32_t*>(msg + kMsgHeaderBytes));
+    count_launch(4);
+  } else if (cudaMemsetAsync(s.offsets, 0, 8, st) != cudaSuccess) {
+    return HCCX_CUDA_FAIL;
+  }
+  msg_header_kernel<<<1, 32, 0, st>>>(msg, s.offsets, nch, n, ib, acct);
+  count_launch();
+  return HCCX_STATUS(cudaGetLastError());
+}
+
+hccx_status_t msg_copy(const uint8_t* src, uint64_t n, uint8_t* const* dsts, int ndst, unsigned long long* acct,
+                       cudaStream_t st) {
+  if (ndst < 1) return HCCX_OK;
+  if (ndst > kMsgMaxDsts) return HCCX_ERR_INVALID_ARGUMENT;
+  MsgDsts D{};
+  for (int k = 0; k < ndst; ++k) D.d[k] = dsts[k];
+  D.nd = ndst;
+  const uint64_t vec = msg_max_bytes(n) / 16;
+  msg_copy_kernel<<<grid_for(vec, 256 * 4), 256, 0, st>>>(src, D, msg_index_bytes(n), acct);
+  count_launch();
+  return HCCX_STATUS(cudaGetLastError());
+}
+
+hccx_status_t msg_decode(const uint8_t* msg, uint64_t msg_cap, uint64_t n, float* out, bool fold, uint32_t* err,
+                         unsigned long long* recv_acct, cudaStream_t st) {
+  const uint64_t nch = msg_chunks(n);
+  smem_attr(reinterpret_cast<const void*>(&msg_decode_kernel), kMsgDecodeSmem, g_decode_attr);
+  msg_decode_kernel<<<grid_for(nch ? nch : 1, kLLWarps), kLLWarps * 32, kMsgDecodeSmem, st>>>(
+      msg, msg_cap, n, nch, msg_index_bytes(n), out, fold ? 1 : 0, err, recv_acct);
+  count_launch();
+  return HCCX_STATUS(cudaGetLastError());
+}
+
+}  // namespace hccx
+
+namespace hccx {
+namespace {
+struct FrameState {
+  MsgScratch scratch;
+  uint32_t* err = nullptr;
+  ~FrameState() {
+    scratch.release();
+    cudaFree(err);
+  }
+};
+FrameState& frame_state() {
+  thread_local FrameState s[16];
+  int d = 0;
+  cudaGetDevice(&d);
+  return s[d & 15];
+}
+hccx_status_t frame_err(FrameState& f) {
+  if (f.err) return HCCX_OK;
+  if (cudaMalloc(&f.err, 4) != cudaSuccess || cudaMemset(f.err, 0, 4) != cudaSuccess) return HCCX_CUDA_FAIL;
+  return HCCX_OK;
+}
+}  // namespace
+}  // namespace hccx
+
+extern "C" uint64_t hccx_lossless_frame_max_bytes(uint64_t n) { return msg_max_bytes(n); }
+
+extern "C" hccx_status_t hccx_lossless_frame_encode(const float* d_in, uint64_t n, uint8_t* d_msg, uint64_t capacity,
+                                                    void* stream) {
+  HCCX_NVTX("hccx_lossless_frame_encode");
+  if (!d_msg || (n && !d_in) || capacity < msg_max_bytes(n) || (reinterpret_cast<uintptr_t>(d_msg) & 15))
+    return HCCX_ERR_INVALID_ARGUMENT;
+  return msg_encode(d_in, n, d_msg, frame_state().scratch, nullptr, static_cast<cudaStream_t>(stream));
+}
+
+extern "C" hccx_status_t hccx_lossless_frame_decode(const uint8_t* d_msg, uint64_t capacity, uint64_t n, float* d_out,
+                                                    int fold, void* stream) {
+  HCCX_NVTX("hccx_lossless_frame_decode");
+  if (!d_msg || (n && !d_out) || (reinterpret_cast<uintptr_t>(d_msg) & 15)) return HCCX_ERR_INVALID_ARGUMENT;
+  FrameState& f = frame_state();
+  const hccx_status_t st = frame_err(f);
+  if (st != HCCX_OK) return st;
+  return msg_decode(d_msg, capacity, n, d_out, fold != 0, f.err, nullptr, static_cast<cudaStream_t>(stream));
+}
+
+extern "C" hccx_status_t hccx_frame_status(void* stream) {
+  FrameState& f = frame_state();
+  const hccx_status_t st = frame_err(f);
+  if (st != HCCX_OK) return st;
+  return read_flag(f.err, static_cast<cudaStream_t>(stream));
 }

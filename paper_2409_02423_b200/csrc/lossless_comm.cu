@@ -4,23 +4,23 @@
 // The reference's MZHybrid scheme sends TP / PP / ZeRO traffic through the
 // LosslessPredictor (proj/src/parallel3d.cpp:63-69): every ring hop carries
 // compress(partial) (proj/src/collectives.cpp:44), whose size is data
-// dependent.  Here each hop is a framed message in the receiver's slot:
-//
-//   [u64 container bytes][HCC1 container header (18 B, codec.cpp:89-99)]
-//   [pad to kFrameBytes][LosslessPredictor payload]
-//
-// The sender compresses straight into the peer's slot (the emit kernel's
-// stores cross NVLink), writes the frame, and publishes the slot's data
-// flag with a system-scope fence + store; the receiver waits for the flag on
-// the device, reads and validates the frame like hcc::from_bytes
-// (codec.cpp:101-121: magic, kind, lengths -> CorruptPayloadError),
-// decompresses, folds (acc = dec + acc, collectives.cpp:50) and acks the
-// slot.  The codec's sizes are host-visible (its size pass synchronises), so
-// the sequence is host-driven per rank; a single-process communicator runs
-// every member's stage before any member's next stage, so no host wait ever
-// depends on work not yet enqueued.  Values are exact (the codec is
-// lossless), so results equal the identity ring's bit for bit; the traced
-// wire bytes are the payload bytes actually pushed.
+// dependent.  Here each hop is a framed message in the receiver's slot
+// (lossless_msg.h: frame + HCC1 header, a chunk index, the payload
+// byte-identical to hcc::compress).  The sender encodes straight into the
+// peer's slot (the emit kernel's stores cross NVLink; the frame's size is
+// written by a kernel from the device-side scan) and publishes the slot's
+// data flag with a system-scope fence + store; the receiver waits for the
+// flag on the device, validates the frame like hcc::from_bytes
+// (codec.cpp:101-121: magic, kind, lengths -> CorruptPayloadError) and
+// decodes warp-per-chunk from the index, folding into its accumulator
+// (acc = acc + dec, collectives.cpp:50), then acks the slot.  No stage
+// waits on the host: sizes, errors and the byte accounting stay on the
+// device until the collective's one synchronisation at the end (broadcast
+// and p2p also read the message size once, to cut it into slot fragments).
+// A single-process communicator enqueues every member's stage before any
+// member's next stage.  Values are exact (the codec is lossless), so results
+// equal the identity ring's bit for bit; the traced wire bytes are the
+// payload bytes actually pushed.
 #include <cstdlib>
 #include <cstring>
 #include <vector>
@@ -29,10 +29,9 @@
 #include "device_common.cuh"
 #include "hccx.h"
 #include "hccx_internal.h"
+#include "lossless_msg.h"
 
 namespace hccx {
-
-cudaError_t ll_fold(float* part, const float* x, uint64_t n, cudaStream_t stream);
 
 namespace {
 
@@ -59,25 +58,11 @@ __global__ void ll_wait_kernel(const uint32_t* flags, uint32_t count, uint32_t e
   }
 }
 
-__global__ void ll_frame_kernel(uint8_t* dst, uint64_t container_bytes, uint64_t n, uint32_t chunks) {
-  if (threadIdx.x != 0) return;
-  uint8_t h[26];
-  for (int i = 0; i < 8; ++i) h[i] = static_cast<uint8_t>(container_bytes >> (8 * i));
-  h[8] = 'H', h[9] = 'C', h[10] = 'C', h[11] = '1';
-  h[12] = HCCX_CODEC_LOSSLESS;  // kind
-  h[13] = 0;                    // rate_bits
-  for (int i = 0; i < 8; ++i) h[14 + i] = static_cast<uint8_t>(n >> (8 * i));
-  for (int i = 0; i < 4; ++i) h[22 + i] = static_cast<uint8_t>(chunks >> (8 * i));
-  for (int i = 0; i < 26; ++i) dst[i] = h[i];
-}
-
 __global__ void ll_scale_kernel(float* x, uint64_t n, int div_mode, float recip, float divisor) {
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
     x[i] = div_mode == 1 ? __fmul_rn(x[i], recip) : __fdiv_rn(x[i], divisor);
 }
-
-constexpr uint32_t kPredictorChunk = 4096;
 
 uint32_t* host_flag(const hccx_comm* c, int rank, int cls, int slot, uint32_t idx) {
   uint32_t* f = reinterpret_cast<uint32_t*>(c->peers[rank] + c->flag_off);
@@ -101,37 +86,16 @@ hccx_status_t ensure(float*& buf, uint64_t& cap, uint64_t n) {
   cudaFree(buf);
   buf = nullptr;
   cap = 0;
-  if (cudaMalloc(&buf, 4 * (n ? n : 1)) != cudaSuccess) return HCCX_ERR_CUDA;
+  if (cudaMalloc(&buf, 4 * (n ? n : 1)) != cudaSuccess) return HCCX_CUDA_FAIL;
   cap = n;
   return HCCX_OK;
 }
 
-hccx_status_t launched() { return cuda_status(cudaGetLastError()); }
+hccx_status_t launched() { return HCCX_STATUS(cudaGetLastError()); }
 
-// One framed message: compress `m` values into slot (cls, slot) of `dst`.
-hccx_status_t send_frame(hccx_comm* c, const float* src, uint64_t m, int dst, int cls, int slot, cudaStream_t s,
-                         uint64_t* payload) {
-  uint8_t* base = host_slot(c, dst, cls, slot);
-  uint64_t bytes = 0;
-  hccx_status_t st = hccx_lossless_compress(src, m, base + kFrameBytes, c->slot_bytes - kFrameBytes, &bytes, s);
-  if (st != HCCX_OK) return st;
-  ll_frame_kernel<<<1, 32, 0, s>>>(base, 18 + bytes, m, static_cast<uint32_t>((m + kPredictorChunk - 1) / kPredictorChunk));
-  count_launch();
-  *payload = bytes;
-  c->last_payload += bytes;
-  c->last_frame += kFrameBytes + bytes;
-  return launched();
-}
-
-// Copy an already framed message (local slot) into `dst`'s slot.
-hccx_status_t copy_frame(hccx_comm* c, const uint8_t* frame, uint64_t payload, int dst, int cls, int slot,
-                         cudaStream_t s) {
-  if (cudaMemcpyAsync(host_slot(c, dst, cls, slot), frame, kFrameBytes + payload, cudaMemcpyDeviceToDevice, s) !=
-      cudaSuccess)
-    return HCCX_ERR_CUDA;
-  c->last_payload += payload;
-  c->last_frame += kFrameBytes + payload;
-  return HCCX_OK;
+// One framed message: encode `m` values into slot (cls, slot) of `dst`.
+hccx_status_t send_frame(hccx_comm* c, const float* src, uint64_t m, int dst, int cls, int slot, cudaStream_t s) {
+  return msg_encode(src, m, host_slot(c, dst, cls, slot), c->ll_msg, c->ll_acct, s);
 }
 
 hccx_status_t signal(hccx_comm* c, int rank, int cls, int slot, uint32_t count, uint32_t value, cudaStream_t s) {
@@ -146,29 +110,13 @@ hccx_status_t wait(hccx_comm* c, int cls, int slot, uint32_t count, uint32_t epo
   return launched();
 }
 
-// Receive side: wait for the slot's data flag, read the frame back and
-// validate it as hcc::from_bytes would, decompress into `out`.
-hccx_status_t recv_frame(hccx_comm* c, int cls, int slot, uint32_t epoch, uint64_t m, float* out, cudaStream_t s) {
-  hccx_status_t st = wait(c, cls, slot, 1, epoch, s);
+// Receive side: wait for the slot's data flag, validate and decode the
+// message into `out` (fold: out = out + value).
+hccx_status_t recv_frame(hccx_comm* c, int cls, int slot, uint32_t epoch, uint64_t m, float* out, bool fold,
+                         cudaStream_t s) {
+  const hccx_status_t st = wait(c, cls, slot, 1, epoch, s);
   if (st != HCCX_OK) return st;
-  const uint8_t* base = host_slot(c, c->rank, cls, slot);
-  uint8_t h[26];
-  uint32_t err = 0;
-  if (cudaMemcpyAsync(h, base, 26, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
-      cudaMemcpyAsync(&err, c->d_err, 4, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
-      cudaStreamSynchronize(s) != cudaSuccess)
-    return HCCX_ERR_CUDA;
-  if (err & kErrTimeout) return HCCX_ERR_TIMEOUT;
-  uint64_t container = 0, n = 0;
-  uint32_t chunks = 0;
-  for (int i = 0; i < 8; ++i) container |= static_cast<uint64_t>(h[i]) << (8 * i);
-  for (int i = 0; i < 8; ++i) n |= static_cast<uint64_t>(h[14 + i]) << (8 * i);
-  for (int i = 0; i < 4; ++i) chunks |= static_cast<uint32_t>(h[22 + i]) << (8 * i);
-  if (container < 18 || kFrameBytes + container - 18 > c->slot_bytes || std::memcmp(h + 8, "HCC1", 4) != 0 ||
-      h[12] != HCCX_CODEC_LOSSLESS || n != m || chunks != (m + kPredictorChunk - 1) / kPredictorChunk)
-    return HCCX_ERR_CORRUPT_PAYLOAD;
-  c->last_recv += container - 18;
-  return hccx_lossless_decompress(base + kFrameBytes, container - 18, m, out, s);
+  return msg_decode(host_slot(c, c->rank, cls, slot), c->slot_bytes, m, out, fold, c->d_err, c->ll_acct + 2, s);
 }
 
 // Consumption ack of slot (cls, slot) in `rank`'s window: every index, so
@@ -248,20 +196,21 @@ hccx_status_t ll_setup(LLRank& r, hccx_comm* c, int op, const float* in, float* 
   if (op == 0 || op == 1) {  // the ring folds into a work copy of the input
     float* w = out;
     if (op == 1) {
-      if (ensure(c->ll_work, c->ll_work_cap, n) != HCCX_OK) return HCCX_ERR_CUDA;
+      if (ensure(c->ll_work, c->ll_work_cap, n) != HCCX_OK) return HCCX_CUDA_FAIL;
       w = c->ll_work;
     }
-    if (w != in && cudaMemcpyAsync(w, in, 4 * n, cudaMemcpyDeviceToDevice, s) != cudaSuccess) return HCCX_ERR_CUDA;
+    if (w != in && cudaMemcpyAsync(w, in, 4 * n, cudaMemcpyDeviceToDevice, s) != cudaSuccess) return HCCX_CUDA_FAIL;
     r.work = w;
   }
-  if (op <= 2 && ensure(c->ll_tmp, c->ll_tmp_cap, r.chunk) != HCCX_OK) return HCCX_ERR_CUDA;
+  if (!c->ll_acct && cudaMalloc(&c->ll_acct, 4 * sizeof(unsigned long long)) != cudaSuccess) return HCCX_CUDA_FAIL;
+  if (cudaMemsetAsync(c->ll_acct, 0, 4 * sizeof(unsigned long long), s) != cudaSuccess) return HCCX_CUDA_FAIL;
   if (op >= 3 && (r.pp_root || r.pp_recv)) {  // message staging (root) / reassembly (receiver)
-    const uint64_t need = kFrameBytes + hccx_lossless_max_bytes(n);
+    const uint64_t need = msg_max_bytes(n);
     if (need > c->ll_stage_cap) {
       cudaFree(c->ll_stage);
       c->ll_stage = nullptr;
       c->ll_stage_cap = 0;
-      if (cudaMalloc(&c->ll_stage, need) != cudaSuccess) return HCCX_ERR_CUDA;
+      if (cudaMalloc(&c->ll_stage, need) != cudaSuccess) return HCCX_CUDA_FAIL;
       c->ll_stage_cap = need;
     }
   }
@@ -277,28 +226,27 @@ hccx_status_t ll_rs_send(LLRank& r, int t) {
   hccx_status_t st = credit(c, 3, t, r.prev_rs, r.s);
   if (st != HCCX_OK) return st;
   const int ch = ((j - 1 - t) % p + p) % p;
-  uint64_t bytes = 0;
-  st = send_frame(c, r.work + static_cast<uint64_t>(ch) * r.chunk, r.chunk, right, 0, t, r.s, &bytes);
+  st = send_frame(c, r.work + static_cast<uint64_t>(ch) * r.chunk, r.chunk, right, 0, t, r.s);
   if (st != HCCX_OK) return st;
   return signal(c, right, 0, t, 1, r.epoch, r.s);
 }
 
-// ... and its receive: acc(chunk j-2-t) = dec(msg) + acc, ack the left neighbour.
+// ... and its receive: acc(chunk j-2-t) = acc + dec(msg) in the decoder,
+// then ack the left neighbour.
 hccx_status_t ll_rs_recv(LLRank& r, int t) {
   hccx_comm* c = r.c;
   DeviceGuard guard(c->device);
   const int p = c->p, j = c->rank, left = (j + p - 1) % p;
-  hccx_status_t st = recv_frame(c, 0, t, r.epoch, r.chunk, c->ll_tmp, r.s);
-  if (st != HCCX_OK) return st;
   const int ch = ((j - 2 - t) % p + p) % p;
-  if (ll_fold(r.work + static_cast<uint64_t>(ch) * r.chunk, c->ll_tmp, r.chunk, r.s) != cudaSuccess)
-    return HCCX_ERR_CUDA;
+  hccx_status_t st = recv_frame(c, 0, t, r.epoch, r.chunk, r.work + static_cast<uint64_t>(ch) * r.chunk, true, r.s);
+  if (st != HCCX_OK) return st;
   return ack(c, left, 3, t, r.epoch, r.s);
 }
 
-// Allgather (collectives.cpp:77-107): the owner compresses its shard once
-// into its own (otherwise unused) ag[j] slot and copies the frame into every
-// peer's ag[j] slot -- each shard's payload crosses the wire p-1 times.
+// Allgather (collectives.cpp:77-107): the owner encodes its shard once
+// into its own (otherwise unused) ag[j] slot and one kernel copies the
+// message into every peer's ag[j] slot -- each shard's payload crosses the
+// wire p-1 times.
 hccx_status_t ll_ag_send(LLRank& r) {
   hccx_comm* c = r.c;
   DeviceGuard guard(c->device);
@@ -308,21 +256,18 @@ hccx_status_t ll_ag_send(LLRank& r) {
     const hccx_status_t st = credit(c, 4, (j + q) % p, r.prev_ag, r.s);
     if (st != HCCX_OK) return st;
   }
-  uint64_t bytes = 0;
-  hccx_status_t st = send_frame(c, shard, r.chunk, j, 1, j, r.s, &bytes);
+  uint8_t* own = host_slot(c, j, 1, j);
+  hccx_status_t st = msg_encode(shard, r.chunk, own, c->ll_msg, nullptr, r.s);  // local staging: not on the wire
   if (st != HCCX_OK) return st;
-  c->last_payload -= bytes;  // the local staging copy is not on the wire
-  c->last_frame -= kFrameBytes + bytes;
-  const uint8_t* frame = host_slot(c, j, 1, j);
-  for (int q = 1; q < p; ++q) {
-    const int d = (j + q) % p;
-    if ((st = copy_frame(c, frame, bytes, d, 1, j, r.s)) != HCCX_OK) return st;
-    if ((st = signal(c, d, 1, j, 1, r.epoch, r.s)) != HCCX_OK) return st;
-  }
+  uint8_t* dsts[kMaxRanks] = {};
+  for (int q = 1; q < p; ++q) dsts[q - 1] = host_slot(c, (j + q) % p, 1, j);
+  if ((st = msg_copy(own, r.chunk, dsts, p - 1, c->ll_acct, r.s)) != HCCX_OK) return st;
+  for (int q = 1; q < p; ++q)
+    if ((st = signal(c, (j + q) % p, 1, j, 1, r.epoch, r.s)) != HCCX_OK) return st;
   // the owner's own chunk: dec(comp(shard)) == shard
-  float* own = r.out + static_cast<uint64_t>(j) * r.chunk;
-  if (own != shard && cudaMemcpyAsync(own, shard, 4 * r.chunk, cudaMemcpyDeviceToDevice, r.s) != cudaSuccess)
-    return HCCX_ERR_CUDA;
+  float* mine = r.out + static_cast<uint64_t>(j) * r.chunk;
+  if (mine != shard && cudaMemcpyAsync(mine, shard, 4 * r.chunk, cudaMemcpyDeviceToDevice, r.s) != cudaSuccess)
+    return HCCX_CUDA_FAIL;
   return HCCX_OK;
 }
 
@@ -332,7 +277,7 @@ hccx_status_t ll_ag_recv(LLRank& r) {
   const int p = c->p, j = c->rank, left = (j + p - 1) % p;
   for (int q = 1; q < p; ++q) {
     const int i = (j - q + p) % p;
-    hccx_status_t st = recv_frame(c, 1, i, r.epoch, r.chunk, r.out + static_cast<uint64_t>(i) * r.chunk, r.s);
+    hccx_status_t st = recv_frame(c, 1, i, r.epoch, r.chunk, r.out + static_cast<uint64_t>(i) * r.chunk, false, r.s);
     if (st != HCCX_OK) return st;
     // ack to the owner (direct-gather credit) and to the left neighbour
     // (ring-gather credit), like the fused kernel's gather receives
@@ -351,16 +296,15 @@ hccx_status_t ll_pp_prepare(LLRank& r) {
   hccx_comm* c = r.c;
   if (!r.pp_root || r.n == 0) return HCCX_OK;
   DeviceGuard guard(c->device);
-  uint64_t bytes = 0;
-  hccx_status_t st = hccx_lossless_compress(r.in, r.n, c->ll_stage + kFrameBytes, c->ll_stage_cap - kFrameBytes,
-                                            &bytes, r.s);
+  hccx_status_t st = msg_encode(r.in, r.n, c->ll_stage, c->ll_msg, nullptr, r.s);
   if (st != HCCX_OK) return st;
-  ll_frame_kernel<<<1, 32, 0, r.s>>>(c->ll_stage, 18 + bytes, r.n,
-                                     static_cast<uint32_t>((r.n + kPredictorChunk - 1) / kPredictorChunk));
-  count_launch();
-  r.msg_bytes = kFrameBytes + bytes;
+  uint64_t container = 0;  // the message size decides the fragment count
+  if (cudaMemcpyAsync(&container, c->ll_stage, 8, cudaMemcpyDeviceToHost, r.s) != cudaSuccess ||
+      cudaStreamSynchronize(r.s) != cudaSuccess)
+    return HCCX_CUDA_FAIL;
+  r.msg_bytes = kMsgHeaderBytes + msg_index_bytes(r.n) + container - 18;
   r.nfrag = static_cast<uint32_t>((r.msg_bytes + c->slot_bytes - 1) / c->slot_bytes);
-  return launched();
+  return HCCX_OK;
 }
 
 // Fragment f: returns HCCX_OK and sets *active when this rank had work.
@@ -378,10 +322,11 @@ hccx_status_t ll_pp_send_frag(LLRank& r, uint32_t f, bool* active) {
     hccx_status_t st = credit(c, 5, d, r.frag_send[d] - 1, r.s);
     if (st != HCCX_OK) return st;
     if (cudaMemcpyAsync(host_slot(c, d, 2, j), c->ll_stage + off, len, cudaMemcpyDeviceToDevice, r.s) != cudaSuccess)
-      return HCCX_ERR_CUDA;
+      return HCCX_CUDA_FAIL;
     if ((st = signal(c, d, 2, j, 1, r.frag_send[d], r.s)) != HCCX_OK) return st;
     c->last_frame += len;
-    const uint64_t hdr_part = off < kFrameBytes ? (kFrameBytes - off < len ? kFrameBytes - off : len) : 0;
+    const uint64_t lead = kMsgHeaderBytes + msg_index_bytes(r.n);  // frame + index before the payload
+    const uint64_t hdr_part = off < lead ? (lead - off < len ? lead - off : len) : 0;
     c->last_payload += len - hdr_part;
   }
   return HCCX_OK;
@@ -402,36 +347,34 @@ hccx_status_t ll_pp_recv_frag(LLRank& r, uint32_t f, bool* active) {
     if (cudaMemcpyAsync(h, host_slot(c, c->rank, 2, r.root), 26, cudaMemcpyDeviceToHost, r.s) != cudaSuccess ||
         cudaMemcpyAsync(&err, c->d_err, 4, cudaMemcpyDeviceToHost, r.s) != cudaSuccess ||
         cudaStreamSynchronize(r.s) != cudaSuccess)
-      return HCCX_ERR_CUDA;
+      return HCCX_CUDA_FAIL;
     if (err & kErrTimeout) return HCCX_ERR_TIMEOUT;
     uint64_t container = 0, n = 0;
     uint32_t chunks = 0;
     for (int i = 0; i < 8; ++i) container |= static_cast<uint64_t>(h[i]) << (8 * i);
     for (int i = 0; i < 8; ++i) n |= static_cast<uint64_t>(h[14 + i]) << (8 * i);
     for (int i = 0; i < 4; ++i) chunks |= static_cast<uint32_t>(h[22 + i]) << (8 * i);
-    if (container < 18 || kFrameBytes + container - 18 > c->ll_stage_cap || std::memcmp(h + 8, "HCC1", 4) != 0 ||
-        h[12] != HCCX_CODEC_LOSSLESS || n != r.n || chunks != (r.n + kPredictorChunk - 1) / kPredictorChunk)
+    r.msg_bytes = kMsgHeaderBytes + msg_index_bytes(r.n) + container - 18;
+    if (container < 18 || r.msg_bytes + 16 > c->ll_stage_cap || std::memcmp(h + 8, "HCC1", 4) != 0 ||
+        h[12] != HCCX_CODEC_LOSSLESS || n != r.n || chunks != msg_chunks(r.n))
       return HCCX_ERR_CORRUPT_PAYLOAD;
-    r.msg_bytes = kFrameBytes + container - 18;
     r.nfrag = static_cast<uint32_t>((r.msg_bytes + c->slot_bytes - 1) / c->slot_bytes);
   }
   const uint64_t len = r.msg_bytes - off < c->slot_bytes ? r.msg_bytes - off : c->slot_bytes;
   if (cudaMemcpyAsync(c->ll_stage + off, host_slot(c, c->rank, 2, r.root), len, cudaMemcpyDeviceToDevice, r.s) !=
       cudaSuccess)
-    return HCCX_ERR_CUDA;
+    return HCCX_CUDA_FAIL;
   return ack(c, r.root, 5, c->rank, r.frag_recv, r.s);
 }
 
 hccx_status_t ll_pp_complete(LLRank& r) {
   hccx_comm* c = r.c;
   DeviceGuard guard(c->device);
-  if (r.pp_recv && r.n) {
-    c->last_recv = r.msg_bytes - kFrameBytes;
-    return hccx_lossless_decompress(c->ll_stage + kFrameBytes, r.msg_bytes - kFrameBytes, r.n, r.out, r.s);
-  }
+  if (r.pp_recv && r.n)
+    return msg_decode(c->ll_stage, c->ll_stage_cap, r.n, r.out, false, c->d_err, c->ll_acct + 2, r.s);
   if (r.pp_root && r.op == 3 && r.out && r.out != r.in && r.n &&
       cudaMemcpyAsync(r.out, r.in, 4 * r.n, cudaMemcpyDeviceToDevice, r.s) != cudaSuccess)
-    return HCCX_ERR_CUDA;
+    return HCCX_CUDA_FAIL;
   return HCCX_OK;
 }
 
@@ -441,7 +384,7 @@ hccx_status_t ll_finish(LLRank& r, const StepParams& div) {
   if (r.op == 1) {  // reduce-scatter: this rank's reduced chunk
     if (cudaMemcpyAsync(r.out, r.work + static_cast<uint64_t>(c->rank) * r.chunk, 4 * r.chunk,
                         cudaMemcpyDeviceToDevice, r.s) != cudaSuccess)
-      return HCCX_ERR_CUDA;
+      return HCCX_CUDA_FAIL;
   }
   if (r.op == 0 && div.div_mode != 0) {  // Average: IEEE v / float(p) after the gather (collectives.cpp:234-239)
     ll_scale_kernel<<<148 * 4, 256, 0, r.s>>>(r.out, r.n, div.div_mode, div.recip, div.divisor);
@@ -449,6 +392,27 @@ hccx_status_t ll_finish(LLRank& r, const StepParams& div) {
     return launched();
   }
   return HCCX_OK;
+}
+
+// The collective's one host synchronisation: device-side byte accounting
+// and error flags (timeouts, corrupt messages) of every rank.
+hccx_status_t ll_settle(std::vector<LLRank>& ranks, hccx_status_t st) {
+  for (LLRank& r : ranks) {
+    hccx_comm* c = r.c;
+    if (!c || !c->ll_acct) continue;
+    DeviceGuard guard(c->device);
+    unsigned long long a[4] = {};
+    if (cudaMemcpyAsync(a, c->ll_acct, sizeof a, cudaMemcpyDeviceToHost, r.s) != cudaSuccess) {
+      if (st == HCCX_OK) st = HCCX_ERR_CUDA;
+      continue;
+    }
+    const hccx_status_t fl = read_flag(c->d_err, r.s);  // synchronises the stream first
+    c->last_payload += a[0];
+    c->last_frame += a[1];
+    c->last_recv += a[2];
+    if (st == HCCX_OK) st = fl;
+  }
+  return st;
 }
 
 // Runs the stages of every rank in `ranks` in lockstep (one rank for a
@@ -513,7 +477,7 @@ hccx_status_t ll_collective(hccx_comm* const* comms, int nr, int op, const float
         DeviceGuard guard(comms[k]->device);
         if (n && out[k] != in[k] &&
             cudaMemcpyAsync(out[k], in[k], 4 * n, cudaMemcpyDeviceToDevice, streams[k]) != cudaSuccess)
-          return HCCX_ERR_CUDA;
+          return HCCX_CUDA_FAIL;
       }
       return HCCX_OK;
     }
@@ -524,7 +488,7 @@ hccx_status_t ll_collective(hccx_comm* const* comms, int nr, int op, const float
       const hccx_status_t st = ll_setup(ranks[k], comms[k], op, in[k], out[k], n, mode, root, dst, streams[k]);
       if (st != HCCX_OK) return st;
     }
-    return ll_run(ranks, div);
+    return ll_settle(ranks, ll_run(ranks, div));
   }
   // broadcast / p2p: one message in fragments (ll_pp_*)
   std::vector<LLRank> ranks(nr);
@@ -532,7 +496,7 @@ hccx_status_t ll_collective(hccx_comm* const* comms, int nr, int op, const float
     const hccx_status_t st = ll_setup(ranks[k], comms[k], op, in[k], out[k], n, mode, root, dst, streams[k]);
     if (st != HCCX_OK) return st;
   }
-  return ll_run(ranks, div);
+  return ll_settle(ranks, ll_run(ranks, div));
 }
 
 }  // namespace hccx

@@ -238,6 +238,25 @@ def test_single_process_multi_gpu(cuda, env, layout):
     got, st = m.p2p(x, "fixed-rate", 8, 0, p - 1)
     assert st == 0
     assert got.tobytes() == O.p2p(x, "fixed-rate", 8)[0].tobytes()
+    # LosslessPredictor framed messages across devices (per-device kernel
+    # attributes, peer-window encodes)
+    for n_per in (1000, 4096 * 3 + 17):
+        x = _inputs(n_per + 3, p, n_per * p)
+        got, st = m.allreduce(x, "lossless", 0)
+        assert st == 0
+        want, _ = O.allreduce(x, "lossless", 0)
+        assert got.tobytes() == want.tobytes(), (layout, n_per)
+        s = np.ascontiguousarray(x[:, :n_per])
+        got, st = m.allgather(s, "lossless")
+        assert st == 0
+        assert got.tobytes() == O.allgather(s, "lossless")[0].tobytes()
+        v = np.ascontiguousarray(x[0])
+        got, st = m.broadcast(v, p - 1, "lossless")
+        assert st == 0
+        assert got.tobytes() == O.broadcast(v, p, "lossless")[0].tobytes()
+        got, st = m.p2p(v, "lossless", 0, p - 1, 0)
+        assert st == 0
+        assert got.tobytes() == O.p2p(v, "lossless")[0].tobytes()
 
 
 @pytest.mark.parametrize("p", [2, 3, 4])

@@ -176,3 +176,61 @@ def H_identity():
     import paper_2409_02423_b200 as H
 
     return H.CodecSpec.identity()
+
+
+@pytest.mark.parametrize("n", [1, 4095, 4096, 4097, 3 * 4096 + 17, 1 << 18])
+@pytest.mark.parametrize("mode", ["bits", "sparse", "normal", "smooth"])
+def test_frame_messages(cuda, n, mode):
+    """The communicator's framed message (lossless_msg.h): payload section
+    byte-identical to the oracle (= hcc::compress), HCC1 header fields, exact
+    decode, folded decode (acc + value, IEEE), and the device-side checks
+    (hcc::from_bytes' magic / lengths, index vs payload) -> CORRUPT."""
+    import torch
+
+    from paper_2409_02423_b200 import _lib
+
+    if mode == "smooth":
+        x = np.cumsum(O.fill(n + 5, "normal", n, 1e-3, 1.0)).astype(np.float32)
+    else:
+        x = O.fill(n * 3 + len(mode), mode, n, {"sparse": 0.9, "normal": 1e-3}.get(mode, -1.0), 1.0)
+    want = O.pred_compress(x)
+    cap = int(_lib.hccx_lossless_frame_max_bytes(n))
+    msg = torch.zeros(cap, dtype=torch.uint8, device="cuda")
+    xd = torch.from_numpy(x).cuda()
+    assert _lib.hccx_lossless_frame_encode(xd.data_ptr(), n, msg.data_ptr(), cap, None) == 0
+    m = msg.cpu().numpy()
+    nch = (n + 4095) // 4096
+    ib = (68 * nch + 15) // 16 * 16
+    container = int(m[:8].view(np.uint64)[0])
+    assert container == 18 + want.size
+    assert m[8:12].tobytes() == b"HCC1" and m[12] == 1 and m[13] == 0
+    assert int(m[14:22].view(np.uint64)[0]) == n and int(m[22:26].view(np.uint32)[0]) == nch
+    assert m[32 + ib:32 + ib + want.size].tobytes() == want.tobytes()
+    out = torch.empty(n, dtype=torch.float32, device="cuda")
+    assert _lib.hccx_lossless_frame_decode(msg.data_ptr(), cap, n, out.data_ptr(), 0, None) == 0
+    assert _lib.hccx_frame_status(None) == 0
+    assert out.cpu().numpy().tobytes() == x.tobytes()
+    if mode != "bits":  # (NaN payloads are not IEEE-specified through an add)
+        acc = O.fill(n + 11, "normal", n, 1.0, 1.0)
+        acc_d = torch.from_numpy(acc).cuda()
+        assert _lib.hccx_lossless_frame_decode(msg.data_ptr(), cap, n, acc_d.data_ptr(), 1, None) == 0
+        assert _lib.hccx_frame_status(None) == 0
+        assert acc_d.cpu().numpy().tobytes() == (acc + x).astype(np.float32).tobytes()
+    # corruptions: each must be reported, never hang or fault
+    bad = []
+    b = m.copy(); b[9] = ord("X"); bad.append(b)                                 # magic
+    b = m.copy(); b[14:22] = np.array([n + 1], np.uint64).view(np.uint8); bad.append(b)  # original_len
+    b = m.copy(); b[:8] = np.array([cap * 2], np.uint64).view(np.uint8); bad.append(b)   # container > capacity
+    if nch > 1:
+        b = m.copy(); b[32 + 68:32 + 72] = np.array([container * 4], np.uint32).view(np.uint8); bad.append(b)
+    coded = [c for c in range(nch) if not (want[c // 8] >> (c % 8)) & 1]
+    if coded:
+        c = coded[0]
+        b = m.copy()
+        lane0 = 32 + 68 * c + 4
+        b[lane0:lane0 + 2] = (np.frombuffer(b[lane0:lane0 + 2].tobytes(), np.uint16) + 8).view(np.uint8)
+        bad.append(b)
+    for b in bad:
+        bm = torch.from_numpy(b).cuda()
+        assert _lib.hccx_lossless_frame_decode(bm.data_ptr(), cap, n, out.data_ptr(), 0, None) == 0
+        assert _lib.hccx_frame_status(None) == 2  # HCCX_ERR_CORRUPT_PAYLOAD
