@@ -749,20 +749,14 @@ extern "C" hccx_status_t hccx_lossless_ring_hops_host(const float* const* h_in, 
 namespace hccx {
 namespace {
 
-constexpr uint32_t kMsgLaneStride = kLaneVals + 1;  // 129: conflict-free lane-major staging
-constexpr size_t kMsgDecodeSmem = sizeof(uint32_t) * kLLWarps * (32 * kMsgLaneStride + 32);
-
 __device__ __forceinline__ uint64_t ld_le64(const uint8_t* p) {
   uint64_t v = 0;
   for (int k = 0; k < 8; ++k) v |= static_cast<uint64_t>(p[k]) << (8 * k);
   return v;
 }
 
-// The frame (lossless_msg.h): u64 container bytes + HCC1 header.
-__global__ void msg_header_kernel(uint8_t* msg, const uint64_t* __restrict__ offsets, uint64_t nch, uint64_t n,
-                                  uint64_t idx_bytes, unsigned long long* acct) {
-  if (threadIdx.x != 0) return;
-  const uint64_t payload = offsets[nch];
+__device__ void write_frame(uint8_t* msg, uint64_t payload, uint64_t n, uint64_t nch, uint64_t idx_bytes,
+                            unsigned long long* acct) {
   const uint64_t container = 18 + payload;
   uint8_t h[26];
   for (int i = 0; i < 8; ++i) h[i] = static_cast<uint8_t>(container >> (8 * i));
@@ -775,6 +769,257 @@ __global__ void msg_header_kernel(uint8_t* msg, const uint64_t* __restrict__ off
   if (acct) {
     atomicAdd(acct, static_cast<unsigned long long>(payload));
     atomicAdd(acct + 1, static_cast<unsigned long long>(kMsgHeaderBytes + idx_bytes + payload));
+  }
+}
+
+// The frame of an empty message (n = 0).
+__global__ void msg_header_kernel(uint8_t* msg, uint64_t* total, unsigned long long* acct) {
+  if (threadIdx.x != 0) return;
+  *total = 0;
+  write_frame(msg, 0, 0, 0, 0, acct);
+}
+
+// ---- single-pass encoder ---------------------------------------------------
+// One CTA per 4096-value chunk, chunks taken in ticket order.  The chunk is
+// staged into shared memory by one bulk copy (TMA engine); each of the 256
+// threads then owns 16 consecutive values (the predecessor of its first one
+// is in shared memory too), counts their code bits, and a block-wide scan
+// gives every thread its bit offset and the chunk its size -- so a raw
+// fallback (codec_kernels.hpp:190-194) is known before anything is coded.
+// Coded chunks: every thread writes its codes into a shared-memory copy of
+// the chunk stream (whole words plain, the two words it may share with its
+// neighbours by atomicOr).  The chunk's size is published, its byte offset
+// found by a decoupled look-back over the predecessors' descriptors (warp
+// 0), and the CTA writes the chunk, its index entry, the raw-flag byte of its
+// group of 8 and (last chunk) the frame.
+constexpr int kEncThreads = 256;
+constexpr int kEncVals = kChunk / kEncThreads;  // 16
+constexpr uint32_t kEncStreamWords = kChunk + 8;  // a coded chunk is < 4096 words
+constexpr size_t kEncSmem = sizeof(uint32_t) * (kChunk + kEncStreamWords + 64);
+
+// descriptor: epoch (24) | status (2: 1 aggregate, 2 inclusive prefix) | raw flag (1) | value (37).
+// Self-contained (no other data is published through it): relaxed accesses.
+constexpr uint64_t kDescValMask = (1ull << 37) - 1;
+__device__ __forceinline__ uint64_t desc_make(uint32_t epoch, uint32_t status, uint32_t fb, uint64_t v) {
+  return (static_cast<uint64_t>(epoch & 0xffffffu) << 40) | (static_cast<uint64_t>(status) << 38) |
+         (static_cast<uint64_t>(fb) << 37) | (v & kDescValMask);
+}
+__device__ __forceinline__ void st_relaxed_gpu_u64(uint64_t* p, uint64_t v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_relaxed_gpu_u64(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+// Spin until descriptor j of this epoch is published; returns it.
+__device__ __forceinline__ uint64_t desc_wait(const uint64_t* desc, uint64_t j, uint32_t epoch) {
+  uint64_t d = ld_relaxed_gpu_u64(desc + j);
+  while (static_cast<uint32_t>(d >> 40) != (epoch & 0xffffffu) || ((d >> 38) & 3u) == 0) {
+    __nanosleep(20);
+    d = ld_relaxed_gpu_u64(desc + j);
+  }
+  return d;
+}
+
+__device__ __forceinline__ uint64_t warp_sum_u64(uint64_t v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+  return v;
+}
+
+// Exclusive byte offset of chunk c: `base` (the flag bytes) + the sizes of
+// chunks 0..c-1, from the nearest inclusive prefix back (one warp).
+__device__ uint64_t lookback(const uint64_t* desc, uint64_t c, uint32_t epoch, uint64_t base, int lane) {
+  uint64_t excl = 0;
+  int64_t pred = static_cast<int64_t>(c) - 1;
+  while (true) {
+    const int64_t j = pred - lane;
+    uint32_t status = 2;
+    uint64_t val = base;
+    if (j >= 0) {
+      const uint64_t d = desc_wait(desc, static_cast<uint64_t>(j), epoch);
+      status = static_cast<uint32_t>((d >> 38) & 3u);
+      val = d & kDescValMask;
+    }
+    const uint32_t pmask = __ballot_sync(kFull, status == 2);
+    const int firstp = pmask ? __ffs(pmask) - 1 : 32;
+    excl += warp_sum_u64(lane <= firstp ? val : 0ull);
+    if (pmask) return excl;
+    pred -= 32;
+  }
+}
+
+// Byte copy of `len` bytes from a word-aligned source to an arbitrary
+// global byte offset by a whole CTA (interior words funnel-shifted).
+__device__ void copy_out_cta(const uint32_t* src, uint8_t* dst, uint32_t len, int tid, int nt) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(dst);
+  const uint32_t h4 = static_cast<uint32_t>((4 - (a & 3)) & 3);
+  const uint32_t head = h4 < len ? h4 : len;
+  const uint8_t* sb = reinterpret_cast<const uint8_t*>(src);
+  for (uint32_t b = tid; b < head; b += nt) dst[b] = sb[b];
+  const uint32_t nw = (len - head) / 4;
+  uint32_t* dw = reinterpret_cast<uint32_t*>(dst + head);
+  for (uint32_t w = tid; w < nw; w += nt) {
+    const uint32_t byte = head + 4 * w;
+    const uint32_t lo = src[byte >> 2], hi = (byte & 3) ? src[(byte >> 2) + 1] : 0u;
+    dw[w] = __funnelshift_r(lo, hi, 8 * (byte & 3));
+  }
+  for (uint32_t b = head + 4 * nw + tid; b < len; b += nt) dst[b] = sb[b];
+}
+
+__global__ void __launch_bounds__(kEncThreads) ll_encode_kernel(const float* __restrict__ in, uint64_t n, uint64_t nch,
+                                                                int vec_ok, uint8_t* __restrict__ pay,
+                                                                uint32_t* __restrict__ index, uint8_t* msg,
+                                                                uint64_t idx_bytes, uint64_t* desc, uint32_t epoch,
+                                                                uint64_t* total, unsigned long long* tickets,
+                                                                unsigned long long* acct) {
+  extern __shared__ __align__(16) uint32_t esm[];
+  uint32_t* xin = esm;                       // the chunk's values
+  uint32_t* sm = xin + kChunk;               // its code stream
+  uint32_t* misc = sm + kEncStreamWords;     // 64 words: warp totals, block bits, broadcast slots, mbarrier
+  uint32_t* wtot = misc;                     // [8]
+  uint32_t* blk = misc + 8;                  // [32] bits per 128-value block (the index's lane counts)
+  uint64_t* bcast = reinterpret_cast<uint64_t*>(misc + 40);  // [0] ticket, [1] offset
+  uint64_t* bar = reinterpret_cast<uint64_t*>(misc + 48);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  uint32_t phase = 0;
+  const uint64_t flag_bytes = (nch + 7) / 8;
+  for (;;) {
+    // chunks in ticket order: a CTA holds chunk c only after chunks < c were
+    // taken by running CTAs, so the look-back cannot wait on an unscheduled one
+    if (tid == 0) bcast[0] = atomicAdd(tickets, 1ull);
+    __syncthreads();
+    const uint64_t c = bcast[0];
+    if (c >= nch) {  // the last CTA out resets the counters for the next call
+      if (tid == 0 && atomicAdd(tickets + 1, 1ull) == gridDim.x - 1ull) {
+        tickets[0] = 0;
+        tickets[1] = 0;
+      }
+      break;
+    }
+    const uint64_t base = c * kChunk;
+    const uint32_t live = static_cast<uint32_t>(n - base < kChunk ? n - base : kChunk);
+    const uint32_t* x = reinterpret_cast<const uint32_t*>(in) + base;
+    // stage the chunk: one bulk copy of its 16-byte multiple, the tail by hand
+    const uint32_t bulk = vec_ok ? (4 * live) & ~15u : 0u;
+    if (bulk && tid == 0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_arrive_expect_tx(bar, bulk);
+      bulk_g2s(xin, x, bulk, bar);
+    }
+    for (uint32_t k = bulk / 4 + tid; k < live; k += kEncThreads) xin[k] = __ldg(x + k);
+    if (bulk) {
+      mbar_wait(bar, phase);
+      phase ^= 1;
+    }
+    __syncthreads();
+    // count: this thread's 16 values
+    const uint32_t i0 = tid * kEncVals;
+    const uint32_t nv = i0 >= live ? 0u : min(static_cast<uint32_t>(kEncVals), live - i0);
+    // values as 4 x 128-bit shared loads (a full chunk; the tail chunk reads
+    // zeros past `live`, which the counts below ignore)
+    uint32_t xv[kEncVals];
+#pragma unroll
+    for (int q = 0; q < kEncVals / 4; ++q) {
+      const uint4 t4 = *reinterpret_cast<const uint4*>(xin + i0 + 4 * q);
+      xv[4 * q] = t4.x, xv[4 * q + 1] = t4.y, xv[4 * q + 2] = t4.z, xv[4 * q + 3] = t4.w;
+    }
+    const uint32_t before = i0 && i0 <= live ? xin[i0 - 1] : 0u;
+    uint32_t bits = 0;
+#pragma unroll
+    for (int k = 0; k < kEncVals; ++k) {
+      const uint32_t r = xv[k] ^ (k ? xv[k - 1] : before);
+      bits += static_cast<uint32_t>(k) < nv ? 37u - min(__clz(r), 31) : 0u;
+    }
+    uint32_t incl = bits;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t t = __shfl_up_sync(kFull, incl, d);
+      if (lane >= d) incl += t;
+    }
+    // bits per 128-value block = 8 consecutive threads
+    const uint32_t end8 = __shfl_sync(kFull, incl, (lane & ~7) + 7);
+    const uint32_t beg8 = __shfl_sync(kFull, incl - bits, lane & ~7);
+    if ((lane & 7) == 0) blk[warp * 4 + (lane >> 3)] = end8 - beg8;
+    if (lane == 31) wtot[warp] = incl;
+    __syncthreads();
+    uint32_t wbase = 0, chunk_bits = 0;
+#pragma unroll
+    for (int w = 0; w < kEncThreads / 32; ++w) {
+      const uint32_t t = wtot[w];
+      wbase += w < warp ? t : 0u;
+      chunk_bits += t;
+    }
+    const uint32_t fb = chunk_bits >= 32u * live ? 1u : 0u;
+    const uint64_t size = fb ? 4ull * live : (chunk_bits + 7) / 8;
+    if (!fb) {
+      const uint32_t words = (chunk_bits + 31) / 32;
+      for (uint32_t w = tid; w < words; w += kEncThreads) sm[w] = 0;
+      __syncthreads();
+      const uint32_t pos = wbase + incl - bits;
+      uint64_t acc = 0;
+      uint32_t fill = pos & 31, wi = pos >> 5;
+      const uint32_t first_word = wi;
+      auto put = [&](uint32_t val, uint32_t nb) {
+        acc |= static_cast<uint64_t>(val) << fill;
+        fill += nb;
+        if (fill >= 32) {
+          const uint32_t wv = static_cast<uint32_t>(acc);
+          if (wi == first_word) atomicOr(&sm[wi], wv);  // shared with the previous thread
+          else sm[wi] = wv;
+          ++wi;
+          acc >>= 32;
+          fill -= 32;
+        }
+      };
+#pragma unroll
+      for (int k = 0; k < kEncVals; ++k) {
+        if (static_cast<uint32_t>(k) < nv) {
+          const uint32_t r = xv[k] ^ (k ? xv[k - 1] : before);
+          const uint32_t z = min(__clz(r), 31);
+          put(z, 5);
+          const uint32_t nb = 32 - z;
+          put(nb == 32 ? r : (r & ((1u << nb) - 1u)), nb);
+        }
+      }
+      if (fill > 0 && bits) atomicOr(&sm[wi], static_cast<uint32_t>(acc));  // may be shared with the next thread
+    }
+    // publish, look back, publish the inclusive prefix
+    if (warp == 0) {
+      if (lane == 0) st_relaxed_gpu_u64(desc + c, desc_make(epoch, c == 0 ? 2u : 1u, fb, c == 0 ? flag_bytes + size : size));
+      const uint64_t off = c == 0 ? flag_bytes : lookback(desc, c, epoch, flag_bytes, lane);
+      if (lane == 0) {
+        if (c != 0) st_relaxed_gpu_u64(desc + c, desc_make(epoch, 2u, fb, off + size));
+        bcast[1] = off;
+      }
+    }
+    __syncthreads();
+    const uint64_t off = bcast[1];
+    copy_out_cta(fb ? xin : sm, pay + off, static_cast<uint32_t>(size), tid, kEncThreads);
+    if (index && tid < static_cast<int>(kMsgIndexWords)) {
+      uint32_t* ix = index + kMsgIndexWords * c;
+      ix[tid] = tid == 0 ? static_cast<uint32_t>(off)
+                         : (fb ? 0u : (blk[2 * (tid - 1)] | (blk[2 * (tid - 1) + 1] << 16)));
+    }
+    // raw-flag byte of chunks 8k..8k+7 (codec_serial.cpp:63), by the group's last chunk
+    if (warp == 1 && ((c & 7) == 7 || c == nch - 1)) {
+      const uint64_t j = (c & ~7ull) + lane;
+      uint32_t bit = 0;
+      if (lane < 8 && j <= c) bit = j == c ? fb : static_cast<uint32_t>((desc_wait(desc, j, epoch) >> 37) & 1u);
+      const uint32_t byte = __ballot_sync(kFull, bit != 0) & 0xffu;
+      if (lane == 0) pay[c / 8] = static_cast<uint8_t>(byte);
+    }
+    if (c == nch - 1 && tid == 0) {
+      *total = off + size;
+      if (msg) write_frame(msg, off + size, n, nch, idx_bytes, acct);
+    }
+    __syncthreads();
   }
 }
 
@@ -800,29 +1045,39 @@ __global__ void msg_copy_kernel(const uint8_t* __restrict__ src, MsgDsts D, uint
   }
 }
 
-// 4 bytes at an arbitrary byte offset of a 4-byte aligned buffer (may read
-// up to 3 bytes past the value: msg_max_bytes' slack).
-__device__ __forceinline__ uint32_t ld_u32_at(const uint8_t* base, uint64_t a) {
-  const uint32_t* q = reinterpret_cast<const uint32_t*>(base);
-  const uint32_t lo = q[a >> 2];
-  const uint32_t sh = static_cast<uint32_t>(a & 3);
-  return sh ? __funnelshift_r(lo, q[(a >> 2) + 1], 8 * sh) : lo;
-}
+// ---- decoder -----------------------------------------------------------------
+// One warp per chunk.  The chunk's bytes (and, folding, the accumulator's
+// 16 KiB) are staged into shared memory by bulk copies (TMA engine); raw
+// chunks are written from there; coded chunks are decoded by 32 lanes from
+// their indexed bit positions (128 codes each) into lane-major shared memory,
+// the lanes' XOR carries are scanned (x_i = x_{i-1} ^ r_i within a chunk),
+// the warp assembles the chunk (+ accumulator) contiguously and one bulk
+// store writes it out.  Unaligned outputs take plain loads and stores.
+constexpr int kDecWarps = 2;
+constexpr uint32_t kDecInWords = kChunk + 12;       // 16 KiB + alignment head/tail
+constexpr uint32_t kMsgLaneStride = kLaneVals + 1;  // 129: conflict-free lane-major staging
+constexpr uint32_t kDecWarpWords = kDecInWords + 32 * kMsgLaneStride + kChunk + 32 + 4;
+constexpr size_t kMsgDecodeSmem = sizeof(uint32_t) * kDecWarps * kDecWarpWords;
+static_assert(kDecWarpWords % 4 == 0, "16-byte aligned per-warp regions");
 
-// Decode: one warp per chunk.  Raw chunks are copied; coded chunks are
-// decoded by 32 lanes from their indexed bit positions (128 codes each) into
-// lane-major shared memory, the lanes' XOR carries are scanned (the
-// predictor is x_i = x_{i-1} ^ r_i within a chunk), and the warp writes the
-// chunk out coalesced, folding into `out` when asked.
-__global__ void __launch_bounds__(kLLWarps * 32) msg_decode_kernel(const uint8_t* __restrict__ msg, uint64_t msg_cap,
-                                                                   uint64_t n, uint64_t nch, uint64_t idx_bytes,
-                                                                   float* __restrict__ out, int fold,
-                                                                   uint32_t* __restrict__ err,
-                                                                   unsigned long long* recv_acct) {
-  extern __shared__ uint32_t msm[];
+__global__ void __launch_bounds__(kDecWarps * 32) msg_decode_kernel(const uint8_t* __restrict__ msg, uint64_t msg_cap,
+                                                                    uint64_t n, uint64_t nch, uint64_t idx_bytes,
+                                                                    float* __restrict__ out, int fold,
+                                                                    uint32_t* __restrict__ err,
+                                                                    unsigned long long* recv_acct) {
+  extern __shared__ __align__(16) uint32_t msm[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint32_t* sm = msm + warp * (32 * kMsgLaneStride + 32);
-  uint32_t* carry = sm + 32 * kMsgLaneStride;
+  uint32_t* ins = msm + warp * kDecWarpWords;
+  uint32_t* sm = ins + kDecInWords;            // lane-major decoded values
+  uint32_t* io = sm + 32 * kMsgLaneStride;     // contiguous chunk: accumulator in, values out
+  uint32_t* carry = io + kChunk;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(carry + 32);
+  if (lane == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+  uint32_t phase = 0;
   // frame checks (hcc::from_bytes, codec.cpp:101-121)
   const uint64_t container = *reinterpret_cast<const uint64_t*>(msg);
   const uint64_t flag_bytes = (nch + 7) / 8;
@@ -839,133 +1094,178 @@ __global__ void __launch_bounds__(kLLWarps * 32) msg_decode_kernel(const uint8_t
   const uint32_t* idx = reinterpret_cast<const uint32_t*>(msg + kMsgHeaderBytes);
   const uint8_t* pay = msg + kMsgHeaderBytes + idx_bytes;
   uint32_t* o32 = reinterpret_cast<uint32_t*>(out);
+  const bool out_al = (reinterpret_cast<uintptr_t>(out) & 15) == 0;
+  const uint64_t* in64 = reinterpret_cast<const uint64_t*>(ins);
   bool bad = false;
-  for (uint64_t c = static_cast<uint64_t>(blockIdx.x) * kLLWarps + warp; c < nch;
-       c += static_cast<uint64_t>(gridDim.x) * kLLWarps) {
+  for (uint64_t c = static_cast<uint64_t>(blockIdx.x) * kDecWarps + warp; c < nch;
+       c += static_cast<uint64_t>(gridDim.x) * kDecWarps) {
     const uint64_t base = c * kChunk;
     const uint32_t live = static_cast<uint32_t>(n - base < kChunk ? n - base : kChunk);
     const uint32_t* e = idx + kMsgIndexWords * c;
     const uint64_t off = e[0];
     const uint64_t end = c + 1 < nch ? idx[kMsgIndexWords * (c + 1)] : payload;
-    if (off < flag_bytes || end < off || end > payload) {
+    const bool raw = (pay[c / 8] >> (c % 8)) & 1u;
+    if (off < flag_bytes || end < off || end > payload || end - off > 4ull * live || (raw && end - off != 4ull * live)) {
       bad = true;
       break;
     }
-    if ((pay[c / 8] >> (c % 8)) & 1u) {  // raw chunk
-      if (end - off != 4ull * live) {
+    // stage [off & ~15, end) rounded up to 16 bytes, and the accumulator
+    const uint64_t a0 = off & ~15ull;
+    const uint32_t in_bytes = static_cast<uint32_t>((end - a0 + 15) & ~15ull);
+    const uint32_t acc_bulk = fold && out_al ? (4 * live) & ~15u : 0u;
+    if (lane == 0) bulk_wait_read<0>();  // the previous chunk's store has read io
+    __syncwarp();
+    if (lane == 0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_arrive_expect_tx(bar, in_bytes + acc_bulk);
+      bulk_g2s(ins, pay + a0, in_bytes, bar);
+      if (acc_bulk) bulk_g2s(io, out + base, acc_bulk, bar);
+    }
+    if (fold)
+      for (uint32_t k = acc_bulk / 4 + lane; k < live; k += 32) io[k] = o32[base + k];
+    mbar_wait(bar, phase);
+    phase ^= 1;
+    const uint32_t head = static_cast<uint32_t>(off - a0);  // bytes
+    if (raw) {
+      for (uint32_t k = lane; k < live; k += 32) {
+        const uint32_t b = head + 4 * k;
+        const uint32_t lo = ins[b >> 2];
+        const uint32_t v = (b & 3) ? __funnelshift_r(lo, ins[(b >> 2) + 1], 8 * (b & 3)) : lo;
+        io[k] = fold ? __float_as_uint(__fadd_rn(__uint_as_float(io[k]), __uint_as_float(v))) : v;
+      }
+    } else {
+      const uint32_t mybits = (e[1 + lane / 2] >> (16 * (lane & 1))) & 0xffffu;
+      uint32_t incl = mybits;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t t = __shfl_up_sync(kFull, incl, d);
+        if (lane >= d) incl += t;
+      }
+      const uint32_t total = __shfl_sync(kFull, incl, 31);
+      if ((total + 7ull) / 8 != end - off) {
         bad = true;
         break;
       }
+      const uint32_t i0 = lane * kLaneVals, i1 = min(live, i0 + kLaneVals);
+      uint32_t bit = 8 * head + (incl - mybits);  // within the staged bytes
+      const uint32_t bit0 = bit;
+      uint32_t wi = bit >> 6;
+      uint64_t lo = in64[wi], hi = in64[wi + 1];
+      uint32_t prev = 0;
+      for (uint32_t i = i0; i < i1; ++i) {
+        const uint32_t w = bit >> 6;
+        if (w != wi) {
+          lo = w == wi + 1 ? hi : in64[w];
+          hi = in64[w + 1];
+          wi = w;
+        }
+        const uint32_t sh = bit & 63;
+        const uint64_t win = sh ? (lo >> sh) | (hi << (64 - sh)) : lo;
+        const uint32_t nb = 32 - static_cast<uint32_t>(win & 31u);
+        const uint32_t low = static_cast<uint32_t>(win >> 5) & (nb >= 32 ? 0xffffffffu : ((1u << nb) - 1u));
+        bit += 5 + nb;
+        prev ^= low;
+        sm[lane * kMsgLaneStride + (i - i0)] = prev;
+      }
+      const bool lane_bad = bit - bit0 != mybits;
+      // exclusive XOR scan of the lanes' totals -> each lane's carry
+      uint32_t x = prev;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t t = __shfl_up_sync(kFull, x, d);
+        if (lane >= d) x ^= t;
+      }
+      carry[lane] = x ^ prev;
+      if (__any_sync(kFull, lane_bad)) {
+        bad = true;
+        break;
+      }
+      __syncwarp();
       for (uint32_t k = lane; k < live; k += 32) {
-        const uint32_t v = ld_u32_at(pay, off + 4ull * k);
-        o32[base + k] = fold ? __float_as_uint(__fadd_rn(out[base + k], __uint_as_float(v))) : v;
+        const uint32_t v = sm[(k >> 7) * kMsgLaneStride + (k & 127)] ^ carry[k >> 7];
+        io[k] = fold ? __float_as_uint(__fadd_rn(__uint_as_float(io[k]), __uint_as_float(v))) : v;
       }
-      continue;
     }
-    const uint32_t mybits = (e[1 + lane / 2] >> (16 * (lane & 1))) & 0xffffu;
-    uint32_t incl = mybits;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const uint32_t t = __shfl_up_sync(kFull, incl, d);
-      if (lane >= d) incl += t;
-    }
-    const uint32_t total = __shfl_sync(kFull, incl, 31);
-    if ((total + 7ull) / 8 != end - off) {
-      bad = true;
-      break;
-    }
-    const uint32_t i0 = lane * kLaneVals, i1 = min(live, i0 + kLaneVals);
-    uint64_t bit = off * 8 + (incl - mybits);
-    const uint64_t bit0 = bit;
-    uint64_t wi = bit >> 6;
-    uint64_t lo = ll_word(pay, payload, wi), hi = ll_word(pay, payload, wi + 1);
-    uint32_t prev = 0;
-    for (uint32_t i = i0; i < i1; ++i) {
-      const uint64_t w = bit >> 6;
-      if (w != wi) {
-        lo = hi;
-        hi = ll_word(pay, payload, w + 1);
-        if (w != wi + 1) lo = ll_word(pay, payload, w);
-        wi = w;
-      }
-      const uint32_t sh = static_cast<uint32_t>(bit & 63);
-      const uint64_t win = sh ? (lo >> sh) | (hi << (64 - sh)) : lo;
-      const uint32_t nb = 32 - static_cast<uint32_t>(win & 31u);
-      const uint32_t low = static_cast<uint32_t>(win >> 5) & (nb >= 32 ? 0xffffffffu : ((1u << nb) - 1u));
-      bit += 5 + nb;
-      prev ^= low;
-      sm[lane * kMsgLaneStride + (i - i0)] = prev;
-    }
-    const bool lane_bad = bit - bit0 != mybits;
-    // exclusive XOR scan of the lanes' totals -> each lane's carry
-    uint32_t x = prev;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const uint32_t t = __shfl_up_sync(kFull, x, d);
-      if (lane >= d) x ^= t;
-    }
-    carry[lane] = x ^ prev;
-    if (__any_sync(kFull, lane_bad)) {
-      bad = true;
-      break;
-    }
+    // write the chunk: one bulk store of the aligned 16-byte multiple, the rest by hand
+    const uint32_t st_bulk = out_al ? (4 * live) & ~15u : 0u;
+    for (uint32_t k = st_bulk / 4 + lane; k < live; k += 32) o32[base + k] = io[k];
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncwarp();
-    for (uint32_t k = lane; k < live; k += 32) {
-      const uint32_t v = sm[(k >> 7) * kMsgLaneStride + (k & 127)] ^ carry[k >> 7];
-      o32[base + k] = fold ? __float_as_uint(__fadd_rn(out[base + k], __uint_as_float(v))) : v;
+    if (lane == 0 && st_bulk) {
+      bulk_s2g(out + base, io, st_bulk);
+      bulk_commit();
     }
-    __syncwarp();
   }
+  if (lane == 0) bulk_wait_all();
   if (bad && lane == 0) atomicOr(err, kErrCorrupt);
 }
+
+int resident_grid(const void* k, int threads, size_t smem, uint64_t want) {
+  int dev = 0, sms = 148, occ = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, threads, smem);
+  const uint64_t cap = static_cast<uint64_t>(sms) * static_cast<uint64_t>(occ > 0 ? occ : 1);
+  return static_cast<int>(want < cap ? (want ? want : 1) : cap);
+}
+
+std::atomic<uint64_t> g_enc_attr{0};
 
 }  // namespace
 
 hccx_status_t MsgScratch::ensure(uint64_t nchunks) {
-  if (nchunks + 1 <= cap && sizes) return HCCX_OK;
+  if (nchunks <= cap && total) return HCCX_OK;
   release();
-  const uint64_t c = nchunks + 1;
-  if (cudaMalloc(&sizes, 4 * c) != cudaSuccess || cudaMalloc(&fallback, c) != cudaSuccess ||
-      cudaMalloc(&offsets, 8 * c) != cudaSuccess) {
+  const uint64_t c = nchunks ? nchunks : 1;
+  if (cudaMalloc(&desc, 8 * c) != cudaSuccess || cudaMalloc(&total, 3 * 8) != cudaSuccess ||
+      cudaMemset(desc, 0, 8 * c) != cudaSuccess || cudaMemset(total, 0, 3 * 8) != cudaSuccess) {
     release();
     return HCCX_CUDA_FAIL;
   }
   cap = c;
+  epoch = 0;
   return HCCX_OK;
 }
 
 void MsgScratch::release() {
-  cudaFree(sizes);
-  cudaFree(fallback);
-  cudaFree(offsets);
-  sizes = nullptr;
-  fallback = nullptr;
-  offsets = nullptr;
+  cudaFree(desc);
+  cudaFree(total);
+  desc = nullptr;
+  total = nullptr;
   cap = 0;
+}
+
+hccx_status_t msg_encode_to(const float* in, uint64_t n, uint8_t* msg, uint8_t* pay, uint32_t* index,
+                            MsgScratch& s, unsigned long long* acct, cudaStream_t st) {
+  const uint64_t nch = msg_chunks(n);
+  if (msg_max_bytes(n) >= (1ull << 32)) return HCCX_ERR_INVALID_ARGUMENT;  // u32 chunk offsets in the index
+  hccx_status_t r = s.ensure(nch);
+  if (r != HCCX_OK) return r;
+  if (n == 0) {
+    msg_header_kernel<<<1, 32, 0, st>>>(msg, s.total, acct);
+    count_launch();
+    return HCCX_STATUS(cudaGetLastError());
+  }
+  if (++s.epoch >= (1u << 24)) {  // descriptors carry 24 epoch bits: clear on wrap
+    s.epoch = 1;
+    if (cudaMemsetAsync(s.desc, 0, 8 * s.cap, st) != cudaSuccess) return HCCX_CUDA_FAIL;
+  }
+  const void* k = reinterpret_cast<const void*>(&ll_encode_kernel);
+  smem_attr(k, kEncSmem, g_enc_attr);
+  const int grid = resident_grid(k, kEncThreads, kEncSmem, nch);
+  const int vec_ok = (reinterpret_cast<uintptr_t>(in) & 15) == 0;
+  ll_encode_kernel<<<grid, kEncThreads, kEncSmem, st>>>(in, n, nch, vec_ok, pay, index, msg, msg_index_bytes(n),
+                                                         s.desc, s.epoch, s.total,
+                                                         reinterpret_cast<unsigned long long*>(s.total + 1), acct);
+  count_launch();
+  return HCCX_STATUS(cudaGetLastError());
 }
 
 hccx_status_t msg_encode(const float* in, uint64_t n, uint8_t* msg, MsgScratch& s, unsigned long long* acct,
                          cudaStream_t st) {
-  const uint64_t nch = msg_chunks(n);
-  hccx_status_t r = s.ensure(nch);
-  if (r != HCCX_OK) return r;
   const uint64_t ib = msg_index_bytes(n);
-  uint8_t* pay = msg + kMsgHeaderBytes + ib;
-  const size_t smem = sizeof(uint32_t) * kLLWarps * (kStreamWords + 2);
-  smem_attr(reinterpret_cast<const void*>(&ll_emit_kernel), smem, g_emit_attr);
-  if (n) {
-    ll_size_kernel<<<grid_for(nch, kLLWarps), kLLWarps * 32, 0, st>>>(in, n, nch, s.sizes, s.fallback);
-    ll_scan_kernel<<<1, 1024, 0, st>>>(s.sizes, nch, (nch + 7) / 8, s.offsets);
-    ll_flags_kernel<<<grid_for((nch + 7) / 8, 256), 256, 0, st>>>(s.fallback, nch, pay);
-    ll_emit_kernel<<<grid_for(nch, kLLWarps), kLLWarps * 32, smem, st>>>(
-        in, n, nch, s.offsets, s.fallback, pay, reinterpret_cast<uint32_t*>(msg + kMsgHeaderBytes));
-    count_launch(4);
-  } else if (cudaMemsetAsync(s.offsets, 0, 8, st) != cudaSuccess) {
-    return HCCX_CUDA_FAIL;
-  }
-  msg_header_kernel<<<1, 32, 0, st>>>(msg, s.offsets, nch, n, ib, acct);
-  count_launch();
-  return HCCX_STATUS(cudaGetLastError());
+  return msg_encode_to(in, n, msg, msg + kMsgHeaderBytes + ib, reinterpret_cast<uint32_t*>(msg + kMsgHeaderBytes), s,
+                       acct, st);
 }
 
 hccx_status_t msg_copy(const uint8_t* src, uint64_t n, uint8_t* const* dsts, int ndst, unsigned long long* acct,
@@ -984,9 +1284,11 @@ hccx_status_t msg_copy(const uint8_t* src, uint64_t n, uint8_t* const* dsts, int
 hccx_status_t msg_decode(const uint8_t* msg, uint64_t msg_cap, uint64_t n, float* out, bool fold, uint32_t* err,
                          unsigned long long* recv_acct, cudaStream_t st) {
   const uint64_t nch = msg_chunks(n);
-  smem_attr(reinterpret_cast<const void*>(&msg_decode_kernel), kMsgDecodeSmem, g_decode_attr);
-  msg_decode_kernel<<<grid_for(nch ? nch : 1, kLLWarps), kLLWarps * 32, kMsgDecodeSmem, st>>>(
-      msg, msg_cap, n, nch, msg_index_bytes(n), out, fold ? 1 : 0, err, recv_acct);
+  const void* k = reinterpret_cast<const void*>(&msg_decode_kernel);
+  smem_attr(k, kMsgDecodeSmem, g_decode_attr);
+  const int grid = resident_grid(k, kDecWarps * 32, kMsgDecodeSmem, (nch + kDecWarps - 1) / kDecWarps);
+  msg_decode_kernel<<<grid, kDecWarps * 32, kMsgDecodeSmem, st>>>(msg, msg_cap, n, nch, msg_index_bytes(n), out,
+                                                                  fold ? 1 : 0, err, recv_acct);
   count_launch();
   return HCCX_STATUS(cudaGetLastError());
 }

@@ -21,6 +21,8 @@
 // member's next stage.  Values are exact (the codec is lossless), so results
 // equal the identity ring's bit for bit; the traced wire bytes are the
 // payload bytes actually pushed.
+#include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <vector>
@@ -36,7 +38,8 @@ namespace hccx {
 namespace {
 
 __global__ void ll_signal_kernel(uint32_t* flags, uint32_t count, uint32_t value) {
-  fence_acq_rel_sys();  // every prior write of this stream (payload, frame) before the flags
+  if (threadIdx.x == 0) fence_acq_rel_sys();  // every prior write of this stream (payload, frame) before the flags
+  __syncthreads();
   for (uint32_t i = threadIdx.x; i < count; i += blockDim.x) st_relaxed_sys(flags + i, value);
 }
 
@@ -98,14 +101,19 @@ hccx_status_t send_frame(hccx_comm* c, const float* src, uint64_t m, int dst, in
   return msg_encode(src, m, host_slot(c, dst, cls, slot), c->ll_msg, c->ll_acct, s);
 }
 
+// One thread per flag (up to kAckIdx = 1024): an ack or credit touches every
+// index of a slot, and serial system-scope accesses would cost ~1 us each.
+unsigned flag_threads(uint32_t count) { return count < 32 ? 32u : (count > 1024 ? 1024u : (count + 31) / 32 * 32); }
+
 hccx_status_t signal(hccx_comm* c, int rank, int cls, int slot, uint32_t count, uint32_t value, cudaStream_t s) {
-  ll_signal_kernel<<<1, 32, 0, s>>>(host_flag(c, rank, cls, slot, 0), count, value);
+  ll_signal_kernel<<<1, flag_threads(count), 0, s>>>(host_flag(c, rank, cls, slot, 0), count, value);
   count_launch();
   return launched();
 }
 
 hccx_status_t wait(hccx_comm* c, int cls, int slot, uint32_t count, uint32_t epoch, cudaStream_t s) {
-  ll_wait_kernel<<<1, 32, 0, s>>>(host_flag(c, c->rank, cls, slot, 0), count, epoch, c->d_err, comm_timeout_ns());
+  ll_wait_kernel<<<1, flag_threads(count), 0, s>>>(host_flag(c, c->rank, cls, slot, 0), count, epoch, c->d_err,
+                                                   comm_timeout_ns());
   count_launch();
   return launched();
 }
@@ -148,6 +156,7 @@ struct LLRank {
   // broadcast / p2p: one message = the whole compressed container, carried
   // in slot-sized fragments (each fragment one pp epoch)
   bool pp_root = false, pp_recv = false;
+  bool single = false;      // the whole message fits one slot: no staging, no host size read
   uint64_t msg_bytes = 0;   // frame + payload (root: after compress; receiver: after fragment 0)
   uint32_t nfrag = 0;
   uint32_t frag_send[kMaxRanks] = {};  // root: epoch of the current fragment per destination
@@ -188,6 +197,7 @@ hccx_status_t ll_setup(LLRank& r, hccx_comm* c, int op, const float* in, float* 
     r.chunk = n;
     r.pp_root = c->rank == root;
     r.pp_recv = !r.pp_root && (op == 3 || c->rank == dst);
+    r.single = msg_max_bytes(n) <= c->slot_bytes;
     if (r.pp_root)
       for (int d = 0; d < p; ++d)
         if (d != root && (op == 3 || d == dst)) c->geo_pp[d] = lossless_key;
@@ -296,6 +306,10 @@ hccx_status_t ll_pp_prepare(LLRank& r) {
   hccx_comm* c = r.c;
   if (!r.pp_root || r.n == 0) return HCCX_OK;
   DeviceGuard guard(c->device);
+  if (r.single) {  // one fragment; a broadcast encodes once and copies (size read on the device)
+    r.nfrag = 1;
+    return r.op == 3 ? msg_encode(r.in, r.n, c->ll_stage, c->ll_msg, nullptr, r.s) : HCCX_OK;
+  }
   hccx_status_t st = msg_encode(r.in, r.n, c->ll_stage, c->ll_msg, nullptr, r.s);
   if (st != HCCX_OK) return st;
   uint64_t container = 0;  // the message size decides the fragment count
@@ -314,6 +328,24 @@ hccx_status_t ll_pp_send_frag(LLRank& r, uint32_t f, bool* active) {
   *active = true;
   DeviceGuard guard(c->device);
   const int p = c->p, j = c->rank;
+  if (r.single) {
+    uint8_t* dsts[kMaxRanks] = {};
+    int nd = 0;
+    hccx_status_t st = HCCX_OK;
+    for (int d = 0; d < p; ++d) {
+      if (d == j || !(r.op == 3 || d == r.dst)) continue;
+      r.frag_send[d] = ++c->send_ep[d];
+      if ((st = credit(c, 5, d, r.frag_send[d] - 1, r.s)) != HCCX_OK) return st;
+      dsts[nd++] = host_slot(c, d, 2, j);
+    }
+    st = r.op == 3 ? msg_copy(c->ll_stage, r.n, dsts, nd, c->ll_acct, r.s)
+                   : msg_encode(r.in, r.n, dsts[0], c->ll_msg, c->ll_acct, r.s);  // straight into the peer's slot
+    if (st != HCCX_OK) return st;
+    for (int d = 0; d < p; ++d)
+      if (d != j && (r.op == 3 || d == r.dst) && (st = signal(c, d, 2, j, 1, r.frag_send[d], r.s)) != HCCX_OK)
+        return st;
+    return HCCX_OK;
+  }
   const uint64_t off = static_cast<uint64_t>(f) * c->slot_bytes;
   const uint64_t len = r.msg_bytes - off < c->slot_bytes ? r.msg_bytes - off : c->slot_bytes;
   for (int d = 0; d < p; ++d) {
@@ -340,6 +372,11 @@ hccx_status_t ll_pp_recv_frag(LLRank& r, uint32_t f, bool* active) {
   r.frag_recv = ++c->recv_ep[r.root];
   hccx_status_t st = wait(c, 2, r.root, 1, r.frag_recv, r.s);
   if (st != HCCX_OK) return st;
+  if (r.single) {  // decode straight from the slot, then free it
+    r.nfrag = 1;
+    st = msg_decode(host_slot(c, c->rank, 2, r.root), c->slot_bytes, r.n, r.out, false, c->d_err, c->ll_acct + 2, r.s);
+    return st != HCCX_OK ? st : ack(c, r.root, 5, c->rank, r.frag_recv, r.s);
+  }
   const uint64_t off = static_cast<uint64_t>(f) * c->slot_bytes;
   if (f == 0) {  // the frame: how many fragments follow (hcc::from_bytes checks)
     uint8_t h[26];
@@ -370,7 +407,7 @@ hccx_status_t ll_pp_recv_frag(LLRank& r, uint32_t f, bool* active) {
 hccx_status_t ll_pp_complete(LLRank& r) {
   hccx_comm* c = r.c;
   DeviceGuard guard(c->device);
-  if (r.pp_recv && r.n)
+  if (r.pp_recv && r.n && !r.single)
     return msg_decode(c->ll_stage, c->ll_stage_cap, r.n, r.out, false, c->d_err, c->ll_acct + 2, r.s);
   if (r.pp_root && r.op == 3 && r.out && r.out != r.in && r.n &&
       cudaMemcpyAsync(r.out, r.in, 4 * r.n, cudaMemcpyDeviceToDevice, r.s) != cudaSuccess)
@@ -422,31 +459,77 @@ hccx_status_t ll_run(std::vector<LLRank>& ranks, const StepParams& div) {
   const LLRank& r0 = ranks[0];
   const int p = r0.c->p;
   hccx_status_t st = HCCX_OK;
+  // HCCX_LL_PROFILE: per-stage device time on the first rank's stream and
+  // host enqueue time, printed to stderr (development aid)
+  static const bool prof = std::getenv("HCCX_LL_PROFILE") != nullptr;
+  std::vector<cudaEvent_t> evs;
+  std::vector<std::chrono::steady_clock::time_point> hts;
+  std::vector<const char*> names;
+  const char* stage = "start";
+  auto mark = [&](const char* name) {
+    if (!prof) return;
+    DeviceGuard guard(r0.c->device);
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, r0.s);
+    evs.push_back(e);
+    hts.push_back(std::chrono::steady_clock::now());
+    names.push_back(name);
+  };
+  mark("start");
   auto all = [&](auto&& fn) {
     for (LLRank& r : ranks)
       if ((st = fn(r)) != HCCX_OK) return false;
+    mark(stage);
     return true;
   };
+  struct Report {
+    std::vector<cudaEvent_t>& evs;
+    std::vector<std::chrono::steady_clock::time_point>& hts;
+    std::vector<const char*>& names;
+    int dev;
+    ~Report() {
+      if (evs.empty()) return;
+      DeviceGuard guard(dev);
+      cudaEventSynchronize(evs.back());
+      for (size_t i = 1; i < evs.size(); ++i) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, evs[i - 1], evs[i]);
+        std::fprintf(stderr, "hccx ll stage %-10s device %8.1f us  host %8.1f us\n", names[i], ms * 1e3,
+                     std::chrono::duration<double, std::micro>(hts[i] - hts[i - 1]).count());
+      }
+      for (cudaEvent_t e : evs) cudaEventDestroy(e);
+    }
+  } report{evs, hts, names, r0.c->device};
   if (r0.op == 0 || r0.op == 1) {
     for (int t = 0; t < p - 1; ++t) {
+      stage = "rs_send";
       if (!all([&](LLRank& r) { return ll_rs_send(r, t); })) return st;
+      stage = "rs_recv";
       if (!all([&](LLRank& r) { return ll_rs_recv(r, t); })) return st;
     }
   }
   if (r0.op == 0 || r0.op == 2) {
+    stage = "ag_send";
     if (!all([&](LLRank& r) { return ll_ag_send(r); })) return st;
+    stage = "ag_recv";
     if (!all([&](LLRank& r) { return ll_ag_recv(r); })) return st;
   }
   if (r0.op == 3 || r0.op == 4) {
+    stage = "pp_prep";
     if (!all([&](LLRank& r) { return ll_pp_prepare(r); })) return st;
     for (uint32_t f = 0;; ++f) {  // every rank's fragment f before anyone's fragment f+1
       bool active = false;
+      stage = "pp_send";
       if (!all([&](LLRank& r) { return ll_pp_send_frag(r, f, &active); })) return st;
+      stage = "pp_recv";
       if (!all([&](LLRank& r) { return ll_pp_recv_frag(r, f, &active); })) return st;
       if (!active) break;
     }
+    stage = "pp_done";
     if (!all([&](LLRank& r) { return ll_pp_complete(r); })) return st;
   }
+  stage = "finish";
   all([&](LLRank& r) { return ll_finish(r, div); });
   return st;
 }

@@ -41,19 +41,27 @@ inline uint64_t msg_max_bytes(uint64_t n) {
   return kMsgHeaderBytes + msg_index_bytes(n) + (msg_chunks(n) + 7) / 8 + 4 * n + 16;
 }
 
-// Per-communicator encoder scratch (chunk sizes, raw flags, offsets); one
-// per rank so members sharing a device never share it.
+// Per-communicator encoder scratch, one per rank so members sharing a
+// device never share it: the single-pass encoder's per-chunk look-back
+// descriptors (tagged with a call epoch, so never cleared between calls),
+// and 3 device words: the last payload size, the chunk ticket counter and
+// its done counter (reset by the kernel's last warp).
 struct MsgScratch {
-  uint32_t* sizes = nullptr;
-  uint8_t* fallback = nullptr;
-  uint64_t* offsets = nullptr;
+  uint64_t* desc = nullptr;
+  uint64_t* total = nullptr;
   uint64_t cap = 0;
+  uint32_t epoch = 0;
   hccx_status_t ensure(uint64_t nchunks);
   void release();
 };
 
+// Encodes n values: payload at `pay`, chunk index at `index` (optional),
+// frame at `msg` (optional).  The payload size lands in s.total.
+hccx_status_t msg_encode_to(const float* in, uint64_t n, uint8_t* msg, uint8_t* pay, uint32_t* index,
+                            MsgScratch& s, unsigned long long* acct, cudaStream_t st);
+
 // Encodes n values into the message at `msg` (device memory, local or a
-// peer's window; 16-byte aligned).  `acct` (optional, device u64[2]) gains
+// peer's window; 16-byte aligned; msg_max_bytes(n) < 4 GiB).  `acct` (optional, device u64[2]) gains
 // payload bytes and whole-message bytes.  Stream-ordered, no host sync.
 hccx_status_t msg_encode(const float* in, uint64_t n, uint8_t* msg, MsgScratch& s, unsigned long long* acct,
                          cudaStream_t st);
