@@ -379,6 +379,9 @@ struct hccx_group {
   uint8_t* ws = nullptr;
   uint64_t ws_bytes = 0;
   uint32_t* d_err = nullptr;
+  // *_host variants: staging buffers kept across calls (grown on demand)
+  std::vector<float*> hbuf;
+  std::vector<uint64_t> hcap;
 };
 
 namespace {
@@ -506,6 +509,7 @@ extern "C" hccx_status_t hccx_group_destroy(hccx_group_t g) {
   DeviceGuard guard(g->device);
   cudaFree(g->ws);
   cudaFree(g->d_err);
+  for (float* b : g->hbuf) cudaFree(b);
   delete g;
   return HCCX_OK;
 }
@@ -654,16 +658,29 @@ extern "C" hccx_status_t hccx_group_status(hccx_group_t g, void* stream) {
 
 namespace {
 
+// The group's staging buffers for one *_host call: slot k of the call is
+// the group's k-th cached buffer, reallocated only when it must grow (no
+// allocator traffic in steady state).
 struct DevBufs {
-  std::vector<float*> ptrs;
-  ~DevBufs() {
-    for (float* p : ptrs) cudaFree(p);
-  }
+  hccx_group* g;
+  size_t next = 0;
+  explicit DevBufs(hccx_group* grp) : g(grp) {}
   float* add(uint64_t n) {
-    float* p = nullptr;
-    if (cudaMalloc(&p, 4 * (n ? n : 1)) != cudaSuccess) return nullptr;
-    ptrs.push_back(p);
-    return p;
+    const size_t k = next++;
+    if (g->hbuf.size() <= k) {
+      g->hbuf.resize(k + 1, nullptr);
+      g->hcap.resize(k + 1, 0);
+    }
+    if (g->hcap[k] < n || !g->hbuf[k]) {
+      cudaFree(g->hbuf[k]);
+      g->hbuf[k] = nullptr;
+      g->hcap[k] = 0;
+      float* p = nullptr;
+      if (cudaMalloc(&p, 4 * (n ? n : 1)) != cudaSuccess) return nullptr;
+      g->hbuf[k] = p;
+      g->hcap[k] = n;
+    }
+    return g->hbuf[k];
   }
 };
 
@@ -700,7 +717,7 @@ extern "C" hccx_status_t hccx_group_allreduce_host(hccx_group_t g, const float* 
   if (st != HCCX_OK) return st;
   if (n % static_cast<uint64_t>(g->p) != 0) return HCCX_ERR_BAD_CHUNKING;
   DeviceGuard guard(g->device);
-  DevBufs B;
+  DevBufs B(g);
   std::vector<float*> din(g->p), dout(g->p);
   for (int j = 0; j < g->p; ++j) {
     if (!(din[j] = B.add(n)) || !(dout[j] = B.add(n))) return HCCX_CUDA_FAIL;
@@ -724,7 +741,7 @@ extern "C" hccx_status_t hccx_group_reduce_scatter_host(hccx_group_t g, const fl
   if (n % static_cast<uint64_t>(g->p) != 0) return HCCX_ERR_BAD_CHUNKING;
   DeviceGuard guard(g->device);
   const uint64_t c = n / g->p;
-  DevBufs B;
+  DevBufs B(g);
   std::vector<float*> din(g->p), dsh(g->p);
   for (int j = 0; j < g->p; ++j) {
     if (!(din[j] = B.add(n)) || !(dsh[j] = B.add(c))) return HCCX_CUDA_FAIL;
@@ -746,7 +763,7 @@ extern "C" hccx_status_t hccx_group_allgather_host(hccx_group_t g, const float* 
   if (st != HCCX_OK) return st;
   DeviceGuard guard(g->device);
   const uint64_t n = shard_n * g->p;
-  DevBufs B;
+  DevBufs B(g);
   std::vector<float*> dsh(g->p), dout(g->p);
   for (int j = 0; j < g->p; ++j) {
     if (!(dsh[j] = B.add(shard_n)) || !(dout[j] = B.add(n))) return HCCX_CUDA_FAIL;
@@ -767,7 +784,7 @@ extern "C" hccx_status_t hccx_group_broadcast_host(hccx_group_t g, int root, con
   hccx_status_t st = check_group(g, codec);
   if (st != HCCX_OK) return st;
   DeviceGuard guard(g->device);
-  DevBufs B;
+  DevBufs B(g);
   float* din = B.add(n);
   std::vector<float*> dout(g->p);
   if (!din) return HCCX_CUDA_FAIL;
@@ -789,7 +806,7 @@ extern "C" hccx_status_t hccx_group_p2p_host(hccx_group_t g, const float* h_in, 
   hccx_status_t st = check_group(g, codec);
   if (st != HCCX_OK) return st;
   DeviceGuard guard(g->device);
-  DevBufs B;
+  DevBufs B(g);
   float* din = B.add(n);
   float* dout = B.add(n);
   if (!din || !dout) return HCCX_CUDA_FAIL;
