@@ -89,14 +89,14 @@ __device__ __forceinline__ uint32_t encode_head(const float (&v)[4], B& b, uint3
 }
 
 // Two blocks -> 4R bits each: prologues, the significance planes of both
-// blocks in one loop (zfp_planes.cuh steppers, table-driven), then each
-// block's verbatim tail in one word operation.
+// blocks in one loop (zfp_planes.cuh window steppers: two planes per table
+// lookup), then each block's verbatim tail straight from its plane window.
 template <int R, class B>
 __device__ __forceinline__ void encode_pair(const float (&a)[4], const float (&c)[4], B& b0, B& b1, uint32_t& bad) {
   uint32_t ua[4], uc[4];
   const uint32_t ba = encode_head<R>(a, b0, bad, ua);
   const uint32_t bc = encode_head<R>(c, b1, bad, uc);
-  zfp_planes::PlaneEnc e0, e1;
+  zfp_planes::PlaneEnc2 e0, e1;
   e0.init(ua, ba, b0);
   e1.init(uc, bc, b1);
   while (e0.sig_active() || e1.sig_active()) {
@@ -129,7 +129,7 @@ __device__ __forceinline__ void decode_pair(B& b0, B& b1, float (&a)[4], float (
   const bool z0 = !b0.get(1), z1 = !b1.get(1);
   const int e0 = z0 ? 0 : static_cast<int>(b0.get(8)) - 127;
   const int e1 = z1 ? 0 : static_cast<int>(b1.get(8)) - 127;
-  zfp_planes::PlaneDec d0, d1;
+  zfp_planes::PlaneDec2 d0, d1;
   d0.init(b0, z0 ? 0u : 4u * R - 9u);
   d1.init(b1, z1 ? 0u : 4u * R - 9u);
   while (d0.sig_active() || d1.sig_active()) {

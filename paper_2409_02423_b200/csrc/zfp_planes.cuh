@@ -237,22 +237,32 @@ HCCX_HD void decode_planes(Bits& b, uint32_t budget, uint32_t (&u)[4]) {
 // bits; a lookup replaces the per-plane loop over group tests and runs.
 // On the device they live in shared memory: 64 enc entries are 32 words,
 // one per bank (conflict-free for any index pattern).
+// enc2[n*256 + y] (n < 4; y = two consecutive planes' bits, low nibble the
+// higher plane) = the two codewords concatenated | total len << 16 | n_out << 24
+// (at most 14 bits: two planes per lookup in the significance phase).
 struct Lut {
   uint16_t enc[64];
   uint16_t dec[512];
+  uint32_t enc2[1024];
 };
-constexpr uint32_t kLutEntries = 64 + 512;
+constexpr uint32_t kLutEntries = 64 + 512 + 1024;
 
 HCCX_HD void lut_build_entry(uint32_t i, Lut& t) {
   if (i < 64) {
     uint32_t code, nn;
     const uint32_t len = plane_code(i >> 4, i & 15u, &code, &nn);
     t.enc[i] = static_cast<uint16_t>(code | (len << 8) | (nn << 12));
-  } else if (i < kLutEntries) {
+  } else if (i < 64 + 512) {
     const uint32_t j = i - 64;
     uint32_t nn = j >> 7, used;
     const uint32_t x = plane_decode(j & 127u, 7, &nn, &used);
     t.dec[j] = static_cast<uint16_t>(x | (used << 4) | (nn << 8));
+  } else if (i < kLutEntries) {
+    const uint32_t j = i - 64 - 512;
+    uint32_t c1, n1, c2, n2;
+    const uint32_t l1 = plane_code(j >> 8, j & 15u, &c1, &n1);
+    const uint32_t l2 = plane_code(n1, (j >> 4) & 15u, &c2, &n2);
+    t.enc2[j] = (c1 | (c2 << l1)) | ((l1 + l2) << 16) | (n2 << 24);
   }
 }
 
@@ -458,6 +468,150 @@ struct PlaneDec {
     u[2] |= ((x >> 2) & 1u) << k;
     u[3] |= ((x >> 3) & 1u) << k;
     --k;
+  }
+};
+
+// ---- window steppers -------------------------------------------------------
+// The coefficients' next 8 planes as one 32-bit word (nibble q = plane k-q,
+// bit i = coefficient i; zero below plane 0), built once per 8 planes from
+// the bit-reversed coefficients.  The encoder reads two planes per table
+// lookup (enc2) and copies the verbatim tail straight out of the window; the
+// decoder collects decoded planes into a window and scatters it into the
+// coefficients once per 8 planes.  Same bits as PlaneEnc / PlaneDec
+// (tests/cpp/test_zfp_planes.cpp).
+HCCX_HD uint32_t plane_window(const uint32_t (&r)[4], int k) {
+  uint32_t v = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) v |= spread4((r[i] >> (31 - k)) & 0xffu) << i;
+  return v;
+}
+
+struct PlaneEnc2 {
+  uint32_t r[4];  // bit-reversed coefficients
+  uint32_t w;     // window: nibble q = plane k + q0 - q (q0 = nibbles already used)
+  uint32_t budget, n;
+  int k, q;
+  template <class B>
+  HCCX_HD void init(const uint32_t (&uu)[4], uint32_t bud, B& b) {
+    const int G = max(max(top_bit(uu[0]), top_bit(uu[1])), max(top_bit(uu[2]), top_bit(uu[3])));
+    const uint32_t lead = static_cast<uint32_t>(31 - G);
+    const uint32_t e = lead < bud ? lead : bud;
+    b.pos += static_cast<int>(e);
+    budget = bud - e;
+    k = G;
+    n = 0;
+    q = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) r[i] = brev32(uu[i]);
+    w = k >= 0 ? plane_window(r, k) : 0u;
+  }
+  HCCX_HD bool sig_active() const { return budget != 0 && k >= 0 && n < 4; }
+  template <class B>
+  HCCX_HD void step(B& b) {
+    if (q == 8) {
+      w = plane_window(r, k);
+      q = 0;
+    }
+    uint32_t code, len, nn;
+    int planes;
+    if (k >= 1 && q <= 6) {
+      const uint32_t e = lut().enc2[n * 256 + ((w >> (4 * q)) & 0xffu)];
+      code = e & 0xffffu;
+      len = (e >> 16) & 0xffu;
+      nn = e >> 24;
+      planes = 2;
+    } else {
+      const uint32_t e = lut().enc[n * 16 + ((w >> (4 * q)) & 15u)];
+      code = e & 0x7fu;
+      len = (e >> 8) & 7u;
+      nn = e >> 12;
+      planes = 1;
+    }
+    const uint32_t m = len < budget ? len : budget;
+    b.put(code & ((1u << m) - 1u), static_cast<int>(m));
+    budget -= m;
+    n = nn;
+    k -= planes;
+    q += planes;
+  }
+  // all four significant: every remaining plane is its nibble, verbatim
+  template <class B>
+  HCCX_HD void tail(B& b) {
+    while (budget && k >= 0) {
+      if (q == 8) {
+        w = plane_window(r, k);
+        q = 0;
+      }
+      const int avail = 8 - q < k + 1 ? 8 - q : k + 1;
+      const uint32_t bits = budget < 4u * avail ? budget : 4u * avail;
+      const uint32_t v = w >> (4 * q);
+      b.put(bits >= 32 ? v : v & ((1u << bits) - 1u), static_cast<int>(bits));
+      budget -= bits;
+      k -= avail;
+      q += avail;
+    }
+    budget = 0;
+  }
+};
+
+struct PlaneDec2 {
+  uint32_t u[4];
+  uint32_t budget, n;
+  int k, top;  // next plane; the window's top plane
+  uint32_t w;  // decoded planes since `top`, nibble q = plane top - q
+  template <class B>
+  HCCX_HD void init(B& b, uint32_t bud) {
+    u[0] = u[1] = u[2] = u[3] = 0;
+    const uint64_t pk = b.peek();
+    uint32_t lead = pk ? static_cast<uint32_t>(
+#if defined(__CUDA_ARCH__)
+                             __ffsll(static_cast<long long>(pk)) - 1
+#else
+                             __builtin_ctzll(pk)
+#endif
+                             )
+                       : 64u;
+    if (lead > 32) lead = 32;
+    if (lead > bud) lead = bud;
+    b.pos += static_cast<int>(lead);
+    budget = bud - lead;
+    k = 31 - static_cast<int>(lead);
+    top = k;
+    w = 0;
+    n = 0;
+  }
+  HCCX_HD bool sig_active() const { return budget != 0 && k >= 0 && n < 4; }
+  HCCX_HD void flush() {
+    if (w && top >= 0) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) u[i] |= brev32(compact4(w >> i)) >> (31 - top);
+    }
+    w = 0;
+    top = k;
+  }
+  template <class B>
+  HCCX_HD void step(B& b) {
+    if (top - k == 8) flush();
+    uint32_t used, x;
+    const uint64_t pk = b.peek();
+    if (budget >= 7) {
+      const uint32_t e = lut().dec[n * 128 + (static_cast<uint32_t>(pk) & 127u)];
+      x = e & 15u;
+      used = (e >> 4) & 15u;
+      n = e >> 8;
+    } else {  // the block's last, truncated plane
+      x = plane_decode(pk, budget, &n, &used);
+    }
+    b.pos += static_cast<int>(used);
+    budget -= used;
+    w |= x << (4 * (top - k));
+    --k;
+  }
+  template <class B>
+  HCCX_HD void tail(B& b) {
+    flush();
+    get_verbatim(b, k, budget, u);
+    budget = 0;
   }
 };
 

@@ -238,6 +238,46 @@ int main() {
     if (R <= 8) run(Bits32{});
     if (R <= 16) run(Bits64{});
     run(Bits{});
+    // the window steppers (two planes per lookup, windowed tails)
+    auto run2 = [&](auto acc) {
+      using B = decltype(acc);
+      B b;
+      b.put(hdr, 9);
+      PlaneEnc2 e;
+      e.init(u, budget, b);
+      while (e.sig_active()) e.step(b);
+      e.tail(b);
+      Bits got;
+      for (int pos = 0; pos < 4 * R; pos += 16) {
+        B tmp = b;
+        tmp.pos = pos;
+        got.put(tmp.peek() & 0xffffu, 16);
+      }
+      const uint64_t m0 = 4 * R >= 64 ? ~0ull : ((1ull << (4 * R)) - 1ull);
+      const uint64_t m1 = 4 * R >= 128 ? ~0ull : (4 * R <= 64 ? 0ull : ((1ull << (4 * R - 64)) - 1ull));
+      ++checks;
+      if ((got.lo & m0) != (ref.lo & m0) || (got.hi & m1) != (ref.hi & m1)) {
+        if (fails++ < 60) std::printf("window encode R=%d u=%x,%x,%x,%x\n", R, u[0], u[1], u[2], u[3]);
+        return;
+      }
+      B d = b;
+      d.pos = 9;
+      PlaneDec2 dd;
+      dd.init(d, budget);
+      while (dd.sig_active()) dd.step(d);
+      dd.tail(d);
+      Bits r2 = ref;
+      r2.pos = 9;
+      uint32_t ru[4];
+      ref_block_decode(r2, budget, ru);
+      ++checks;
+      if (dd.u[0] != ru[0] || dd.u[1] != ru[1] || dd.u[2] != ru[2] || dd.u[3] != ru[3]) {
+        if (fails++ < 60) std::printf("window decode R=%d u=%x,%x,%x,%x\n", R, u[0], u[1], u[2], u[3]);
+      }
+    };
+    if (R <= 8) run2(Bits32{});
+    if (R <= 16) run2(Bits64{});
+    run2(Bits{});
   }
   std::printf("zfp plane coder: %d checks, %d failures\n", checks, fails);
   return fails ? 1 : 0;
