@@ -99,9 +99,11 @@ __device__ __forceinline__ void encode_pair(const float (&a)[4], const float (&c
   zfp_planes::PlaneEnc2 e0, e1;
   e0.init(ua, ba, b0);
   e1.init(uc, bc, b1);
-  while (e0.sig_active() || e1.sig_active()) {
-    if (e0.sig_active()) e0.step(b0);
-    if (e1.sig_active()) e1.step(b1);
+  for (;;) {
+    const bool a0 = e0.sig_active(), a1 = e1.sig_active();
+    if (!(a0 || a1)) break;
+    if (a0) e0.step(b0);
+    if (a1) e1.step(b1);
   }
   e0.tail(b0);
   e1.tail(b1);
@@ -132,9 +134,11 @@ __device__ __forceinline__ void decode_pair(B& b0, B& b1, float (&a)[4], float (
   zfp_planes::PlaneDec2 d0, d1;
   d0.init(b0, z0 ? 0u : 4u * R - 9u);
   d1.init(b1, z1 ? 0u : 4u * R - 9u);
-  while (d0.sig_active() || d1.sig_active()) {
-    if (d0.sig_active()) d0.step(b0);
-    if (d1.sig_active()) d1.step(b1);
+  for (;;) {
+    const bool a0 = d0.sig_active(), a1 = d1.sig_active();
+    if (!(a0 || a1)) break;
+    if (a0) d0.step(b0);
+    if (a1) d1.step(b1);
   }
   d0.tail(b0);
   d1.tail(b1);

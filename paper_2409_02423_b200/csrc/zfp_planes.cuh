@@ -240,12 +240,15 @@ HCCX_HD void decode_planes(Bits& b, uint32_t budget, uint32_t (&u)[4]) {
 // enc2[n*256 + y] (n < 4; y = two consecutive planes' bits, low nibble the
 // higher plane) = the two codewords concatenated | total len << 16 | n_out << 24
 // (at most 14 bits: two planes per lookup in the significance phase).
+// dec[512 + n*128 + ((1 << b) | bits)] (b = 1..6 bits of budget left, the
+// block's last plane): the truncated decode, which depends only on those b
+// bits -- every plane decodes by one lookup.
 struct Lut {
   uint16_t enc[64];
-  uint16_t dec[512];
+  uint16_t dec[1024];
   uint32_t enc2[1024];
 };
-constexpr uint32_t kLutEntries = 64 + 512 + 1024;
+constexpr uint32_t kLutEntries = 64 + 1024 + 1024;
 
 HCCX_HD void lut_build_entry(uint32_t i, Lut& t) {
   if (i < 64) {
@@ -257,8 +260,24 @@ HCCX_HD void lut_build_entry(uint32_t i, Lut& t) {
     uint32_t nn = j >> 7, used;
     const uint32_t x = plane_decode(j & 127u, 7, &nn, &used);
     t.dec[j] = static_cast<uint16_t>(x | (used << 4) | (nn << 8));
-  } else if (i < kLutEntries) {
+  } else if (i < 64 + 1024) {
     const uint32_t j = i - 64 - 512;
+    uint32_t nn = j >> 7, used = 0;
+    const uint32_t v = j & 127u;  // (1 << b) | bits
+    uint32_t x = 0;
+    if (v >= 2) {
+      const uint32_t b = 31u - static_cast<uint32_t>(
+#if defined(__CUDA_ARCH__)
+                                   __clz(v)
+#else
+                                   __builtin_clz(v)
+#endif
+                               );
+      if (b <= 6) x = plane_decode(v & ((1u << b) - 1u), b, &nn, &used);
+    }
+    t.dec[512 + j] = static_cast<uint16_t>(x | (used << 4) | (nn << 8));
+  } else if (i < kLutEntries) {
+    const uint32_t j = i - 64 - 1024;
     uint32_t c1, n1, c2, n2;
     const uint32_t l1 = plane_code(j >> 8, j & 15u, &c1, &n1);
     const uint32_t l2 = plane_code(n1, (j >> 4) & 15u, &c2, &n2);
@@ -267,10 +286,8 @@ HCCX_HD void lut_build_entry(uint32_t i, Lut& t) {
 }
 
 #if defined(__CUDACC__)
-__device__ __forceinline__ Lut& lut_dev() {
-  __shared__ Lut t;  // one per CTA; filled by lut_init() before first use
-  return t;
-}
+__shared__ Lut g_lut;  // one per CTA (of the kernels that use it); filled by lut_init() before first use
+__device__ __forceinline__ Lut& lut_dev() { return g_lut; }
 // every thread of the CTA, then a CTA barrier before any lookup
 __device__ __forceinline__ void lut_init() {
   for (uint32_t i = threadIdx.x; i < kLutEntries; i += blockDim.x) lut_build_entry(i, lut_dev());
@@ -279,7 +296,7 @@ __device__ __forceinline__ void lut_init() {
 
 HCCX_HD Lut& lut() {
 #if defined(__CUDA_ARCH__)
-  return lut_dev();
+  return g_lut;
 #else
   static Lut t = [] {
     Lut x{};
@@ -592,16 +609,12 @@ struct PlaneDec2 {
   template <class B>
   HCCX_HD void step(B& b) {
     if (top - k == 8) flush();
-    uint32_t used, x;
-    const uint64_t pk = b.peek();
-    if (budget >= 7) {
-      const uint32_t e = lut().dec[n * 128 + (static_cast<uint32_t>(pk) & 127u)];
-      x = e & 15u;
-      used = (e >> 4) & 15u;
-      n = e >> 8;
-    } else {  // the block's last, truncated plane
-      x = plane_decode(pk, budget, &n, &used);
-    }
+    const uint32_t pk = static_cast<uint32_t>(b.peek());
+    // full plane: the next 7 bits; the block's last, truncated plane: its b < 7 bits
+    const uint32_t idx = budget >= 7 ? (pk & 127u) : (512u | (1u << budget) | (pk & ((1u << budget) - 1u)));
+    const uint32_t e = lut().dec[n * 128 + idx];
+    const uint32_t x = e & 15u, used = (e >> 4) & 15u;
+    n = e >> 8;
     b.pos += static_cast<int>(used);
     budget -= used;
     w |= x << (4 * (top - k));
