@@ -285,9 +285,11 @@ def bench_codec(args):
         b.record(s)
         torch.cuda.synchronize()
         soak_ms = a.elapsed_time(b) / (reps * args.steps)
+        torch.cuda.nvtx.range_push("bench_timed")  # ncu --nvtx --nvtx-include bench_timed/ (launch list)
         t0.record(s)
         g_steps.replay()
         t1.record(s)
+        torch.cuda.nvtx.range_pop()
         torch.cuda.synchronize()
     ms = t0.elapsed_time(t1) / args.steps
 
