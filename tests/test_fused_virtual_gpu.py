@@ -210,17 +210,23 @@ def _ngpus():
 
 
 @pytest.mark.skipif(_ngpus() < 2, reason="needs >= 2 GPUs")
-@pytest.mark.parametrize("layout", ["one-per-gpu", "two-per-gpu"])
+@pytest.mark.parametrize("layout", ["one-per-gpu", "two-per-gpu", "eight-ranks"])
 def test_single_process_multi_gpu(cuda, env, layout):
     """hccx_mcomm over distinct GPUs (peer access over NVLink), including a
     ring whose neighbours alternate between GPUs with two virtual ranks per
-    GPU, vs the oracle."""
+    GPU, and the p = 8 ring (north_star's rank count) over every GPU of the
+    box (two ranks per GPU on a 4-GPU box), vs the oracle."""
     import hccx_util as U
 
     g = min(_ngpus(), 4)
-    devices = list(range(g)) if layout == "one-per-gpu" else [j % 2 for j in range(4)]
+    if layout == "one-per-gpu":
+        devices = list(range(g))
+    elif layout == "two-per-gpu":
+        devices = [j % 2 for j in range(4)]
+    else:
+        devices = [j * g // 8 for j in range(8)]
     p = len(devices)
-    m = U.MComm(p, 1 << 21, devices)
+    m = U.MComm(p, max(1 << 21, p * ((1 << 19) + 256)), devices)
     for mode in ("ring-fwd", "ring-direct", "oneshot-ll", "oneshot-flags"):
         env(*MODES[mode])
         for n_per, kind, rate in ((1000, "fixed-rate", 8), (6144 * 5 + 64, "fixed-rate", 4),
