@@ -148,8 +148,9 @@ HCCX_API hccx_status_t hccx_lossless_decompress_host(const uint8_t* h_in, uint64
 
 /* The communicator's framed LosslessPredictor message (one ring hop, one
  * p2p / broadcast message): [32 B frame: u64 container bytes + the HCC1
- * container header][chunk index: 17 u32 per 4096-value chunk -- byte offset,
- * 32 u16 lane bit counts][payload byte-identical to hccx_lossless_compress].
+ * container header][chunk index: 33 u32 per 4096-value chunk -- byte offset,
+ * 64 u16 bit counts of its 64-value blocks][payload byte-identical to
+ * hccx_lossless_compress].
  * Neither call synchronises: sizes stay on the device.  frame_decode
  * validates the frame (as hcc::from_bytes) and the index against the
  * payload; a bad message -> HCCX_ERR_CORRUPT_PAYLOAD from hccx_frame_status.

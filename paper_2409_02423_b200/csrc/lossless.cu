@@ -132,8 +132,7 @@ __device__ void copy_stream_out(const uint32_t* sm, uint8_t* dst, uint32_t len, 
 __global__ void __launch_bounds__(kLLWarps * 32) ll_emit_kernel(const float* __restrict__ in, uint64_t n,
                                                                 uint64_t nchunks, const uint64_t* __restrict__ offsets,
                                                                 const uint8_t* __restrict__ fallback,
-                                                                uint8_t* __restrict__ out,
-                                                                uint32_t* __restrict__ index) {
+                                                                uint8_t* __restrict__ out) {
   extern __shared__ uint32_t llsm[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint32_t* sm = llsm + warp * (kStreamWords + 2);
@@ -143,9 +142,7 @@ __global__ void __launch_bounds__(kLLWarps * 32) ll_emit_kernel(const float* __r
     const uint32_t live = static_cast<uint32_t>(n - base < kChunk ? n - base : kChunk);
     const uint32_t* x = reinterpret_cast<const uint32_t*>(in) + base;
     uint8_t* dst = out + offsets[c];
-    uint32_t* ix = index ? index + kMsgIndexWords * c : nullptr;  // lossless_msg.h
     if (fallback[c]) {  // raw chunk (codec_kernels.hpp:190-194)
-      if (ix && lane <= 16) ix[lane] = lane ? 0u : static_cast<uint32_t>(offsets[c]);
       copy_stream_out(x, dst, 4 * live, lane);
       continue;
     }
@@ -160,11 +157,6 @@ __global__ void __launch_bounds__(kLLWarps * 32) ll_emit_kernel(const float* __r
       if (lane >= o) incl += t;
     }
     const uint32_t total = __shfl_sync(kFull, incl, 31);
-    if (ix) {  // chunk offset, then the lane bit counts as u16 pairs
-      const uint32_t up = __shfl_down_sync(kFull, mybits, 1);
-      if (lane == 0) ix[0] = static_cast<uint32_t>(offsets[c]);
-      if (!(lane & 1)) ix[1 + lane / 2] = mybits | (up << 16);
-    }
     const uint32_t words = (total + 31) / 32;
     for (uint32_t w = lane; w < words + 1; w += 32) sm[w] = 0;
     __syncwarp();
@@ -493,15 +485,6 @@ constexpr uint64_t kJumpMaxBytes = 1ull << 30;
 constexpr uint64_t kJumpKeepBytes = 256ull << 20;
 
 }  // namespace
-
-// part = part + x on `stream` (the lossless ring's fold, used by the engine)
-cudaError_t ll_fold(float* part, const float* x, uint64_t n, cudaStream_t stream) {
-  if (n == 0) return cudaSuccess;
-  ll_fold_kernel<<<grid_for(n, 256 * 4), 256, 0, stream>>>(part, x, n);
-  count_launch();
-  return cudaGetLastError();
-}
-
 }  // namespace hccx
 
 using namespace hccx;
@@ -534,7 +517,7 @@ extern "C" hccx_status_t hccx_lossless_compress(const float* d_in, uint64_t n, u
   smem_attr(reinterpret_cast<const void*>(&ll_emit_kernel), smem, g_emit_attr);
   ll_flags_kernel<<<grid_for((nch + 7) / 8, 256), 256, 0, st>>>(t_scratch.fallback, nch, d_out);
   ll_emit_kernel<<<grid_for(nch, kLLWarps), kLLWarps * 32, smem, st>>>(d_in, n, nch, t_scratch.offsets,
-                                                                      t_scratch.fallback, d_out, nullptr);
+                                                                      t_scratch.fallback, d_out);
   count_launch(2);
   return HCCX_STATUS(cudaGetLastError());
 }
@@ -795,7 +778,7 @@ __global__ void msg_header_kernel(uint8_t* msg, uint64_t* total, unsigned long l
 constexpr int kEncThreads = 256;
 constexpr int kEncVals = kChunk / kEncThreads;  // 16
 constexpr uint32_t kEncStreamWords = kChunk + 8;  // a coded chunk is < 4096 words
-constexpr size_t kEncSmem = sizeof(uint32_t) * (kChunk + kEncStreamWords + 64);
+constexpr size_t kEncSmem = sizeof(uint32_t) * (kChunk + kEncStreamWords + 80);
 
 // descriptor: epoch (24) | status (2: 1 aggregate, 2 inclusive prefix) | raw flag (1) | value (37).
 // Self-contained (no other data is published through it): relaxed accesses.
@@ -877,11 +860,11 @@ __global__ void __launch_bounds__(kEncThreads) ll_encode_kernel(const float* __r
   extern __shared__ __align__(16) uint32_t esm[];
   uint32_t* xin = esm;                       // the chunk's values
   uint32_t* sm = xin + kChunk;               // its code stream
-  uint32_t* misc = sm + kEncStreamWords;     // 64 words: warp totals, block bits, broadcast slots, mbarrier
+  uint32_t* misc = sm + kEncStreamWords;     // 80 words: warp totals, block bits, broadcast slots, mbarrier
   uint32_t* wtot = misc;                     // [8]
-  uint32_t* blk = misc + 8;                  // [32] bits per 128-value block (the index's lane counts)
-  uint64_t* bcast = reinterpret_cast<uint64_t*>(misc + 40);  // [0] ticket, [1] offset
-  uint64_t* bar = reinterpret_cast<uint64_t*>(misc + 48);
+  uint32_t* blk = misc + 8;                  // [64] bits per 64-value block (the index's sub-lane counts)
+  uint64_t* bcast = reinterpret_cast<uint64_t*>(misc + 72);  // [0] ticket, [1] offset
+  uint64_t* bar = reinterpret_cast<uint64_t*>(misc + 76);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) {
     mbar_init(bar, 1);
@@ -943,10 +926,10 @@ __global__ void __launch_bounds__(kEncThreads) ll_encode_kernel(const float* __r
       const uint32_t t = __shfl_up_sync(kFull, incl, d);
       if (lane >= d) incl += t;
     }
-    // bits per 128-value block = 8 consecutive threads
-    const uint32_t end8 = __shfl_sync(kFull, incl, (lane & ~7) + 7);
-    const uint32_t beg8 = __shfl_sync(kFull, incl - bits, lane & ~7);
-    if ((lane & 7) == 0) blk[warp * 4 + (lane >> 3)] = end8 - beg8;
+    // bits per 64-value block = 4 consecutive threads
+    const uint32_t end4 = __shfl_sync(kFull, incl, (lane & ~3) + 3);
+    const uint32_t beg4 = __shfl_sync(kFull, incl - bits, lane & ~3);
+    if ((lane & 3) == 0) blk[warp * 8 + (lane >> 2)] = end4 - beg4;
     if (lane == 31) wtot[warp] = incl;
     __syncthreads();
     uint32_t wbase = 0, chunk_bits = 0;
@@ -1002,7 +985,7 @@ __global__ void __launch_bounds__(kEncThreads) ll_encode_kernel(const float* __r
     __syncthreads();
     const uint64_t off = bcast[1];
     copy_out_cta(fb ? xin : sm, pay + off, static_cast<uint32_t>(size), tid, kEncThreads);
-    if (index && tid < static_cast<int>(kMsgIndexWords)) {
+    if (index && tid < static_cast<int>(kMsgIndexWords)) {  // offset, then 64 u16 block bit counts
       uint32_t* ix = index + kMsgIndexWords * c;
       ix[tid] = tid == 0 ? static_cast<uint32_t>(off)
                          : (fb ? 0u : (blk[2 * (tid - 1)] | (blk[2 * (tid - 1) + 1] << 16)));
@@ -1056,7 +1039,7 @@ __global__ void msg_copy_kernel(const uint8_t* __restrict__ src, MsgDsts D, uint
 constexpr int kDecWarps = 2;
 constexpr uint32_t kDecInWords = kChunk + 12;       // 16 KiB + alignment head/tail
 constexpr uint32_t kMsgLaneStride = kLaneVals + 1;  // 129: conflict-free lane-major staging
-constexpr uint32_t kDecWarpWords = kDecInWords + 32 * kMsgLaneStride + kChunk + 32 + 4;
+constexpr uint32_t kDecWarpWords = kDecInWords + 32 * kMsgLaneStride + kChunk + 64 + 4;
 constexpr size_t kMsgDecodeSmem = sizeof(uint32_t) * kDecWarps * kDecWarpWords;
 static_assert(kDecWarpWords % 4 == 0, "16-byte aligned per-warp regions");
 
@@ -1071,7 +1054,7 @@ __global__ void __launch_bounds__(kDecWarps * 32) msg_decode_kernel(const uint8_
   uint32_t* sm = ins + kDecInWords;            // lane-major decoded values
   uint32_t* io = sm + 32 * kMsgLaneStride;     // contiguous chunk: accumulator in, values out
   uint32_t* carry = io + kChunk;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(carry + 32);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(carry + 64);
   if (lane == 0) {
     mbar_init(bar, 1);
     fence_mbar_init();
@@ -1095,7 +1078,6 @@ __global__ void __launch_bounds__(kDecWarps * 32) msg_decode_kernel(const uint8_
   const uint8_t* pay = msg + kMsgHeaderBytes + idx_bytes;
   uint32_t* o32 = reinterpret_cast<uint32_t*>(out);
   const bool out_al = (reinterpret_cast<uintptr_t>(out) & 15) == 0;
-  const uint64_t* in64 = reinterpret_cast<const uint64_t*>(ins);
   bool bad = false;
   for (uint64_t c = static_cast<uint64_t>(blockIdx.x) * kDecWarps + warp; c < nch;
        c += static_cast<uint64_t>(gridDim.x) * kDecWarps) {
@@ -1134,7 +1116,11 @@ __global__ void __launch_bounds__(kDecWarps * 32) msg_decode_kernel(const uint8_
         io[k] = fold ? __float_as_uint(__fadd_rn(__uint_as_float(io[k]), __uint_as_float(v))) : v;
       }
     } else {
-      const uint32_t mybits = (e[1 + lane / 2] >> (16 * (lane & 1))) & 0xffffu;
+      // lane l decodes values [128 l, 128 l + 128) as two independent
+      // chains (64-value blocks 2l and 2l+1, from their indexed offsets)
+      const uint32_t cw = e[1 + lane];
+      const uint32_t bits_a = cw & 0xffffu, bits_b = cw >> 16;
+      const uint32_t mybits = bits_a + bits_b;
       uint32_t incl = mybits;
 #pragma unroll
       for (int d = 1; d < 32; d <<= 1) {
@@ -1146,43 +1132,57 @@ __global__ void __launch_bounds__(kDecWarps * 32) msg_decode_kernel(const uint8_
         bad = true;
         break;
       }
-      const uint32_t i0 = lane * kLaneVals, i1 = min(live, i0 + kLaneVals);
-      uint32_t bit = 8 * head + (incl - mybits);  // within the staged bytes
-      const uint32_t bit0 = bit;
-      uint32_t wi = bit >> 6;
-      uint64_t lo = in64[wi], hi = in64[wi + 1];
-      uint32_t prev = 0;
-      for (uint32_t i = i0; i < i1; ++i) {
-        const uint32_t w = bit >> 6;
-        if (w != wi) {
-          lo = w == wi + 1 ? hi : in64[w];
-          hi = in64[w + 1];
-          wi = w;
+      const uint32_t i0 = lane * kLaneVals;
+      const uint32_t na = live > i0 ? min(live - i0, 64u) : 0u;
+      const uint32_t nb2 = live > i0 + 64 ? min(live - i0 - 64, 64u) : 0u;
+      uint32_t bit_a = 8 * head + (incl - mybits), bit_b = bit_a + bits_a;  // within the staged bytes
+      const uint32_t a0 = bit_a, b0 = bit_b;
+      uint32_t pa = 0, pb = 0;
+      uint32_t* row = sm + lane * kMsgLaneStride;
+      // one code at `bit` from the staged words: (bits consumed, low value)
+      auto code_at = [&](uint32_t bit, uint32_t& low) {
+        const uint32_t w = bit >> 5, sh = bit & 31;
+        const uint32_t x0 = ins[w], x1 = ins[w + 1], x2 = ins[w + 2];
+        const uint32_t lo = __funnelshift_r(x0, x1, sh), hi = __funnelshift_r(x1, x2, sh);
+        const uint32_t nb = 32 - (lo & 31u);
+        const uint32_t v = __funnelshift_r(lo, hi, 5);  // the 32 bits after the length field
+        low = nb >= 32 ? v : (v & ((1u << nb) - 1u));
+        return 5 + nb;
+      };
+      for (uint32_t i = 0; i < 64; ++i) {
+        if (i < na) {
+          uint32_t low;
+          bit_a += code_at(bit_a, low);
+          pa ^= low;
+          row[i] = pa;
         }
-        const uint32_t sh = bit & 63;
-        const uint64_t win = sh ? (lo >> sh) | (hi << (64 - sh)) : lo;
-        const uint32_t nb = 32 - static_cast<uint32_t>(win & 31u);
-        const uint32_t low = static_cast<uint32_t>(win >> 5) & (nb >= 32 ? 0xffffffffu : ((1u << nb) - 1u));
-        bit += 5 + nb;
-        prev ^= low;
-        sm[lane * kMsgLaneStride + (i - i0)] = prev;
+        if (i < nb2) {
+          uint32_t low;
+          bit_b += code_at(bit_b, low);
+          pb ^= low;
+          row[64 + i] = pb;
+        }
       }
-      const bool lane_bad = bit - bit0 != mybits;
-      // exclusive XOR scan of the lanes' totals -> each lane's carry
-      uint32_t x = prev;
+      const bool lane_bad = bit_a - a0 != bits_a || bit_b - b0 != bits_b;
+      // chain b continues chain a; then an exclusive XOR scan of the lanes'
+      // totals gives each lane its carry (x_i = x_{i-1} ^ r_i within a chunk)
+      const uint32_t tot = pa ^ pb;
+      uint32_t x = tot;
 #pragma unroll
       for (int d = 1; d < 32; d <<= 1) {
         const uint32_t t = __shfl_up_sync(kFull, x, d);
         if (lane >= d) x ^= t;
       }
-      carry[lane] = x ^ prev;
+      carry[lane] = x ^ tot;
+      carry[32 + lane] = pa;
       if (__any_sync(kFull, lane_bad)) {
         bad = true;
         break;
       }
       __syncwarp();
       for (uint32_t k = lane; k < live; k += 32) {
-        const uint32_t v = sm[(k >> 7) * kMsgLaneStride + (k & 127)] ^ carry[k >> 7];
+        const uint32_t l = k >> 7;
+        const uint32_t v = sm[l * kMsgLaneStride + (k & 127)] ^ carry[l] ^ ((k & 64) ? carry[32 + l] : 0u);
         io[k] = fold ? __float_as_uint(__fadd_rn(__uint_as_float(io[k]), __uint_as_float(v))) : v;
       }
     }

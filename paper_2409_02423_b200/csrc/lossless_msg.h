@@ -7,18 +7,18 @@
 //                        header (proj/src/codec.cpp:89-99: magic, kind,
 //                        rate, original_len, chunk_count)
 //   [32, 32 + I)         chunk index (this transport's, not the reference's):
-//                        per 4096-value chunk 17 u32 words -- the chunk's byte
-//                        offset in the payload, then 32 u16 lane bit counts
-//                        (bits coded for values [128 l, 128 l + 128)); I is
-//                        a multiple of 16
+//                        per 4096-value chunk 33 u32 words -- the chunk's byte
+//                        offset in the payload, then 64 u16 block bit counts
+//                        (bits coded for values [64 b, 64 b + 64)); I is a
+//                        multiple of 16
 //   [32 + I, ...)        the LosslessPredictor payload, byte-identical to
 //                        hcc::compress (codec_kernels.hpp:165-239)
 //
 // The reference's payload stores no offsets, so a decoder of the bare
 // payload must walk the 5-bit length fields serially (lossless.cu).  The
-// index costs 68 B per 16 KiB of input (0.4%) and lets the receiver decode
-// every chunk with a full warp (32 lanes x 128 codes) straight from the
-// slot, folding into the accumulator on the way.  The encoder writes it for
+// index costs 132 B per 16 KiB of input (0.8%) and lets the receiver decode
+// every chunk with a full warp (32 lanes x two independent 64-code chains)
+// straight from the slot, folding into the accumulator on the way.  The encoder writes it for
 // free: the emit kernel already computes every lane's bit count.
 #pragma once
 #include <cstdint>
@@ -29,7 +29,7 @@
 namespace hccx {
 
 constexpr uint64_t kMsgHeaderBytes = 32;
-constexpr uint64_t kMsgIndexWords = 17;  // per chunk
+constexpr uint64_t kMsgIndexWords = 33;  // per chunk
 constexpr uint64_t kMsgChunk = 4096;
 constexpr int kMsgMaxDsts = 16;  // msg_copy destinations (the communicator's kMaxRanks)
 

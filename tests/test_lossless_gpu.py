@@ -200,7 +200,7 @@ def test_frame_messages(cuda, n, mode):
     assert _lib.hccx_lossless_frame_encode(xd.data_ptr(), n, msg.data_ptr(), cap, None) == 0
     m = msg.cpu().numpy()
     nch = (n + 4095) // 4096
-    ib = (68 * nch + 15) // 16 * 16
+    ib = (132 * nch + 15) // 16 * 16
     container = int(m[:8].view(np.uint64)[0])
     assert container == 18 + want.size
     assert m[8:12].tobytes() == b"HCC1" and m[12] == 1 and m[13] == 0
@@ -222,12 +222,12 @@ def test_frame_messages(cuda, n, mode):
     b = m.copy(); b[14:22] = np.array([n + 1], np.uint64).view(np.uint8); bad.append(b)  # original_len
     b = m.copy(); b[:8] = np.array([cap * 2], np.uint64).view(np.uint8); bad.append(b)   # container > capacity
     if nch > 1:
-        b = m.copy(); b[32 + 68:32 + 72] = np.array([container * 4], np.uint32).view(np.uint8); bad.append(b)
+        b = m.copy(); b[32 + 132:32 + 136] = np.array([container * 4], np.uint32).view(np.uint8); bad.append(b)
     coded = [c for c in range(nch) if not (want[c // 8] >> (c % 8)) & 1]
     if coded:
         c = coded[0]
         b = m.copy()
-        lane0 = 32 + 68 * c + 4
+        lane0 = 32 + 132 * c + 4
         b[lane0:lane0 + 2] = (np.frombuffer(b[lane0:lane0 + 2].tobytes(), np.uint16) + 8).view(np.uint8)
         bad.append(b)
     for b in bad:
