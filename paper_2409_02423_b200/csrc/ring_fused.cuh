@@ -316,12 +316,25 @@ struct StageGeom {
   int n;
 };
 
+// HCCX_UNIFORM_STAGES: one stage geometry (the largest phase's) for the
+// whole collective, so the input ring runs on across phase boundaries
+// without draining; otherwise the arena is re-carved per phase.
+#ifndef HCCX_UNIFORM_STAGES
+#define HCCX_UNIFORM_STAGES 0
+#endif
+constexpr bool kFUniform = HCCX_UNIFORM_STAGES != 0;
+
 template <class Codec>
 __device__ __forceinline__ StageGeom stage_geom(int kind) {
   StageGeom g;
   g.a = kind == kPhEnc ? kSegVals * 4u : (kSegGroups * Codec::kGroupBytes + 127u) / 128u * 128u;
   g.b = (kind == kPhDar || kind == kPhFinAr || kind == kPhFinRs) ? kSegVals * 4u : 0u;
   g.stride = g.a + g.b;
+  if constexpr (kFUniform) {
+    const uint32_t pay = (kSegGroups * Codec::kGroupBytes + 127u) / 128u * 128u;
+    const uint32_t big = pay + kSegVals * 4u;  // Dar / Fin (>= Enc's fp32 segment)
+    g.stride = big > kSegVals * 4u ? big : kSegVals * 4u;
+  }
   const uint32_t fit = kFArena / g.stride;
   g.n = static_cast<int>(fit < kFMaxStages ? fit : kFMaxStages);
   return g;
@@ -619,12 +632,15 @@ __device__ __forceinline__ void ring_fused_body(const FusedParams& P, const uint
     if (lane == 0) {
       uint64_t c_empty = 0, c_flag = 0, c_total = prof_clock();
       uint32_t pu = 0;  // per-barrier fill parity
+      int st = 0;
       for (int ph = 0; ph < nph; ++ph) {
         const Phase f = phase_of(P, ph);
         const StageGeom sg_ = stage_geom<Codec>(f.kind);
-        // the arena is re-carved for this phase: every earlier fill must be consumed
-        for (int b = 0; b < kFMaxStages; ++b) mbar_wait_to(P, &S.empty[b], ((pu >> b) & 1u) ^ 1u, 0x100u | b, S.prog);
-        int st = 0;
+        if constexpr (!kFUniform) {
+          // the arena is re-carved for this phase: every earlier fill must be consumed
+          for (int b = 0; b < kFMaxStages; ++b) mbar_wait_to(P, &S.empty[b], ((pu >> b) & 1u) ^ 1u, 0x100u | b, S.prog);
+          st = 0;
+        }
         for (uint32_t k0 = 0, k1; k0 < myseg; k0 = k1) {
           k1 = step_end(k0);
           if (f.wait_cls >= 0) {
@@ -950,10 +966,11 @@ __device__ __forceinline__ void ring_fused_body(const FusedParams& P, const uint
   uint32_t tbit = 0;
   uint8_t* gen = S.gen + warp * kStageBytes;
   uint64_t c_full = 0, c_tile = 0, c_comp = 0, c_total = prof_clock();
+  int st = 0;
   for (int ph = 0; ph < nph; ++ph) {
     const Phase f = phase_of(P, ph);
     const StageGeom sg_ = stage_geom<Codec>(f.kind);
-    int st = 0;
+    if constexpr (!kFUniform) st = 0;
     for (uint32_t k = 0; k < myseg; ++k) {
       const uint32_t sg = seg_of(k);
       if (lane == 0) HCCX_PROG(S.prog[warp] = (ph << 20) | (k << 4) | 1u);
