@@ -243,12 +243,14 @@ HCCX_HD void decode_planes(Bits& b, uint32_t budget, uint32_t (&u)[4]) {
 // dec[512 + n*128 + ((1 << b) | bits)] (b = 1..6 bits of budget left, the
 // block's last plane): the truncated decode, which depends only on those b
 // bits -- every plane decodes by one lookup.
+// enc2[1024 + n*16 + x]: the one-plane codes in enc2's packing (for the
+// window stepper's last plane of a window or of the block).
 struct Lut {
   uint16_t enc[64];
   uint16_t dec[1024];
-  uint32_t enc2[1024];
+  uint32_t enc2[1024 + 64];
 };
-constexpr uint32_t kLutEntries = 64 + 1024 + 1024;
+constexpr uint32_t kLutEntries = 64 + 1024 + 1024 + 64;
 
 HCCX_HD void lut_build_entry(uint32_t i, Lut& t) {
   if (i < 64) {
@@ -276,12 +278,17 @@ HCCX_HD void lut_build_entry(uint32_t i, Lut& t) {
       if (b <= 6) x = plane_decode(v & ((1u << b) - 1u), b, &nn, &used);
     }
     t.dec[512 + j] = static_cast<uint16_t>(x | (used << 4) | (nn << 8));
-  } else if (i < kLutEntries) {
+  } else if (i < 64 + 1024 + 1024) {
     const uint32_t j = i - 64 - 1024;
     uint32_t c1, n1, c2, n2;
     const uint32_t l1 = plane_code(j >> 8, j & 15u, &c1, &n1);
     const uint32_t l2 = plane_code(n1, (j >> 4) & 15u, &c2, &n2);
     t.enc2[j] = (c1 | (c2 << l1)) | ((l1 + l2) << 16) | (n2 << 24);
+  } else if (i < kLutEntries) {
+    const uint32_t j = i - 64 - 2048;
+    uint32_t c1, n1;
+    const uint32_t l1 = plane_code(j >> 4, j & 15u, &c1, &n1);
+    t.enc2[1024 + j] = c1 | (l1 << 16) | (n1 << 24);
   }
 }
 
@@ -551,6 +558,28 @@ struct PlaneEnc2 {
     k -= planes;
     q += planes;
   }
+  // step() when `act`, else no change -- branch-free apart from the rare
+  // window refill, so two blocks advance in one converged loop
+  template <class B>
+  HCCX_HD void step_if(B& b, bool act) {
+    if (act && q == 8) {
+      w = plane_window(r, k);
+      q = 0;
+    }
+    const bool two = k >= 1 && q <= 6;
+    const uint32_t nn0 = act ? n : 0u;
+    const uint32_t sh = 4u * static_cast<uint32_t>(q & 7);
+    const uint32_t idx = two ? nn0 * 256u + ((w >> sh) & 0xffu) : 1024u + nn0 * 16u + ((w >> sh) & 15u);
+    const uint32_t e = lut().enc2[idx];
+    const uint32_t len = (e >> 16) & 0xffu;
+    const uint32_t m = act ? (len < budget ? len : budget) : 0u;
+    b.put((e & 0xffffu) & ((1u << m) - 1u), static_cast<int>(m));
+    budget -= m;
+    const int planes = act ? (two ? 2 : 1) : 0;
+    n = act ? (e >> 24) : n;
+    k -= planes;
+    q += planes;
+  }
   // all four significant: every remaining plane is its nibble, verbatim
   template <class B>
   HCCX_HD void tail(B& b) {
@@ -619,6 +648,22 @@ struct PlaneDec2 {
     budget -= used;
     w |= x << (4 * (top - k));
     --k;
+  }
+  // step() when `act`, else no change (see PlaneEnc2::step_if)
+  template <class B>
+  HCCX_HD void step_if(B& b, bool act) {
+    if (act && top - k == 8) flush();
+    const uint32_t pk = static_cast<uint32_t>(b.peek());
+    const uint32_t bud = budget < 7 ? budget : 7u;
+    const uint32_t idx = bud >= 7 ? (pk & 127u) : (512u | (1u << bud) | (pk & ((1u << bud) - 1u)));
+    const uint32_t e = lut().dec[(act ? n : 0u) * 128 + idx];
+    const uint32_t used = act ? (e >> 4) & 15u : 0u;
+    b.pos += static_cast<int>(used);
+    budget -= used;
+    n = act ? (e >> 8) : n;
+    const int sh = 4 * (top - k);
+    w |= act ? (e & 15u) << (sh & 31) : 0u;
+    k -= act ? 1 : 0;
   }
   template <class B>
   HCCX_HD void tail(B& b) {

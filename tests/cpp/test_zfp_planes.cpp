@@ -278,6 +278,61 @@ int main() {
     if (R <= 8) run2(Bits32{});
     if (R <= 16) run2(Bits64{});
     run2(Bits{});
+    // the predicated steppers in a joint two-block loop (the device's form),
+    // the second block a different random block
+    {
+      uint32_t u2[4];
+      for (int i = 0; i < 4; ++i) {
+        const int sh = static_cast<int>(rng() % 33);
+        u2[i] = sh == 32 ? 0u : static_cast<uint32_t>(rng()) >> sh;
+      }
+      Bits ref2;
+      ref2.put(hdr, 9);
+      ref_block_encode(u2, budget, ref2);
+      Bits b0, b1;
+      b0.put(hdr, 9);
+      b1.put(hdr, 9);
+      PlaneEnc2 e0, e1;
+      e0.init(u, budget, b0);
+      e1.init(u2, budget, b1);
+      for (;;) {
+        const bool a0 = e0.sig_active(), a1 = e1.sig_active();
+        if (!(a0 || a1)) break;
+        e0.step_if(b0, a0);
+        e1.step_if(b1, a1);
+      }
+      e0.tail(b0);
+      e1.tail(b1);
+      ++checks;
+      if (b0.lo != ref.lo || b0.hi != ref.hi || b1.lo != ref2.lo || b1.hi != ref2.hi) {
+        if (fails++ < 60) std::printf("joint encode R=%d\n", R);
+      } else {
+        Bits c0 = ref, c1 = ref2;
+        c0.pos = 9;
+        c1.pos = 9;
+        PlaneDec2 d0, d1;
+        d0.init(c0, budget);
+        d1.init(c1, budget);
+        for (;;) {
+          const bool a0 = d0.sig_active(), a1 = d1.sig_active();
+          if (!(a0 || a1)) break;
+          d0.step_if(c0, a0);
+          d1.step_if(c1, a1);
+        }
+        d0.tail(c0);
+        d1.tail(c1);
+        Bits r0 = ref, r1 = ref2;
+        r0.pos = 9;
+        r1.pos = 9;
+        uint32_t w0[4], w1[4];
+        ref_block_decode(r0, budget, w0);
+        ref_block_decode(r1, budget, w1);
+        ++checks;
+        bool ok = true;
+        for (int i = 0; i < 4; ++i) ok = ok && d0.u[i] == w0[i] && d1.u[i] == w1[i];
+        if (!ok && fails++ < 60) std::printf("joint decode R=%d\n", R);
+      }
+    }
   }
   std::printf("zfp plane coder: %d checks, %d failures\n", checks, fails);
   return fails ? 1 : 0;
