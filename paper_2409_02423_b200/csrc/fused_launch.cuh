@@ -36,8 +36,25 @@ inline cudaError_t launch_ranks(const void* kernel_1, const void* kernel_v, cons
     // plain launch is enough (every CTA runs once its GPU has a free SM);
     // HCCX_COOP=1 keeps the cooperative launch (co-residency guaranteed).
     const char* e = std::getenv("HCCX_COOP");
-    if (!(e && e[0] == '1'))
-      return cudaLaunchKernel(kernel_1, dim3(G), dim3(threads), args, smem, stream);
+    if (!(e && e[0] == '1')) {
+      // HCCX_PDL=1: programmatic stream serialization -- the grid is
+      // scheduled while the previous kernel of the stream drains (the kernel
+      // waits for it with griddepcontrol.wait before touching memory).
+      // Measured (profiles/r02_small_pdl.jsonl): 4 KiB 0.9-1.5 us faster,
+      // 64-256 KiB 0.4-0.6 us slower, 256 MiB flat -- off by default.
+      const char* pe = std::getenv("HCCX_PDL");
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(G);
+      cfg.blockDim = dim3(threads);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = stream;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[0].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = (pe && pe[0] == '1') ? 1 : 0;
+      return cudaLaunchKernelExC(&cfg, kernel_1, args);
+    }
     return cudaLaunchCooperativeKernel(kernel_1, dim3(G), dim3(threads), args, smem,
                                        stream);
   }

@@ -366,6 +366,10 @@ __device__ __forceinline__ void oneshot_body(const FusedParams& P, const uint32_
 
 template <class Codec>
 __global__ void __launch_bounds__(kOsWarps * 32) oneshot_allreduce_kernel(const __grid_constant__ FusedParams P) {
+  // launched with programmatic stream serialization (fused_launch.cuh): the
+  // grid is scheduled while the previous kernel drains; nothing is touched
+  // before that kernel has completed
+  pdl_wait_and_release();
   oneshot_body<Codec>(P, blockIdx.x, gridDim.x);
 }
 

@@ -1017,6 +1017,7 @@ __device__ __forceinline__ void ring_fused_body(const FusedParams& P, const uint
 
 template <class Codec>
 __global__ void __launch_bounds__(kFThreads2, kFCtasPerSm) ring_fused_kernel(const __grid_constant__ FusedParams P) {
+  pdl_wait_and_release();  // see oneshot_allreduce_kernel
   ring_fused_body<Codec>(P, blockIdx.x, gridDim.x);
 }
 
