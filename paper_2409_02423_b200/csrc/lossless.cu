@@ -251,49 +251,82 @@ __global__ void ll_walk_kernel(const uint8_t* __restrict__ in, uint64_t in_bytes
 }
 
 // decompress (a'): the same offsets by pointer doubling.  J0[x] = the bit
-// position after the code starting at bit x (S+1 when it would run past the
-// S-bit stream; S+1 is absorbing).  Twelve rounds of J <- J o J give
-// J12[x] = the position after 4096 codes, so a coded chunk starting at byte
-// B ends at byte ceil(J12[8B] / 8): the serial walk shrinks to one lookup
-// per chunk.  Every position of the stream is a candidate start because the
-// chunk starts are unknown; 8 bytes of table per stream bit.
-__global__ void ll_jump0_kernel(const uint8_t* __restrict__ in, uint64_t in_bytes, uint32_t S,
-                                uint32_t* __restrict__ J) {
-  const uint64_t total = static_cast<uint64_t>(S) + 2;
-  for (uint64_t x = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; x < total;
-       x += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-    uint32_t nx = S + 1;
-    if (x + 5 <= S) {
-      const uint64_t B = x >> 3;
-      uint32_t w = __ldg(in + B);
-      if (B + 1 < in_bytes) w |= static_cast<uint32_t>(__ldg(in + B + 1)) << 8;
-      const uint64_t e = x + 37 - ((w >> (x & 7)) & 31u);
-      if (e <= S) nx = static_cast<uint32_t>(e);
-    }
-    J[x] = nx;
-  }
-}
-
+// position after the code starting at bit x; twelve rounds of J <- J o J give
+// the position after 4096 codes, so a coded chunk starting at byte B ends at
+// byte ceil(J12[8B] / 8): the serial walk shrinks to one lookup per chunk.
+// Every position of the stream is a candidate start because the chunk starts
+// are unknown (the format stores no offsets).
 __global__ void ll_jump_kernel(const uint32_t* __restrict__ Jin, uint32_t* __restrict__ Jout, uint64_t total) {
   for (uint64_t x = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; x < total;
        x += static_cast<uint64_t>(gridDim.x) * blockDim.x)
     Jout[x] = Jin[Jin[x]];
 }
 
-__global__ void ll_walk_jump_kernel(const uint8_t* __restrict__ in, uint64_t in_bytes, uint64_t n, uint64_t nchunks,
-                                    const uint32_t* __restrict__ J12, uint32_t S, uint64_t* __restrict__ offsets,
-                                    uint32_t* __restrict__ err) {
+// decompress (a''), memory-bounded: the same doubling over slabs of the
+// stream.  A chain of 4096 codes from a slab position ends at most
+// kChainBits later, so slab [lo, hi) needs the jump table only over
+// [lo, hi + kChainBits): positions are slab-relative (u32), `sent` is the
+// absorbing "past the end" index, and the result is kept per payload BYTE
+// (chunks start byte-aligned): F[B] = the byte after a coded chunk starting
+// at byte B, or ~0u when it would run past the payload.
+constexpr uint64_t kChainBits = 4096ull * 37ull;
+// J0 jumps kJump0Codes codes, kJumpRounds doublings reach 4096.  Walking 8
+// codes in J0 and doubling 9 times measured no faster at 2^24 values and
+// 1.5x slower on sparse 2^26-value payloads (the walk's byte loads).
+constexpr int kJump0Codes = 1;
+constexpr int kJumpRounds = 12;
+
+__global__ void ll_jump0_slab_kernel(const uint8_t* __restrict__ in, uint64_t in_bytes, uint64_t S, uint64_t lo,
+                                     uint64_t ext, uint32_t* __restrict__ J) {
+  const uint64_t span = ext - lo;  // positions 0..span (ext itself included), sentinel span + 1
+  const uint32_t sent = static_cast<uint32_t>(span + 1);
+  for (uint64_t x = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; x <= span + 1;
+       x += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    // the position after kJump0Codes codes
+    uint32_t nx = sent;
+    uint64_t pos = lo + x;
+    if (x < span) {
+      int k = 0;
+      for (; k < kJump0Codes; ++k) {
+        if (pos + 5 > S) break;
+        const uint64_t B = pos >> 3;
+        uint32_t w = __ldg(in + B);
+        if (B + 1 < in_bytes) w |= static_cast<uint32_t>(__ldg(in + B + 1)) << 8;
+        const uint64_t e = pos + 37 - ((w >> (pos & 7)) & 31u);
+        if (e > S || e > ext) break;  // past ext: only halo chains go there
+        pos = e;
+      }
+      if (k == kJump0Codes) nx = static_cast<uint32_t>(pos - lo);
+    }
+    J[x] = nx;
+  }
+}
+
+__global__ void ll_jump_out_kernel(const uint32_t* __restrict__ J, uint64_t lo, uint64_t hi, uint64_t span,
+                                   uint32_t* __restrict__ F) {
+  const uint64_t b0 = (lo + 7) / 8, b1 = (hi + 7) / 8;  // bytes whose first bit lies in [lo, hi)
+  for (uint64_t b = b0 + blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; b < b1;
+       b += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t e = J[8 * b - lo];
+    F[b] = e > span ? ~0u : static_cast<uint32_t>((lo + e + 7) / 8);
+  }
+}
+
+// Chunk offsets from F: one dependent lookup per coded chunk.
+__global__ void ll_walk_f_kernel(const uint8_t* __restrict__ in, uint64_t in_bytes, uint64_t n, uint64_t nch,
+                                 const uint32_t* __restrict__ F, uint64_t* __restrict__ offsets,
+                                 uint32_t* __restrict__ err) {
   if (threadIdx.x != 0) return;
-  uint64_t pos = (nchunks + 7) / 8;
+  uint64_t pos = (nch + 7) / 8;
   const uint64_t end_bit = 8 * in_bytes;
-  for (uint64_t c = 0; c < nchunks; ++c) {
+  for (uint64_t c = 0; c < nch; ++c) {
     offsets[c] = pos;
     const uint32_t live = static_cast<uint32_t>(n - c * kChunk < kChunk ? n - c * kChunk : kChunk);
     if ((__ldg(in + c / 8) >> (c % 8)) & 1u) {
       pos += 4ull * live;
     } else if (live == kChunk) {
-      const uint32_t b = J12[8 * pos <= S ? 8 * pos : static_cast<uint64_t>(S) + 1];
-      pos = b > S ? in_bytes + 1 : (static_cast<uint64_t>(b) + 7) / 8;
+      const uint32_t b = pos < in_bytes ? F[pos] : ~0u;
+      pos = b == ~0u ? in_bytes + 1 : b;
     } else {  // the short last chunk: walk it
       uint64_t bit = pos * 8;
       for (uint32_t i = 0; i < live && bit <= end_bit; ++i) {
@@ -313,7 +346,95 @@ __global__ void ll_walk_jump_kernel(const uint8_t* __restrict__ in, uint64_t in_
       pos = in_bytes;
     }
   }
-  offsets[nchunks] = pos;
+  offsets[nch] = pos;
+}
+
+// F^(2^k) over payload bytes (F[in_bytes] = ~0u ends every chain).
+__global__ void ll_fjump_kernel(const uint32_t* __restrict__ Fin, uint32_t* __restrict__ Fout, uint64_t entries) {
+  for (uint64_t b = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; b < entries;
+       b += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t f = Fin[b];
+    Fout[b] = f < entries ? Fin[f] : ~0u;
+  }
+}
+
+constexpr uint64_t kWalkBlock = 64;  // chunks per anchor block (F^64 jumps)
+
+// Chunk-start anchors every kWalkBlock chunks: a block of full coded chunks
+// is one F^64 lookup, any other block is stepped chunk by chunk.
+__global__ void ll_walk_anchor_kernel(const uint8_t* __restrict__ in, uint64_t in_bytes, uint64_t n, uint64_t nch,
+                                      const uint32_t* __restrict__ F, const uint32_t* __restrict__ F64,
+                                      uint64_t* __restrict__ offsets, uint32_t* __restrict__ err) {
+  if (threadIdx.x != 0) return;
+  uint64_t pos = (nch + 7) / 8;
+  for (uint64_t a = 0; a < nch; a += kWalkBlock) {
+    offsets[a] = pos;
+    const uint64_t e = a + kWalkBlock < nch ? a + kWalkBlock : nch;
+    bool uniform = e - a == kWalkBlock && e * kChunk <= n;
+    for (uint64_t c = a; c < e && uniform; c += 8)
+      if (__ldg(in + c / 8)) uniform = false;  // a raw chunk in the block (8-aligned blocks)
+    if (uniform) {
+      const uint32_t b = pos < in_bytes ? F64[pos] : ~0u;
+      pos = b == ~0u ? in_bytes + 1 : b;
+    } else {
+      for (uint64_t c = a; c < e && pos <= in_bytes; ++c) {
+        const uint32_t live = static_cast<uint32_t>(n - c * kChunk < kChunk ? n - c * kChunk : kChunk);
+        if ((__ldg(in + c / 8) >> (c % 8)) & 1u) {
+          pos += 4ull * live;
+        } else if (live == kChunk) {
+          const uint32_t b = pos < in_bytes ? F[pos] : ~0u;
+          pos = b == ~0u ? in_bytes + 1 : b;
+        } else {
+          break;  // the short last chunk: ll_walk_fill_kernel walks it
+        }
+      }
+    }
+    if (pos > in_bytes) {
+      atomicOr(err, 8u);
+      pos = in_bytes;
+    }
+  }
+}
+
+// Every block's chunks from its anchor, one thread per block.
+__global__ void ll_walk_fill_kernel(const uint8_t* __restrict__ in, uint64_t in_bytes, uint64_t n, uint64_t nch,
+                                    const uint32_t* __restrict__ F, uint64_t* __restrict__ offsets,
+                                    uint32_t* __restrict__ err) {
+  const uint64_t nblk = (nch + kWalkBlock - 1) / kWalkBlock;
+  const uint64_t end_bit = 8 * in_bytes;
+  for (uint64_t k = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; k < nblk;
+       k += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t a = k * kWalkBlock, e = a + kWalkBlock < nch ? a + kWalkBlock : nch;
+    uint64_t pos = offsets[a];
+    for (uint64_t c = a; c < e; ++c) {
+      offsets[c] = pos;
+      const uint32_t live = static_cast<uint32_t>(n - c * kChunk < kChunk ? n - c * kChunk : kChunk);
+      if ((__ldg(in + c / 8) >> (c % 8)) & 1u) {
+        pos += 4ull * live;
+      } else if (live == kChunk) {
+        const uint32_t b = pos < in_bytes ? F[pos] : ~0u;
+        pos = b == ~0u ? in_bytes + 1 : b;
+      } else {  // the short last chunk: walk it
+        uint64_t bit = pos * 8;
+        for (uint32_t i = 0; i < live && bit <= end_bit; ++i) {
+          if (bit + 5 > end_bit) {
+            bit = end_bit + 1;
+            break;
+          }
+          const uint64_t B = bit >> 3;
+          uint32_t w = __ldg(in + B);
+          if (B + 1 < in_bytes) w |= static_cast<uint32_t>(__ldg(in + B + 1)) << 8;
+          bit += 5 + (32 - ((w >> (bit & 7)) & 31u));
+        }
+        pos = bit > end_bit ? in_bytes + 1 : (bit + 7) / 8;
+      }
+      if (pos > in_bytes) {
+        atomicOr(err, 8u);
+        pos = in_bytes;
+      }
+    }
+    if (e == nch) offsets[nch] = pos;
+  }
 }
 
 // decompress (b): raw chunks, one warp per chunk (coalesced copies)
@@ -406,11 +527,14 @@ struct Scratch {
   uint64_t* offsets = nullptr;
   uint32_t* err = nullptr;
   uint64_t cap = 0;
-  uint32_t* jump[2] = {nullptr, nullptr};  // pointer-doubling tables
+  uint32_t* jump[2] = {nullptr, nullptr};  // pointer-doubling tables (one slab)
   uint64_t jump_cap = 0;
+  uint32_t* fend = nullptr;  // per payload byte: the byte after a coded chunk starting there
+  uint64_t fend_cap = 0;
   ~Scratch() {
     cudaFree(jump[0]);
     cudaFree(jump[1]);
+    cudaFree(fend);
     cudaFree(sizes);
     cudaFree(fallback);
     cudaFree(offsets);
@@ -429,11 +553,26 @@ struct Scratch {
     cap = c;
     return HCCX_OK;
   }
+  bool ensure_fend(uint64_t entries) {
+    if (entries <= fend_cap && fend) return true;
+    cudaFree(fend);
+    fend = nullptr;
+    fend_cap = 0;
+    if (cudaMalloc(&fend, 4 * entries) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    fend_cap = entries;
+    return true;
+  }
   void drop_jump() {
     cudaFree(jump[0]);
     cudaFree(jump[1]);
     jump[0] = jump[1] = nullptr;
     jump_cap = 0;
+    cudaFree(fend);
+    fend = nullptr;
+    fend_cap = 0;
   }
   bool ensure_jump(uint64_t entries) {
     if (entries <= jump_cap) return true;
@@ -478,11 +617,13 @@ Scratch& scratch() {
   return s[d & 15];
 }
 
-// Pointer-doubling tables cost 8 bytes per payload bit: above this budget
-// the serial walk is used instead, and tables above kJumpKeepBytes are
-// freed after the call rather than pinned for the thread's lifetime.
-constexpr uint64_t kJumpMaxBytes = 1ull << 30;
-constexpr uint64_t kJumpKeepBytes = 256ull << 20;
+// Pointer doubling runs over slabs of at most kSlabBits stream bits (tables
+// 8 bytes per slab bit + halo: ~0.5 GiB), so the scratch is bounded for any
+// payload; scratch above kJumpKeepBytes is freed after the call rather than
+// pinned for the thread's lifetime.
+constexpr uint64_t kSlabBits = 64ull << 20;
+constexpr uint64_t kJumpKeepBytes = 1ull << 30;  // slab tables (~0.5 GiB) stay allocated
+constexpr uint64_t kFendKeepBytes = 1ull << 30;  // per-byte chunk ends (4 B per payload byte)
 
 }  // namespace
 }  // namespace hccx
@@ -534,30 +675,56 @@ extern "C" hccx_status_t hccx_lossless_decompress(const uint8_t* d_in, uint64_t 
   hccx_status_t r = t_scratch.ensure(nch);
   if (r != HCCX_OK) return r;
   cudaMemsetAsync(t_scratch.err, 0, 4, st);
-  // Offsets: pointer doubling over the whole stream when there are many
-  // full chunks and the tables fit (8 bytes per stream bit), else the
-  // serial walk (cheap for all-raw payloads: O(1) per raw chunk).
+  // Offsets: pointer doubling (slab by slab, bounded scratch) when there
+  // are many coded chunks, else the serial walk (cheap for few or raw
+  // chunks: O(1) per raw chunk).
   const uint64_t S = 8 * in_bytes;
-  bool jump = nch >= 64 && S + 2 < (1ull << 32) && 8 * (S + 2) <= kJumpMaxBytes &&
-              std::getenv("HCCX_LL_SERIAL") == nullptr;
-  if (jump) {  // worth it only with many coded chunks: count them from the flag bytes
+  bool jump = nch >= 64 && in_bytes < (1ull << 32) - 1 && std::getenv("HCCX_LL_SERIAL") == nullptr;
+  if (jump) {  // count the coded chunks from the flag bytes
     std::vector<uint8_t> flags((nch + 7) / 8);
     if (cudaMemcpyAsync(flags.data(), d_in, flags.size(), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
         cudaStreamSynchronize(st) != cudaSuccess)
       return HCCX_CUDA_FAIL;
     uint64_t raw = 0;
     for (uint64_t c = 0; c < nch; ++c) raw += (flags[c / 8] >> (c % 8)) & 1u;
-    jump = nch - raw >= 64 && t_scratch.ensure_jump(S + 2);
+    const uint64_t slab = S < kSlabBits ? S : kSlabBits;
+    jump = nch - raw >= 64 && t_scratch.ensure_jump(slab + kChainBits + 2) && t_scratch.ensure_fend(in_bytes + 1);
   }
   if (jump) {
     const int g = 148 * 8;
-    ll_jump0_kernel<<<g, 256, 0, st>>>(d_in, in_bytes, static_cast<uint32_t>(S), t_scratch.jump[0]);
-    int cur = 0;
-    for (int r = 0; r < 12; ++r, cur ^= 1)
-      ll_jump_kernel<<<g, 256, 0, st>>>(t_scratch.jump[cur], t_scratch.jump[cur ^ 1], S + 2);
-    ll_walk_jump_kernel<<<1, 32, 0, st>>>(d_in, in_bytes, n, nch, t_scratch.jump[cur], static_cast<uint32_t>(S),
-                                          t_scratch.offsets, t_scratch.err);
-    count_launch(13);
+    for (uint64_t lo = 0; lo < S; lo += kSlabBits) {
+      const uint64_t hi = lo + kSlabBits < S ? lo + kSlabBits : S;
+      const uint64_t ext = hi + kChainBits < S ? hi + kChainBits : S;
+      const uint64_t span = ext - lo;
+      ll_jump0_slab_kernel<<<g, 256, 0, st>>>(d_in, in_bytes, S, lo, ext, t_scratch.jump[0]);
+      int cur = 0;
+      for (int r = 0; r < kJumpRounds; ++r, cur ^= 1)
+        ll_jump_kernel<<<g, 256, 0, st>>>(t_scratch.jump[cur], t_scratch.jump[cur ^ 1], span + 2);
+      ll_jump_out_kernel<<<g, 256, 0, st>>>(t_scratch.jump[cur], lo, hi, span, t_scratch.fend);
+      count_launch(2 + kJumpRounds);
+    }
+    // chunk starts: F^64 by six doubling rounds over the payload's bytes
+    // (in the slab tables, free now), anchors every 64 chunks, then every
+    // block filled in parallel -- or the plain chain when the bytes do not fit
+    const uint64_t entries = in_bytes + 1;
+    if (entries <= t_scratch.jump_cap && nch >= 2 * kWalkBlock) {
+      cudaMemsetAsync(t_scratch.fend + in_bytes, 0xff, 4, st);
+      const int g = 148 * 8;
+      const uint32_t* src = t_scratch.fend;
+      int cur = 0;
+      for (int r = 0; r < 6; ++r, cur ^= 1) {
+        ll_fjump_kernel<<<g, 256, 0, st>>>(src, t_scratch.jump[cur], entries);
+        src = t_scratch.jump[cur];
+      }
+      ll_walk_anchor_kernel<<<1, 32, 0, st>>>(d_in, in_bytes, n, nch, t_scratch.fend, src, t_scratch.offsets,
+                                              t_scratch.err);
+      ll_walk_fill_kernel<<<grid_for((nch + kWalkBlock - 1) / kWalkBlock, 128), 128, 0, st>>>(
+          d_in, in_bytes, n, nch, t_scratch.fend, t_scratch.offsets, t_scratch.err);
+      count_launch(8);
+    } else {
+      ll_walk_f_kernel<<<1, 32, 0, st>>>(d_in, in_bytes, n, nch, t_scratch.fend, t_scratch.offsets, t_scratch.err);
+      count_launch();
+    }
   } else {
     ll_walk_kernel<<<1, 32, 0, st>>>(d_in, in_bytes, n, nch, t_scratch.offsets, t_scratch.err);
   }
@@ -574,7 +741,8 @@ extern "C" hccx_status_t hccx_lossless_decompress(const uint8_t* d_in, uint64_t 
       cudaStreamSynchronize(st) != cudaSuccess)
     return HCCX_CUDA_FAIL;
   (void)end;  // trailing bytes are ignored, as in codec_serial.cpp:85-107
-  if (8 * t_scratch.jump_cap > kJumpKeepBytes) t_scratch.drop_jump();  // do not pin large tables
+  // do not pin large scratch for the thread's lifetime
+  if (8 * t_scratch.jump_cap > kJumpKeepBytes || 4 * t_scratch.fend_cap > kFendKeepBytes) t_scratch.drop_jump();
   if (e) return HCCX_ERR_CORRUPT_PAYLOAD;
   return HCCX_OK;
 }
