@@ -270,35 +270,59 @@ __global__ void ll_jump_kernel(const uint32_t* __restrict__ Jin, uint32_t* __res
 // (chunks start byte-aligned): F[B] = the byte after a coded chunk starting
 // at byte B, or ~0u when it would run past the payload.
 constexpr uint64_t kChainBits = 4096ull * 37ull;
-// J0 jumps kJump0Codes codes, kJumpRounds doublings reach 4096.  Walking 8
-// codes in J0 and doubling 9 times measured no faster at 2^24 values and
-// 1.5x slower on sparse 2^26-value payloads (the walk's byte loads).
-constexpr int kJump0Codes = 1;
-constexpr int kJumpRounds = 12;
 
-__global__ void ll_jump0_slab_kernel(const uint8_t* __restrict__ in, uint64_t in_bytes, uint64_t S, uint64_t lo,
-                                     uint64_t ext, uint32_t* __restrict__ J) {
-  const uint64_t span = ext - lo;  // positions 0..span (ext itself included), sentinel span + 1
+
+// The first doublings in 16-bit relative form (a jump of 2^k codes spans at
+// most 37 * 2^k bits: < 2^16 up to k = 10), half the table traffic of the
+// 32-bit rounds; 0xFFFF = past the end.
+constexpr uint16_t kRel16End = 0xFFFFu;
+constexpr int kRel16Rounds = 10;
+
+__global__ void ll_jump0_rel16_kernel(const uint8_t* __restrict__ in, uint64_t in_bytes, uint64_t S, uint64_t lo,
+                                      uint64_t ext, uint16_t* __restrict__ D) {
+  const uint64_t span = ext - lo;
+  for (uint64_t x = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; x <= span;
+       x += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    uint16_t d = kRel16End;
+    const uint64_t pos = lo + x;
+    if (x < span && pos + 5 <= S) {
+      const uint64_t B = pos >> 3;
+      uint32_t w = __ldg(in + B);
+      if (B + 1 < in_bytes) w |= static_cast<uint32_t>(__ldg(in + B + 1)) << 8;
+      const uint32_t len = 37u - ((w >> (pos & 7)) & 31u);
+      if (pos + len <= S && pos + len <= ext) d = static_cast<uint16_t>(len);
+    }
+    D[x] = d;
+  }
+}
+
+__global__ void ll_jump_rel16_kernel(const uint16_t* __restrict__ Din, uint16_t* __restrict__ Dout, uint64_t entries) {
+  for (uint64_t x = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; x < entries;
+       x += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t d = Din[x];
+    uint16_t o = kRel16End;
+    if (d != kRel16End) {
+      const uint32_t d2 = Din[x + d];
+      if (d2 != kRel16End) o = static_cast<uint16_t>(d + d2);
+    }
+    Dout[x] = o;
+  }
+}
+
+// Last 16-bit doubling, written as 32-bit slab positions (sentinel span + 1).
+__global__ void ll_jump_rel16_to32_kernel(const uint16_t* __restrict__ Din, uint32_t* __restrict__ J, uint64_t span) {
   const uint32_t sent = static_cast<uint32_t>(span + 1);
   for (uint64_t x = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; x <= span + 1;
        x += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-    // the position after kJump0Codes codes
-    uint32_t nx = sent;
-    uint64_t pos = lo + x;
-    if (x < span) {
-      int k = 0;
-      for (; k < kJump0Codes; ++k) {
-        if (pos + 5 > S) break;
-        const uint64_t B = pos >> 3;
-        uint32_t w = __ldg(in + B);
-        if (B + 1 < in_bytes) w |= static_cast<uint32_t>(__ldg(in + B + 1)) << 8;
-        const uint64_t e = pos + 37 - ((w >> (pos & 7)) & 31u);
-        if (e > S || e > ext) break;  // past ext: only halo chains go there
-        pos = e;
+    uint32_t o = sent;
+    if (x <= span) {
+      const uint32_t d = Din[x];
+      if (d != kRel16End) {
+        const uint32_t d2 = Din[x + d];
+        if (d2 != kRel16End) o = static_cast<uint32_t>(x + d + d2);
       }
-      if (k == kJump0Codes) nx = static_cast<uint32_t>(pos - lo);
     }
-    J[x] = nx;
+    J[x] = o;
   }
 }
 
@@ -696,12 +720,19 @@ extern "C" hccx_status_t hccx_lossless_decompress(const uint8_t* d_in, uint64_t 
       const uint64_t hi = lo + kSlabBits < S ? lo + kSlabBits : S;
       const uint64_t ext = hi + kChainBits < S ? hi + kChainBits : S;
       const uint64_t span = ext - lo;
-      ll_jump0_slab_kernel<<<g, 256, 0, st>>>(d_in, in_bytes, S, lo, ext, t_scratch.jump[0]);
+      // J0 .. J10 as 16-bit relative jumps, J11 into 32 bits, J12
+      uint16_t* d16[2] = {reinterpret_cast<uint16_t*>(t_scratch.jump[0]),
+                          reinterpret_cast<uint16_t*>(t_scratch.jump[1])};
+      ll_jump0_rel16_kernel<<<g, 256, 0, st>>>(d_in, in_bytes, S, lo, ext, d16[0]);
       int cur = 0;
-      for (int r = 0; r < kJumpRounds; ++r, cur ^= 1)
-        ll_jump_kernel<<<g, 256, 0, st>>>(t_scratch.jump[cur], t_scratch.jump[cur ^ 1], span + 2);
+      for (int r = 0; r < kRel16Rounds; ++r, cur ^= 1)
+        ll_jump_rel16_kernel<<<g, 256, 0, st>>>(d16[cur], d16[cur ^ 1], span + 1);
+      ll_jump_rel16_to32_kernel<<<g, 256, 0, st>>>(d16[cur], t_scratch.jump[cur ^ 1], span);
+      cur ^= 1;
+      ll_jump_kernel<<<g, 256, 0, st>>>(t_scratch.jump[cur], t_scratch.jump[cur ^ 1], span + 2);
+      cur ^= 1;
       ll_jump_out_kernel<<<g, 256, 0, st>>>(t_scratch.jump[cur], lo, hi, span, t_scratch.fend);
-      count_launch(2 + kJumpRounds);
+      count_launch(4 + kRel16Rounds);
     }
     // chunk starts: F^64 by six doubling rounds over the payload's bytes
     // (in the slab tables, free now), anchors every 64 chunks, then every
