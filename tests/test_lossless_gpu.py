@@ -234,3 +234,34 @@ def test_frame_messages(cuda, n, mode):
         bm = torch.from_numpy(b).cuda()
         assert _lib.hccx_lossless_frame_decode(bm.data_ptr(), cap, n, out.data_ptr(), 0, None) == 0
         assert _lib.hccx_frame_status(None) == 2  # HCCX_ERR_CORRUPT_PAYLOAD
+
+
+@pytest.mark.parametrize("mode", ["smooth", "sparse"])
+def test_decompress_multislab(cuda, mode):
+    """Reference-format payloads large enough for several doubling slabs
+    (csrc/lossless.cu: 64 Mi stream bits per slab) and the F^64-anchored
+    chunk walk: the bare payload (no offsets) decodes to the input bit for
+    bit, and a truncated payload is reported, not mis-decoded."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2409_02423_b200 import _lib
+
+    n = 1 << 24 if mode == "smooth" else 1 << 23  # ~101 M / ~200 M stream bits
+    if mode == "smooth":
+        t = torch.arange(n, device="cuda", dtype=torch.float32)
+        x = ((torch.sin(t * 1e-4) * 1e-2) * 4096).round() / 4096
+    else:
+        g = torch.Generator(device="cuda").manual_seed(7)
+        x = torch.randn(n, device="cuda", generator=g) * (torch.rand(n, device="cuda", generator=g) < 0.1)
+    cap = int(_lib.hccx_lossless_max_bytes(n))
+    pay = torch.empty(cap, dtype=torch.uint8, device="cuda")
+    nb = C.c_uint64()
+    assert _lib.hccx_lossless_compress(x.data_ptr(), n, pay.data_ptr(), cap, C.byref(nb), None) == 0
+    assert 8 * nb.value > (64 << 20)  # more than one slab
+    y = torch.empty(n, device="cuda")
+    assert _lib.hccx_lossless_decompress(pay.data_ptr(), nb.value, n, y.data_ptr(), None) == 0
+    assert torch.equal(y.view(torch.int32), x.view(torch.int32))
+    # truncated: CorruptPayloadError (codec_serial.cpp:98-101)
+    assert _lib.hccx_lossless_decompress(pay.data_ptr(), nb.value // 2, n, y.data_ptr(), None) == 2
