@@ -2,6 +2,7 @@
 (HCCX_DEBUG knobs, HCCX_STEP_SEGS, ...), run under torchrun:
 
   AB="HCCX_DEBUG=0;HCCX_DEBUG=128" torchrun --nproc-per-node N tools/nvl_ab.py [n] [rounds]
+  (AB_RATE=R picks the rate, AB_CODEC=zfp the ZFP-mode codec)
 
 Each round times K back-to-back allreduces per variant (CUDA events, max
 over ranks); rank 0 prints the per-variant median ms and GB/s.
@@ -23,7 +24,8 @@ rank, p = dist.get_rank(), dist.get_world_size()
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 1 << 26
 rounds = int(sys.argv[2]) if len(sys.argv) > 2 else 5
 K = int(os.environ.get("AB_K", "10"))
-spec = CodecSpec.fixed_rate(int(os.environ.get("AB_RATE", "8")))
+spec = (CodecSpec.zfp_rate(int(os.environ.get("AB_RATE", "8"))) if os.environ.get("AB_CODEC") == "zfp"
+        else CodecSpec.fixed_rate(int(os.environ.get("AB_RATE", "8"))))
 variants = [v for v in os.environ.get("AB", "HCCX_DEBUG=0").split(";") if v]
 comm = D.NvlinkComm(n)
 x = torch.randn(n, device="cuda") * 1e-3
