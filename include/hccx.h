@@ -154,7 +154,9 @@ HCCX_API hccx_status_t hccx_lossless_decompress_host(const uint8_t* h_in, uint64
  * Neither call synchronises: sizes stay on the device.  frame_decode
  * validates the frame (as hcc::from_bytes) and the index against the
  * payload; a bad message -> HCCX_ERR_CORRUPT_PAYLOAD from hccx_frame_status.
- * fold != 0: d_out = d_out + value (the ring's accumulation). */
+ * fold != 0: d_out = d_out + value (the ring's accumulation).  The encoder's
+ * scratch is per device and host thread: one thread's encodes on one device
+ * must be stream-ordered (one stream, or events between streams). */
 HCCX_API uint64_t hccx_lossless_frame_max_bytes(uint64_t n);
 HCCX_API hccx_status_t hccx_lossless_frame_encode(const float* d_in, uint64_t n, uint8_t* d_msg, uint64_t capacity,
                                                   void* stream);
