@@ -323,6 +323,10 @@ struct StageGeom {
 #define HCCX_UNIFORM_STAGES 0
 #endif
 constexpr bool kFUniform = HCCX_UNIFORM_STAGES != 0;
+#ifndef HCCX_ROTATE
+#define HCCX_ROTATE 0
+#endif
+constexpr bool kFRotate = HCCX_ROTATE != 0;
 
 template <class Codec>
 __device__ __forceinline__ StageGeom stage_geom(int kind) {
@@ -594,13 +598,18 @@ __device__ __forceinline__ void ring_fused_body(const FusedParams& P, const uint
   const uint32_t nseg = static_cast<uint32_t>((ngroups + kSegGroups - 1) / kSegGroups);
   const uint64_t GB = Codec::kGroupBytes;
   const uint64_t wire = Codec::wire_bytes(c);
-  const uint32_t myseg = nseg > cta ? (nseg - cta + G - 1) / G : 0;
+  // Segment set of this CTA: set, set + G, ... (acks and credits are per
+  // set).  HCCX_ROTATE: the set index is rotated by rank, so a segment's
+  // chain around the ring passes through different CTA indices (SMs) on
+  // different ranks instead of CTA b everywhere.
+  const uint32_t set = kFRotate ? (cta + static_cast<uint32_t>(j) * ((G + p - 1) / p)) % G : cta;
+  const uint32_t myseg = nseg > set ? (nseg - set + G - 1) / G : 0;
   const int nph = nphases(P);
   // TMA needs whole 16B-multiple segments at 16B-aligned addresses: word
   // codecs with 32B-aligned fp32 chunks (payload segments are 8*GB bytes,
   // a multiple of 16, at 256B-aligned slot offsets).
   const bool tma_ok = Codec::kFastPath && P.vec_ok;
-  auto seg_of = [&](uint32_t k) { return cta + k * G; };
+  auto seg_of = [&](uint32_t k) { return set + k * G; };
   auto seg_full = [&](uint32_t sg) { return (static_cast<uint64_t>(sg) + 1) * kSegVals <= c; };
   // Step boundaries within a phase: a short first step (P.first_segs) so the
   // neighbour's next phase can start early, then P.step_segs per step.
@@ -776,7 +785,7 @@ __device__ __forceinline__ void ring_fused_body(const FusedParams& P, const uint
           if (all) {
             for (uint32_t k = lane; k < P.ack_span; k += 32) spin_ge(P, fl + k, need, 0x900u | (ph << 4) | f.credit_cls);
           } else if (lane == 0) {
-            spin_ge(P, fl + cta, need, 0x800u | (ph << 4) | f.credit_cls);
+            spin_ge(P, fl + set, need, 0x800u | (ph << 4) | f.credit_cls);
           }
         }
       }
@@ -944,7 +953,7 @@ __device__ __forceinline__ void ring_fused_body(const FusedParams& P, const uint
       if (f.ack_rank >= 0) {
         const uint64_t ta = prof_clock();
         need(++events);
-        for (uint32_t kk = cta + lane * G; kk < kAckIdx; kk += G * 32) {
+        for (uint32_t kk = set + lane * G; kk < kAckIdx; kk += G * 32) {
           st_relaxed_sys(flag_ptr(P, f.ack_rank, f.ack_cls, f.ack_slot, 0) + kk, f.ack_ep);
           if (f.ack2_rank >= 0) st_relaxed_sys(flag_ptr(P, f.ack2_rank, f.ack2_cls, f.ack2_slot, 0) + kk, f.ack_ep);
         }
