@@ -202,6 +202,31 @@ def cpu_allreduce(x, rate: int, reps: int):
     return sorted(times)[len(times) // 2], kind
 
 
+def pinned_local(device: int, shapes):
+    """Pinned host buffers for the e2e copies, allocated while this process
+    runs on the CPUs NVML reports as local to `device`, so their pages sit on
+    the GPU's own NUMA node (first touch); the previous CPU affinity is
+    restored afterwards (the CPU baseline keeps every host thread).
+    shapes: [(numel, dtype)].  Returns (buffers, note)."""
+    import torch
+
+    before = os.sched_getaffinity(0)
+    note = "pinned pages allocated on the launching CPUs"
+    try:
+        import pynvml
+
+        pynvml.nvmlInit()
+        pynvml.nvmlDeviceSetCpuAffinity(pynvml.nvmlDeviceGetHandleByIndex(device))
+        note = f"pinned pages first-touched on gpu {device}'s NVML-local CPUs ({len(os.sched_getaffinity(0))})"
+    except Exception:
+        pass
+    try:
+        bufs = [torch.empty(k, dtype=dt, pin_memory=True) for k, dt in shapes]
+    finally:
+        os.sched_setaffinity(0, before)
+    return bufs, note
+
+
 def host_threads() -> int:
     try:
         return len(os.sched_getaffinity(0))
@@ -326,10 +351,8 @@ def bench_codec(args):
 
     # e2e: the reference-facing host-buffer API (hccx_compress_host /
     # hccx_decompress_host), pinned host buffers, copies inside the region.
-    hx = torch.empty(n, dtype=torch.float32, pin_memory=True)
+    (hx, hp, hy), numa_note = pinned_local(0, [(n, torch.float32), (W, torch.uint8), (n, torch.float32)])
     hx.copy_(torch.from_numpy(x0))
-    hp = torch.empty(W, dtype=torch.uint8, pin_memory=True)
-    hy = torch.empty(n, dtype=torch.float32, pin_memory=True)
     for _ in range(2):
         assert _lib.hccx_compress_host(codec, hx.data_ptr(), n, hp.data_ptr(), 0) == 0
         assert _lib.hccx_decompress_host(codec, hp.data_ptr(), W, n, hy.data_ptr(), 0) == 0
@@ -387,6 +410,7 @@ def bench_codec(args):
             "value": round(4 * n / e2e_s / 1e9, 3), "unit": "GB/s", "h2d_bytes_per_step": 4 * n + W,
             "d2h_bytes_per_step": W + 4 * n,
             "api": "hccx_compress_host + hccx_decompress_host (pinned host buffers)",
+            "host_buffers": numa_note,
             "timer": "host wall clock around the synchronous host-buffer API, device synced both sides",
         },
         "gpu_launches": int(launches),
@@ -507,9 +531,9 @@ def bench_allreduce(args):
     # Steps are software-pipelined over three streams with two buffer sets
     # (PCIe is full duplex: step k's result read overlaps step k+1's input
     # copy and allreduce); every copy of every step is inside the region.
-    hx = torch.empty(n, dtype=torch.float32, pin_memory=True)
+    (hx, hy0, hy1), numa_note = pinned_local(local, [(n, torch.float32)] * 3)
     hx.copy_(torch.from_numpy(x_host))
-    hy = [torch.empty(n, dtype=torch.float32, pin_memory=True) for _ in range(2)]
+    hy = [hy0, hy1]
     dx = [torch.empty_like(x), x]  # x is free again (its checks are done)
     dout = [out, torch.empty_like(x)]
     s_in, s_ar, s_out = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
@@ -604,6 +628,7 @@ def bench_allreduce(args):
             "e2e": {"value": round(4 * n / e2e_s / 1e9, 3), "unit": "GB/s", "h2d_bytes_per_step": 4 * n,
                     "d2h_bytes_per_step": 4 * n, "api": "hccx_allreduce (C ABI) with pinned host in/out",
                     "pipeline": "steps overlapped over 3 streams x 2 buffer sets (H2D | allreduce | D2H)",
+                    "host_buffers": numa_note,
                     "timer": "host wall clock, device synced both sides, max over ranks"},
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
