@@ -1140,10 +1140,24 @@ __global__ void __launch_bounds__(kEncThreads) ll_encode_kernel(const float* __r
     }
     const uint32_t fb = chunk_bits >= 32u * live ? 1u : 0u;
     const uint64_t size = fb ? 4ull * live : (chunk_bits + 7) / 8;
+    // the size is known: publish it now, so successors' look-backs see it
+    // while this chunk is still being coded
+    if (tid == 0) st_relaxed_gpu_u64(desc + c, desc_make(epoch, c == 0 ? 2u : 1u, fb, c == 0 ? flag_bytes + size : size));
     if (!fb) {
       const uint32_t words = (chunk_bits + 31) / 32;
       for (uint32_t w = tid; w < words; w += kEncThreads) sm[w] = 0;
       __syncthreads();
+    }
+    // warp 0 looks back (and publishes the inclusive prefix) while the other
+    // warps write their codes; then it writes its own
+    if (warp == 0) {
+      const uint64_t off = c == 0 ? flag_bytes : lookback(desc, c, epoch, flag_bytes, lane);
+      if (lane == 0) {
+        if (c != 0) st_relaxed_gpu_u64(desc + c, desc_make(epoch, 2u, fb, off + size));
+        bcast[1] = off;
+      }
+    }
+    if (!fb) {
       const uint32_t pos = wbase + incl - bits;
       uint64_t acc = 0;
       uint32_t fill = pos & 31, wi = pos >> 5;
@@ -1171,15 +1185,6 @@ __global__ void __launch_bounds__(kEncThreads) ll_encode_kernel(const float* __r
         }
       }
       if (fill > 0 && bits) atomicOr(&sm[wi], static_cast<uint32_t>(acc));  // may be shared with the next thread
-    }
-    // publish, look back, publish the inclusive prefix
-    if (warp == 0) {
-      if (lane == 0) st_relaxed_gpu_u64(desc + c, desc_make(epoch, c == 0 ? 2u : 1u, fb, c == 0 ? flag_bytes + size : size));
-      const uint64_t off = c == 0 ? flag_bytes : lookback(desc, c, epoch, flag_bytes, lane);
-      if (lane == 0) {
-        if (c != 0) st_relaxed_gpu_u64(desc + c, desc_make(epoch, 2u, fb, off + size));
-        bcast[1] = off;
-      }
     }
     __syncthreads();
     const uint64_t off = bcast[1];
