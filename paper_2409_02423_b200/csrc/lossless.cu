@@ -1233,37 +1233,40 @@ __global__ void msg_copy_kernel(const uint8_t* __restrict__ src, MsgDsts D, uint
 }
 
 // ---- decoder -----------------------------------------------------------------
-// One warp per chunk.  The chunk's bytes (and, folding, the accumulator's
-// 16 KiB) are staged into shared memory by bulk copies (TMA engine); raw
-// chunks are written from there; coded chunks are decoded by 32 lanes from
-// their indexed bit positions (128 codes each) into lane-major shared memory,
-// the lanes' XOR carries are scanned (x_i = x_{i-1} ^ r_i within a chunk),
-// the warp assembles the chunk (+ accumulator) contiguously and one bulk
-// store writes it out.  Unaligned outputs take plain loads and stores.
-constexpr int kDecWarps = 2;
+// One CTA (4 warps) per chunk.  The chunk's bytes (and, folding, the
+// accumulator's 16 KiB) are staged into shared memory by bulk copies (TMA
+// engine).  Coded chunks: warp 0's 32 lanes decode the chunk as 64
+// independent 64-code chains from their indexed bit positions into lane-major
+// shared memory and scan the lanes' XOR carries (x_i = x_{i-1} ^ r_i within a
+// chunk); then all four warps assemble the chunk (+ accumulator)
+// contiguously, and one bulk store writes it out.  Raw chunks are assembled
+// by all warps straight from the staged bytes.  Unaligned outputs take plain
+// loads and stores.
+constexpr int kDecThreads = 128;
 constexpr uint32_t kDecInWords = kChunk + 12;       // 16 KiB + alignment head/tail
 constexpr uint32_t kMsgLaneStride = kLaneVals + 1;  // 129: conflict-free lane-major staging
-constexpr uint32_t kDecWarpWords = kDecInWords + 32 * kMsgLaneStride + kChunk + 64 + 4;
-constexpr size_t kMsgDecodeSmem = sizeof(uint32_t) * kDecWarps * kDecWarpWords;
-static_assert(kDecWarpWords % 4 == 0, "16-byte aligned per-warp regions");
+constexpr uint32_t kDecWords = kDecInWords + 32 * kMsgLaneStride + kChunk + 64 + 8;
+constexpr size_t kMsgDecodeSmem = sizeof(uint32_t) * kDecWords;
+static_assert(kDecInWords % 4 == 0 && (32 * kMsgLaneStride) % 4 == 0, "16-byte aligned regions");
 
-__global__ void __launch_bounds__(kDecWarps * 32) msg_decode_kernel(const uint8_t* __restrict__ msg, uint64_t msg_cap,
-                                                                    uint64_t n, uint64_t nch, uint64_t idx_bytes,
-                                                                    float* __restrict__ out, int fold,
-                                                                    uint32_t* __restrict__ err,
-                                                                    unsigned long long* recv_acct) {
+__global__ void __launch_bounds__(kDecThreads) msg_decode_kernel(const uint8_t* __restrict__ msg, uint64_t msg_cap,
+                                                                 uint64_t n, uint64_t nch, uint64_t idx_bytes,
+                                                                 float* __restrict__ out, int fold,
+                                                                 uint32_t* __restrict__ err,
+                                                                 unsigned long long* recv_acct) {
   extern __shared__ __align__(16) uint32_t msm[];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint32_t* ins = msm + warp * kDecWarpWords;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  uint32_t* ins = msm;
   uint32_t* sm = ins + kDecInWords;            // lane-major decoded values
   uint32_t* io = sm + 32 * kMsgLaneStride;     // contiguous chunk: accumulator in, values out
-  uint32_t* carry = io + kChunk;
+  uint32_t* carry = io + kChunk;               // [64]: lane carries, chain-a totals
   uint64_t* bar = reinterpret_cast<uint64_t*>(carry + 64);
-  if (lane == 0) {
+  uint32_t* status = carry + 66;               // CTA-wide "bad chunk" flag
+  if (tid == 0) {
     mbar_init(bar, 1);
     fence_mbar_init();
   }
-  __syncwarp();
+  __syncthreads();
   uint32_t phase = 0;
   // frame checks (hcc::from_bytes, codec.cpp:101-121)
   const uint64_t container = *reinterpret_cast<const uint64_t*>(msg);
@@ -1273,18 +1276,16 @@ __global__ void __launch_bounds__(kDecWarps * 32) msg_decode_kernel(const uint8_
                         (ld_le64(msg + 22) & 0xffffffffull) == nch && container - 18 >= flag_bytes &&
                         kMsgHeaderBytes + idx_bytes + (container - 18) + 16 <= msg_cap;
   if (!frame_ok) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(err, kErrCorrupt);
+    if (blockIdx.x == 0 && tid == 0) atomicOr(err, kErrCorrupt);
     return;
   }
   const uint64_t payload = container - 18;
-  if (recv_acct && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(recv_acct, static_cast<unsigned long long>(payload));
+  if (recv_acct && blockIdx.x == 0 && tid == 0) atomicAdd(recv_acct, static_cast<unsigned long long>(payload));
   const uint32_t* idx = reinterpret_cast<const uint32_t*>(msg + kMsgHeaderBytes);
   const uint8_t* pay = msg + kMsgHeaderBytes + idx_bytes;
   uint32_t* o32 = reinterpret_cast<uint32_t*>(out);
   const bool out_al = (reinterpret_cast<uintptr_t>(out) & 15) == 0;
-  bool bad = false;
-  for (uint64_t c = static_cast<uint64_t>(blockIdx.x) * kDecWarps + warp; c < nch;
-       c += static_cast<uint64_t>(gridDim.x) * kDecWarps) {
+  for (uint64_t c = blockIdx.x; c < nch; c += gridDim.x) {
     const uint64_t base = c * kChunk;
     const uint32_t live = static_cast<uint32_t>(n - base < kChunk ? n - base : kChunk);
     const uint32_t* e = idx + kMsgIndexWords * c;
@@ -1292,99 +1293,102 @@ __global__ void __launch_bounds__(kDecWarps * 32) msg_decode_kernel(const uint8_
     const uint64_t end = c + 1 < nch ? idx[kMsgIndexWords * (c + 1)] : payload;
     const bool raw = (pay[c / 8] >> (c % 8)) & 1u;
     if (off < flag_bytes || end < off || end > payload || end - off > 4ull * live || (raw && end - off != 4ull * live)) {
-      bad = true;
-      break;
+      if (tid == 0) atomicOr(err, kErrCorrupt);
+      break;  // CTA-uniform
     }
     // stage [off & ~15, end) rounded up to 16 bytes, and the accumulator
     const uint64_t a0 = off & ~15ull;
     const uint32_t in_bytes = static_cast<uint32_t>((end - a0 + 15) & ~15ull);
     const uint32_t acc_bulk = fold && out_al ? (4 * live) & ~15u : 0u;
-    if (lane == 0) bulk_wait_read<0>();  // the previous chunk's store has read io
-    __syncwarp();
-    if (lane == 0) {
+    if (tid == 0) bulk_wait_read<0>();  // the previous chunk's store has read io
+    __syncthreads();
+    if (tid == 0) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       mbar_arrive_expect_tx(bar, in_bytes + acc_bulk);
       bulk_g2s(ins, pay + a0, in_bytes, bar);
       if (acc_bulk) bulk_g2s(io, out + base, acc_bulk, bar);
     }
     if (fold)
-      for (uint32_t k = acc_bulk / 4 + lane; k < live; k += 32) io[k] = o32[base + k];
+      for (uint32_t k = acc_bulk / 4 + tid; k < live; k += kDecThreads) io[k] = o32[base + k];
     mbar_wait(bar, phase);
     phase ^= 1;
     const uint32_t head = static_cast<uint32_t>(off - a0);  // bytes
     if (raw) {
-      for (uint32_t k = lane; k < live; k += 32) {
+      __syncthreads();  // the hand-loaded accumulator words
+      for (uint32_t k = tid; k < live; k += kDecThreads) {
         const uint32_t b = head + 4 * k;
         const uint32_t lo = ins[b >> 2];
         const uint32_t v = (b & 3) ? __funnelshift_r(lo, ins[(b >> 2) + 1], 8 * (b & 3)) : lo;
         io[k] = fold ? __float_as_uint(__fadd_rn(__uint_as_float(io[k]), __uint_as_float(v))) : v;
       }
     } else {
-      // lane l decodes values [128 l, 128 l + 128) as two independent
-      // chains (64-value blocks 2l and 2l+1, from their indexed offsets)
-      const uint32_t cw = e[1 + lane];
-      const uint32_t bits_a = cw & 0xffffu, bits_b = cw >> 16;
-      const uint32_t mybits = bits_a + bits_b;
-      uint32_t incl = mybits;
+      if (warp == 0) {
+        // lane l decodes values [128 l, 128 l + 128) as two independent
+        // chains (64-value blocks 2l and 2l+1, from their indexed offsets)
+        const uint32_t cw = e[1 + lane];
+        const uint32_t bits_a = cw & 0xffffu, bits_b = cw >> 16;
+        const uint32_t mybits = bits_a + bits_b;
+        uint32_t incl = mybits;
 #pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const uint32_t t = __shfl_up_sync(kFull, incl, d);
-        if (lane >= d) incl += t;
-      }
-      const uint32_t total = __shfl_sync(kFull, incl, 31);
-      if ((total + 7ull) / 8 != end - off) {
-        bad = true;
-        break;
-      }
-      const uint32_t i0 = lane * kLaneVals;
-      const uint32_t na = live > i0 ? min(live - i0, 64u) : 0u;
-      const uint32_t nb2 = live > i0 + 64 ? min(live - i0 - 64, 64u) : 0u;
-      uint32_t bit_a = 8 * head + (incl - mybits), bit_b = bit_a + bits_a;  // within the staged bytes
-      const uint32_t a0 = bit_a, b0 = bit_b;
-      uint32_t pa = 0, pb = 0;
-      uint32_t* row = sm + lane * kMsgLaneStride;
-      // one code at `bit` from the staged words: (bits consumed, low value)
-      auto code_at = [&](uint32_t bit, uint32_t& low) {
-        const uint32_t w = bit >> 5, sh = bit & 31;
-        const uint32_t x0 = ins[w], x1 = ins[w + 1], x2 = ins[w + 2];
-        const uint32_t lo = __funnelshift_r(x0, x1, sh), hi = __funnelshift_r(x1, x2, sh);
-        const uint32_t nb = 32 - (lo & 31u);
-        const uint32_t v = __funnelshift_r(lo, hi, 5);  // the 32 bits after the length field
-        low = nb >= 32 ? v : (v & ((1u << nb) - 1u));
-        return 5 + nb;
-      };
-      for (uint32_t i = 0; i < 64; ++i) {
-        if (i < na) {
-          uint32_t low;
-          bit_a += code_at(bit_a, low);
-          pa ^= low;
-          row[i] = pa;
+        for (int d = 1; d < 32; d <<= 1) {
+          const uint32_t t = __shfl_up_sync(kFull, incl, d);
+          if (lane >= d) incl += t;
         }
-        if (i < nb2) {
-          uint32_t low;
-          bit_b += code_at(bit_b, low);
-          pb ^= low;
-          row[64 + i] = pb;
-        }
-      }
-      const bool lane_bad = bit_a - a0 != bits_a || bit_b - b0 != bits_b;
-      // chain b continues chain a; then an exclusive XOR scan of the lanes'
-      // totals gives each lane its carry (x_i = x_{i-1} ^ r_i within a chunk)
-      const uint32_t tot = pa ^ pb;
-      uint32_t x = tot;
+        const uint32_t total = __shfl_sync(kFull, incl, 31);
+        bool bad = (total + 7ull) / 8 != end - off;
+        if (!bad) {
+          const uint32_t i0 = lane * kLaneVals;
+          const uint32_t na = live > i0 ? min(live - i0, 64u) : 0u;
+          const uint32_t nb2 = live > i0 + 64 ? min(live - i0 - 64, 64u) : 0u;
+          uint32_t bit_a = 8 * head + (incl - mybits), bit_b = bit_a + bits_a;  // within the staged bytes
+          const uint32_t a0b = bit_a, b0b = bit_b;
+          uint32_t pa = 0, pb = 0;
+          uint32_t* row = sm + lane * kMsgLaneStride;
+          auto code_at = [&](uint32_t bit, uint32_t& low) {
+            const uint32_t w = bit >> 5, sh = bit & 31;
+            const uint32_t x0 = ins[w], x1 = ins[w + 1], x2 = ins[w + 2];
+            const uint32_t lo = __funnelshift_r(x0, x1, sh), hi = __funnelshift_r(x1, x2, sh);
+            const uint32_t nb = 32 - (lo & 31u);
+            const uint32_t v = __funnelshift_r(lo, hi, 5);  // the 32 bits after the length field
+            low = nb >= 32 ? v : (v & ((1u << nb) - 1u));
+            return 5 + nb;
+          };
+          for (uint32_t i = 0; i < 64; ++i) {
+            if (i < na) {
+              uint32_t low;
+              bit_a += code_at(bit_a, low);
+              pa ^= low;
+              row[i] = pa;
+            }
+            if (i < nb2) {
+              uint32_t low;
+              bit_b += code_at(bit_b, low);
+              pb ^= low;
+              row[64 + i] = pb;
+            }
+          }
+          bad = bit_a - a0b != bits_a || bit_b - b0b != bits_b;
+          // chain b continues chain a; an exclusive XOR scan of the lanes'
+          // totals gives each lane its carry
+          const uint32_t tot = pa ^ pb;
+          uint32_t x = tot;
 #pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const uint32_t t = __shfl_up_sync(kFull, x, d);
-        if (lane >= d) x ^= t;
+          for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t t = __shfl_up_sync(kFull, x, d);
+            if (lane >= d) x ^= t;
+          }
+          carry[lane] = x ^ tot;
+          carry[32 + lane] = pa;
+        }
+        const bool any_bad = __any_sync(kFull, bad);
+        if (lane == 0) status[0] = any_bad ? 1u : 0u;
       }
-      carry[lane] = x ^ tot;
-      carry[32 + lane] = pa;
-      if (__any_sync(kFull, lane_bad)) {
-        bad = true;
-        break;
+      __syncthreads();
+      if (status[0]) {
+        if (tid == 0) atomicOr(err, kErrCorrupt);
+        break;  // CTA-uniform
       }
-      __syncwarp();
-      for (uint32_t k = lane; k < live; k += 32) {
+      for (uint32_t k = tid; k < live; k += kDecThreads) {
         const uint32_t l = k >> 7;
         const uint32_t v = sm[l * kMsgLaneStride + (k & 127)] ^ carry[l] ^ ((k & 64) ? carry[32 + l] : 0u);
         io[k] = fold ? __float_as_uint(__fadd_rn(__uint_as_float(io[k]), __uint_as_float(v))) : v;
@@ -1392,16 +1396,15 @@ __global__ void __launch_bounds__(kDecWarps * 32) msg_decode_kernel(const uint8_
     }
     // write the chunk: one bulk store of the aligned 16-byte multiple, the rest by hand
     const uint32_t st_bulk = out_al ? (4 * live) & ~15u : 0u;
-    for (uint32_t k = st_bulk / 4 + lane; k < live; k += 32) o32[base + k] = io[k];
+    for (uint32_t k = st_bulk / 4 + tid; k < live; k += kDecThreads) o32[base + k] = io[k];
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    __syncwarp();
-    if (lane == 0 && st_bulk) {
+    __syncthreads();
+    if (tid == 0 && st_bulk) {
       bulk_s2g(out + base, io, st_bulk);
       bulk_commit();
     }
   }
-  if (lane == 0) bulk_wait_all();
-  if (bad && lane == 0) atomicOr(err, kErrCorrupt);
+  if (tid == 0) bulk_wait_all();
 }
 
 int resident_grid(const void* k, int threads, size_t smem, uint64_t want) {
@@ -1490,9 +1493,9 @@ hccx_status_t msg_decode(const uint8_t* msg, uint64_t msg_cap, uint64_t n, float
   const uint64_t nch = msg_chunks(n);
   const void* k = reinterpret_cast<const void*>(&msg_decode_kernel);
   smem_attr(k, kMsgDecodeSmem, g_decode_attr);
-  const int grid = resident_grid(k, kDecWarps * 32, kMsgDecodeSmem, (nch + kDecWarps - 1) / kDecWarps);
-  msg_decode_kernel<<<grid, kDecWarps * 32, kMsgDecodeSmem, st>>>(msg, msg_cap, n, nch, msg_index_bytes(n), out,
-                                                                  fold ? 1 : 0, err, recv_acct);
+  const int grid = resident_grid(k, kDecThreads, kMsgDecodeSmem, nch);
+  msg_decode_kernel<<<grid, kDecThreads, kMsgDecodeSmem, st>>>(msg, msg_cap, n, nch, msg_index_bytes(n), out,
+                                                               fold ? 1 : 0, err, recv_acct);
   count_launch();
   return HCCX_STATUS(cudaGetLastError());
 }
